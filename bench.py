@@ -1,0 +1,399 @@
+#!/usr/bin/env python3
+"""bench.py — frames/s of the change-based scene-labeling net on B200.
+
+Workload (BASELINE.json configs[1]): the paper's scene-labeling net
+(make_seg7_spec layer list, io.cpp:568-617, derived dims) at 640x480, weights
+fill_random_weights(seed 1), tau = 0.05 on every conv layer, S independent
+camera streams per GPU; stream g (global id) is gen_synthetic{seed 1000+g,
+n_objects, object_size, velocity} (io.cpp:499-552). A "step" = one frame of
+every stream on this GPU through the whole per-frame hot path
+(detect -> dilate/compact -> gather+tcgen05 GEMM+scatter -> CB max-pool, 18
+kernels in one CUDA graph). The bootstrap frame is excluded.
+
+  value : whole-job frames/s, frames already resident in HBM (zero-copy ingest)
+  e2e   : same metric through the public C ABI with HOST frames (pinned), the
+          H2D copy of each step's frames and the D2H copy of each step's result
+          (last node's retained output, all streams) inside the timed region
+  roofline : dominant kernel, algorithmic bytes/flops per launch / CUDA-event
+          duration (instrumented pass on the same sequence)
+  cpu_baseline : the unmodified reference (oracle/_ref/ref_bench, one CBNetwork
+          per host thread), rank 0 at N=1, bounded sample
+
+Multi-GPU: one process per GPU (torchrun), streams sharded by rank, no data-path
+collective; barrier + max-over-ranks of the device time ("scaling": "weak").
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/s per B200 vs changed-pixel % (scene-labeling net); % HBM/TC roofline"
+REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--streams", type=int, default=16, help="camera streams per GPU")
+    ap.add_argument("--height", type=int, default=480)
+    ap.add_argument("--width", type=int, default=640)
+    ap.add_argument("--objects", type=int, default=6)
+    ap.add_argument("--object-size", type=int, default=40)
+    ap.add_argument("--velocity", type=int, default=4)
+    ap.add_argument("--noise", type=float, default=0.0)
+    ap.add_argument("--tau", type=float, default=0.05)
+    ap.add_argument("--profile-steps", type=int, default=5, help="instrumented steps for the roofline")
+    ap.add_argument("--dense-steps", type=int, default=5, help="steps of the dense (full-update) path")
+    ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU-baseline work")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def config_dict(a, world):
+    return {"workload": f"scene-labeling net (seg7 layers, derived dims) {a.width}x{a.height}, "
+                        f"{a.streams} streams/GPU, gen_synthetic {a.objects}x{a.object_size}px objects "
+                        f"v={a.velocity} noise={a.noise}, tau={a.tau}",
+            "height": a.height, "width": a.width, "streams_per_gpu": a.streams,
+            "total_streams": a.streams * world, "objects": a.objects, "object_size": a.object_size,
+            "velocity": a.velocity, "noise_std": a.noise, "tau": a.tau,
+            "parallelism": f"streams sharded over {world} GPU(s), no collective",
+            "l2": "inputs larger than L2 (frame ring + per-stream state >> 126 MB)"}
+
+
+# ---------------------------------------------------------------------------
+# CPU reference (oracle/_ref/ref_bench = the unmodified reference build)
+# ---------------------------------------------------------------------------
+def run_ref_bench(a, threads, frames, budget, streams=None):
+    if not os.path.exists(REF_BENCH):
+        return None
+    streams = streams or threads
+    cmd = [REF_BENCH, "--height", str(a.height), "--width", str(a.width), "--streams", str(streams),
+           "--threads", str(threads), "--frames", str(frames), "--objects", str(a.objects),
+           "--object-size", str(a.object_size), "--velocity", str(a.velocity), "--noise", str(a.noise),
+           "--tau", str(a.tau), "--time-budget", str(budget)]
+    out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
+    return json.loads(out.strip().splitlines()[-1])
+
+
+def reference_arm(a, rank, world):
+    if rank != 0:
+        return
+    threads = os.cpu_count() or 1
+    base = {"metric": METRIC, "unit": "frames/s", "impl": "reference", "n_gpus": a.gpus, "steps": a.steps,
+            "warmup": a.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic (gen_synthetic, seeded)", "config": config_dict(a, world)}
+    if not os.path.exists(REF_BENCH):
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_bench not built"}))
+        return
+    # each step = one frame of every host-thread stream; bootstrap excluded
+    r = run_ref_bench(a, threads, max(1, a.steps), budget=max(10.0, a.cpu_budget * 3))
+    sample = (f"{r['frames']} post-bootstrap frames over {r['streams']} streams ({threads} threads), "
+              f"L1 change {100 * r['l1_change_frac']:.2f}%")
+    base.update({"value": r["fps"], "ms_per_step": 1000.0 * r["seconds"] / max(1, r["frames"]) * threads,
+                 "cpu_baseline": {"value": r["fps"], "unit": "frames/s", "cores": threads, "kind": "reference",
+                                  "sample": sample},
+                 "e2e": {"value": r["fps"], "unit": "frames/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}})
+    print(json.dumps(base))
+
+
+# ---------------------------------------------------------------------------
+# clocks
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+# ---------------------------------------------------------------------------
+# algorithmic work per kernel
+# ---------------------------------------------------------------------------
+def kernel_work(node, kernel, n_out, n_up, S_counts):
+    """Algorithmic (bytes, flops) of one launch, summed over the streams.
+    n_out/n_up: per-stream lists of this node's / its producer's changed pixels."""
+    kind, name, cin, hin, win, cout, hout, wout, k, ops_pp = node
+    b = f = 0.0
+    for s in range(S_counts):
+        no = n_out[s]
+        nu = n_up[s] if n_up is not None else None
+        if kernel == "detect":
+            if nu is None:  # dense scan of the network input: read x and state
+                b += 8.0 * cin * hin * win
+            else:           # sparse: x and state at the producer's update set
+                b += 8.0 * cin * nu
+        elif kernel == "dilcomp":
+            b += hin * win / 8.0 + hout * wout / 8.0 + 4.0 * no + 4
+        elif kernel == "gemm":
+            f += ops_pp * no
+            # gather lower bound (each changed pixel's own receptive-field centre),
+            # weights once, scatter of the Cout vector
+            b += 4.0 * cin * no + 4.0 * cout * no + (4.0 * cout * cin * k * k if s == 0 else 0.0)
+        elif kernel == "pool":
+            b += 4.0 * cin * 4 * no + 4.0 * cin * no
+    return b, f
+
+
+def main():
+    a = parse()
+    rank, world, local = dist_env()
+    if a.impl == "reference":
+        reference_arm(a, rank, world)
+        return
+
+    import numpy as np
+    import torch
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1808_05488_b200 import cbi
+
+    peaks = {"hbm_gbs": 6538.6, "bf16_tflops": 1661.9, "bf16_tflops_sustained": 1399.9, "source": "fallback"}
+    pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(pk_path):
+        with open(pk_path) as fh:
+            peaks.update(json.load(fh))
+        peaks["source"] = "measured (MEASURED_PEAKS.json)"
+
+    S, H, W = a.streams, a.height, a.width
+    ctx = cbi.Context(local)
+    spec = cbi.make_seg_spec(1, H, W)
+    taus = [a.tau] * 5
+    n_frames = 1 + a.warmup + a.steps + a.profile_steps + a.dense_steps
+    # frame ring [T][S][C][H][W], pinned on the host and resident in HBM
+    host = torch.empty((n_frames, S, 3, H, W), dtype=torch.float32, pin_memory=True)
+    hnp = host.numpy()
+    for s in range(S):
+        g = rank * S + s
+        hnp[:, s] = cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, n_frames, a.objects, a.object_size, a.velocity,
+                                                          a.velocity, a.noise, 1000 + g))
+    dev = host.to(f"cuda:{local}")
+    torch.cuda.synchronize()
+    frame_bytes = S * 3 * H * W * 4
+
+    def barrier():
+        if world > 1:
+            torch.distributed.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        return float(t.item())
+
+    ext = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
+    net = cbi.convert_to_cb(spec, taus, n_streams=S, ctx=ctx)
+    n_slots, node_slot = net.count_layout()
+    nodes = net.nodes()
+    counts_pinned = torch.empty((a.steps + 1, n_slots, S), dtype=torch.int32, pin_memory=True)
+
+    def dptr(t):
+        return dev[t].data_ptr()
+
+    # ---- value: frames resident in HBM ---------------------------------------
+    net.enqueue_device(dptr(0))  # bootstrap (untimed)
+    for t in range(1, 1 + a.warmup):
+        net.enqueue_device(dptr(t))
+    ctx.synchronize()
+    barrier()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clocks:
+        torch.cuda.synchronize()
+        t0.record(ext)
+        for k in range(a.steps):
+            net.enqueue_device(dptr(1 + a.warmup + k))
+            net.copy_counts_async(counts_pinned[k].data_ptr())
+        t1.record(ext)
+        t1.synchronize()
+        torch.cuda.synchronize()
+    ms = max_over_ranks(t0.elapsed_time(t1))
+    barrier()
+    launches = net.last_launches()
+    cnt = counts_pinned[:a.steps].numpy()
+    l1_px = nodes[0].out_shape[1] * nodes[0].out_shape[2]
+    l1_frac = float(cnt[:, node_slot[0], :].mean()) / l1_px
+    per_layer = {n.name: float(cnt[:, node_slot[i], :].mean()) / (n.out_shape[1] * n.out_shape[2])
+                 for i, n in enumerate(nodes)}
+    value = S * world * a.steps / (ms / 1000.0)
+
+    # ---- roofline: instrumented pass (per-kernel CUDA events) -----------------
+    net.set_kernel_timing(True)
+    work = {}
+    base_t = 1 + a.warmup + a.steps
+    prof_counts = torch.empty((n_slots, S), dtype=torch.int32, pin_memory=True)
+    for k in range(a.profile_steps):
+        net.enqueue_device(dptr(base_t + k))
+        net.copy_counts_async(prof_counts.data_ptr())
+        ctx.synchronize()
+        c = prof_counts.numpy()
+        for i, n in enumerate(nodes):
+            src = n.inputs[0] if n.inputs else -1
+            cin, hin, win = n.in_shape
+            cout, hout, wout = n.out_shape
+            kk = 0
+            if n.kind == cbi.LayerKind.Conv:
+                kk = int(round((n.ops_per_pixel / (2 * cout * max(1, cin))) ** 0.5))
+            desc = (n.kind, n.name, cin, hin, win, cout, hout, wout, kk, n.ops_per_pixel)
+            n_out = c[node_slot[i]]
+            n_up = c[node_slot[src]] if src >= 0 else None
+            for kern in ("detect", "dilcomp", "gemm", "pool"):
+                bb, ff = kernel_work(desc, kern, n_out, n_up, S)
+                wsum = work.setdefault(f"{n.name}.{kern}", [0.0, 0.0])
+                wsum[0] += bb
+                wsum[1] += ff
+    rep = net.timing_report()
+    net.set_kernel_timing(False)
+    hbm = peaks["hbm_gbs"] * 1e9
+    tf32 = peaks["bf16_tflops"] * 1e12 / 2  # tf32 dense = half the measured bf16 rate
+    kernels = []
+    for label, (tot_ms, nl) in rep["kernels"].items():
+        bb, ff = work.get(label, [0.0, 0.0])
+        t = tot_ms / 1000.0
+        t_roof = max(bb / hbm, ff / tf32)
+        kernels.append({"kernel": label, "ms_per_launch": tot_ms / max(1, nl), "share": 0.0,
+                        "bytes_per_launch": bb / max(1, nl), "flops_per_launch": ff / max(1, nl),
+                        "roofline_frac": (t_roof / t) if t > 0 else None,
+                        "bound": "tensor" if ff / tf32 > bb / hbm else "hbm"})
+    tot = sum(k["ms_per_launch"] for k in kernels) or 1.0
+    for k in kernels:
+        k["share"] = k["ms_per_launch"] / tot
+    kernels.sort(key=lambda k: -k["ms_per_launch"])
+    dom = kernels[0]
+    if dom["bound"] == "tensor":
+        achieved = dom["flops_per_launch"] / (dom["ms_per_launch"] / 1000.0) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tf32 / 1e12, "unit": "TFLOP/s",
+                "frac": achieved / (tf32 / 1e12)}
+    else:
+        achieved = dom["bytes_per_launch"] / (dom["ms_per_launch"] / 1000.0) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                "frac": achieved / peaks["hbm_gbs"]}
+    roof.update({"kernel": dom["kernel"], "traffic": None, "peak_source": peaks["source"],
+                 "step_roofline_frac": (sum(max(k["bytes_per_launch"] / hbm, k["flops_per_launch"] / tf32)
+                                            for k in kernels) / (tot / 1000.0)),
+                 "top_kernels": kernels[:6]})
+
+    # ---- dense path (same kernels, every frame a full update) -------------------
+    dense_fps = None
+    if a.dense_steps > 0:
+        dnet = cbi.convert_to_cb(spec, taus, n_streams=S, ctx=ctx)
+        dnet.set_dense(True)
+        dbase = 1 + a.warmup + a.steps + a.profile_steps
+        dnet.enqueue_device(dptr(0))
+        dnet.enqueue_device(dptr(1))
+        ctx.synchronize()
+        t0.record(ext)
+        for k in range(a.dense_steps):
+            dnet.enqueue_device(dptr(dbase + k))
+        t1.record(ext)
+        t1.synchronize()
+        dms = max_over_ranks(t0.elapsed_time(t1))
+        dense_fps = S * world * a.dense_steps / (dms / 1000.0)
+        del dnet
+
+    # ---- e2e: host frames through the C ABI, H2D + D2H in the timed region -------
+    e2e = None
+    if not a.no_e2e:
+        enet = cbi.convert_to_cb(spec, taus, n_streams=S, ctx=ctx)
+        out_bytes = enet.output_bytes(-1)
+        out_host = torch.empty(out_bytes // 4, dtype=torch.float32, pin_memory=True)
+        enet.enqueue(hnp[0])
+        for t in range(1, 1 + a.warmup):
+            enet.enqueue(hnp[t])
+        ctx.synchronize()
+        barrier()
+        t0.record(ext)
+        for k in range(a.steps):
+            enet.enqueue(hnp[1 + a.warmup + k])
+            enet.copy_output_async(out_host.data_ptr())
+        t1.record(ext)
+        t1.synchronize()
+        ems = max_over_ranks(t0.elapsed_time(t1))
+        e2e = {"value": S * world * a.steps / (ems / 1000.0), "unit": "frames/s",
+               "h2d_bytes_per_step": frame_bytes, "d2h_bytes_per_step": out_bytes,
+               "ms_per_step": ems / a.steps}
+        del enet
+
+    # ---- CPU baseline (rank 0, N=1) ---------------------------------------------
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        r = run_ref_bench(a, threads, frames=3, budget=a.cpu_budget)
+        if r:
+            cpu = {"value": r["fps"], "unit": "frames/s", "cores": threads, "kind": "reference",
+                   "sample": f"oracle/_ref/ref_bench: {r['frames']} post-bootstrap frames of {r['streams']} "
+                             f"streams, one cbi::CBNetwork per thread, L1 change "
+                             f"{100 * r['l1_change_frac']:.2f}%"}
+
+    if rank == 0:
+        out = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
+               "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+               "vs_baseline": None, "dtype": "f32", "gemm_precision": "3xTF32 tcgen05 (fp32-accurate)",
+               "data": "synthetic (gen_synthetic, seeded; random-init He-uniform weights)",
+               "config": config_dict(a, world),
+               "change": {"l1_changed_frac": l1_frac, "per_layer_changed_frac": per_layer},
+               "dense_path_fps": dense_fps, "speedup_vs_dense": (value / dense_fps) if dense_fps else None,
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * a.steps,
+               "clocks": clocks.summary()}
+        print(json.dumps(out))
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

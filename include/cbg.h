@@ -1,0 +1,249 @@
+/*
+ * cbg.h — C ABI of the B200-native change-based inference (CBinfer) hot path.
+ *
+ * This is the drop-in boundary for the reference's layer/operator API
+ * (reference: /root/reference/proj, namespace cbi). Every entry point below
+ * replaces one reference interface; the citation names the reference
+ * file:line it mirrors. Plain pointers and sizes only: no C++ or torch types
+ * cross this boundary.
+ *
+ * Conventions
+ *  - Every function returns an int status: CBG_OK (0) or one of the error
+ *    categories below. The matching message is available from
+ *    cbg_last_error() (thread-local), and the C++ wrapper
+ *    (include/cbg/cbi_gpu.hpp) rethrows it as the matching cbi-style
+ *    exception: INVALID_INPUT -> InvalidInputError, CONFIG -> ConfigError
+ *    (reference: proj/include/cbi/common.hpp:11-21).
+ *  - Tensors crossing the boundary on the host side use the reference's
+ *    Tensor3 layout: channel-major, row-major planes, fp32
+ *    (reference: proj/include/cbi/tensor.hpp:13-35).
+ *  - Index lists cross as int32 (row, col) pairs in row-major order
+ *    (reference: PixelIndex/IndexList, tensor.hpp:38-44).
+ *  - All device work is enqueued on the context's CUDA stream. Only the
+ *    cbg_*_read_* functions and cbg_ctx_sync synchronise.
+ *  - A handle must be used by one host thread at a time (the reference's
+ *    layers are externally serialised as well). Distinct
+ *    handles may be used concurrently.
+ */
+#ifndef CBG_H_
+#define CBG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CBG_ABI_VERSION 1
+
+/* ---- status codes (reference error taxonomy, common.hpp:11-48) ---------- */
+enum {
+  CBG_OK = 0,
+  CBG_ERR_INVALID_INPUT = 1, /* cbi::InvalidInputError */
+  CBG_ERR_CONFIG = 2,        /* cbi::ConfigError */
+  CBG_ERR_CUDA = 3,          /* CUDA runtime / launch failure */
+  CBG_ERR_OOM = 4,           /* device allocation failure */
+  CBG_ERR_UNSUPPORTED = 5    /* no sm_100 device, or a shape the kernels do not cover */
+};
+
+/* ---- enums mirroring the reference ---------------------------------------- */
+/* LayerKind, network.hpp:10 */
+enum { CBG_LAYER_CONV = 0, CBG_LAYER_ACT = 1, CBG_LAYER_POOL = 2, CBG_LAYER_ADD = 3, CBG_LAYER_CONCAT = 4 };
+/* DetectionPolicy, layers.hpp:8 */
+enum { CBG_POLICY_DETECT = 0, CBG_POLICY_PROPAGATE = 1, CBG_POLICY_REUSE1X1 = 2 };
+/* DetectMode, change.hpp:34 */
+enum { CBG_MODE_FEEDFORWARD = 0, CBG_MODE_CLOSEDLOOP = 1 };
+
+/* forward flags (ConvForwardOptions, layers.hpp:21-25) */
+enum {
+  CBG_FWD_FORCE_FULL = 1u << 0,        /* force_full_update: bootstrap-style full recompute */
+  CBG_FWD_RECORD_WORST_CASE = 1u << 1, /* record_worst_case: also compute propagate_changes(up) */
+  CBG_FWD_INPUT_ON_DEVICE = 1u << 2    /* the frame pointer is a device pointer */
+};
+
+/* ---- descriptions --------------------------------------------------------- */
+/* ConvSpec, tensor.hpp:54-80. weights: [out][in][kh][kw] fp32, bias: [out]. */
+typedef struct cbg_conv_spec {
+  int in_channels, out_channels;
+  int kernel_h, kernel_w;
+  int stride, padding;
+  int out_h, out_w; /* 0 = derived floor formula; >0 pins (crop), tensor.hpp:49-53 */
+  const float* weights;
+  const float* bias;
+} cbg_conv_spec;
+
+/* LayerDesc, network.hpp:25-37 */
+typedef struct cbg_layer_desc {
+  int kind;                /* CBG_LAYER_* */
+  const char* name;        /* NULL or "" -> "L<i+1>" (network.cpp:14-16) */
+  int n_from;              /* 0 -> previous row (network input for row 0) */
+  const char* const* from; /* producer names; "input" = network input */
+  cbg_conv_spec conv;      /* CONV */
+  int fuse_relu;           /* CONV */
+  int pool_size, pool_stride, pool_out_h, pool_out_w; /* POOL (out dims 0 = floor formula) */
+} cbg_layer_desc;
+
+/* NetworkSpec, network.hpp:39-44 */
+typedef struct cbg_network_spec {
+  int in_channels, in_height, in_width;
+  int n_layers;
+  const cbg_layer_desc* layers;
+} cbg_network_spec;
+
+/* SyntheticConfig, io.hpp:47-58 */
+typedef struct cbg_synthetic_config {
+  int height, width, channels, n_frames;
+  int n_objects, object_size;
+  int velocity_y, velocity_x;
+  float noise_std;
+  uint32_t seed;
+} cbg_synthetic_config;
+
+/* Per-node static information (CBNode, network.hpp:129-137). */
+typedef struct cbg_node_info {
+  int kind;           /* CBG_LAYER_* (never ACT: absorbed) */
+  char name[64];
+  int n_inputs;
+  int inputs[8];      /* node ids, -1 = network input */
+  int out_channels, out_height, out_width;
+  int in_channels, in_height, in_width;
+  int policy;         /* conv only */
+  int fuse_relu;      /* conv only */
+  float tau;          /* conv only */
+  int64_t ops_per_pixel; /* conv only: 2*Cout*Cin*kh*kw (layers.hpp:65-67) */
+} cbg_node_info;
+
+/* LayerFrameStats subset (network.hpp:98-110), deterministic fields only. */
+typedef struct cbg_layer_stats {
+  int64_t changed_px;
+  int64_t total_px;
+  int64_t eff_ops;
+  int64_t propagated_px; /* -1 = not recorded */
+} cbg_layer_stats;
+
+typedef struct cbg_ctx_s* cbg_ctx;
+typedef struct cbg_net_s* cbg_net;
+typedef struct cbg_conv_s* cbg_conv;
+typedef struct cbg_pool_s* cbg_pool;
+
+/* ---- errors / library ------------------------------------------------------ */
+const char* cbg_last_error(void);
+int cbg_abi_version(void);
+/* 1 when a CUDA device of compute capability 10.x is visible. */
+int cbg_device_available(void);
+
+/* ---- context: one device + one CUDA stream -------------------------------- */
+int cbg_ctx_create(int device, cbg_ctx* out);
+void cbg_ctx_destroy(cbg_ctx ctx);
+int cbg_ctx_sync(cbg_ctx ctx);
+/* The context's cudaStream_t, for interop (returned as void*). */
+void* cbg_ctx_stream(cbg_ctx ctx);
+
+/* ---- host-side harness mirrors of the reference io.cpp (no device) -------- */
+/* gen_synthetic, io.cpp:499-552: frames_out holds n_frames*channels*height*width
+ * floats (CHW per frame); corners_out (nullable) n_frames*n_objects*2 ints. */
+int cbg_gen_synthetic(const cbg_synthetic_config* cfg, float* frames_out, int32_t* corners_out);
+/* fill_random_weights, io.cpp:554-566: conv rows in spec order; weights[i]
+ * and biases[i] are writable buffers for the i-th CONV row. */
+int cbg_fill_random_weights(const cbg_network_spec* spec, uint32_t seed, float* const* weights,
+                            float* const* biases);
+
+/* ---- network (CBNetwork, network.hpp:141-181) ----------------------------- */
+/* resolve() + convert_to_cb() validation only, no device (network.cpp:37-133,416-503). */
+int cbg_net_validate(const cbg_network_spec* spec, const float* taus, int n_taus,
+                     const int* policies /* nullable */, int mode);
+/* convert_to_cb(DenseNetwork(spec), taus, policies, mode) for n_streams
+ * independent camera streams (each one CBNetwork instance of the reference;
+ * they share the immutable weights and are processed in the same launches). */
+int cbg_net_create(cbg_ctx ctx, const cbg_network_spec* spec, const float* taus, int n_taus,
+                   const int* policies /* nullable */, int mode, int n_streams, cbg_net* out);
+void cbg_net_destroy(cbg_net net);
+/* Copying a CBNetwork yields independent streams (network.hpp:139-141). */
+int cbg_net_clone(cbg_net net, cbg_net* out);
+int cbg_net_node_count(cbg_net net, int* n_nodes);
+int cbg_net_stream_count(cbg_net net, int* n_streams);
+int cbg_net_node_info(cbg_net net, int node, cbg_node_info* info);
+/* forward_frame (network.cpp:309-414) for every stream at once: frames holds
+ * n_streams frames, CHW each. Host pointers are copied in on the ctx stream
+ * (pinned memory makes it asynchronous). Flags: CBG_FWD_*. */
+int cbg_net_forward(cbg_net net, const float* frames, unsigned flags);
+/* reset() (network.cpp:274-290); stream = -1 resets all streams. */
+int cbg_net_reset(cbg_net net, int stream);
+/* set_thresholds() / thresholds() (network.cpp:256-272). */
+int cbg_net_set_thresholds(cbg_net net, const float* taus, int n_taus);
+int cbg_net_thresholds(cbg_net net, float* taus, int n_taus);
+/* Dense path: every frame is a full update through the same kernels and
+ * GEMM precision (the implementation's own dense-conv baseline). */
+int cbg_net_set_dense(cbg_net net, int dense);
+
+/* ---- synchronising readers ----------------------------------------------- */
+/* Node retained output (node = -1 -> last node, network.cpp:307), CHW. */
+int cbg_net_read_output(cbg_net net, int node, int stream, float* out_chw);
+/* Detect-policy input state (InputState, change.hpp:30-32), CHW. */
+int cbg_net_read_state(cbg_net net, int node, int stream, float* out_chw);
+/* Last frame's output-frame change map (uint8 0/1, H*W) and index list. */
+int cbg_net_read_changes(cbg_net net, int node, int stream, uint8_t* map_out /* nullable */,
+                         int32_t* rowcol_out /* nullable, 2*count */, int64_t* count_out);
+/* Last frame's worst-case map (record_worst_case), conv nodes only. */
+int cbg_net_read_worst_case(cbg_net net, int node, int stream, uint8_t* map_out,
+                            int64_t* count_out);
+/* Per-node stats of the last frame, stats[node] for one stream. */
+int cbg_net_read_stats(cbg_net net, int stream, cbg_layer_stats* stats, int n_nodes);
+/* changed_px of every node and stream of the last frame: counts[node*S+s]. */
+int cbg_net_read_counts(cbg_net net, int64_t* counts);
+
+/* ---- standalone layers (CBConvLayer / CBPoolLayer, layers.hpp:45-91) ------- */
+/* CBConvLayer ctor, layers.cpp:33-53. */
+int cbg_conv_create(cbg_ctx ctx, const cbg_conv_spec* spec, float tau, int policy, int fuse_relu,
+                    int mode, int in_h, int in_w, cbg_conv* out);
+void cbg_conv_destroy(cbg_conv layer);
+int cbg_conv_out_dims(cbg_conv layer, int* out_h, int* out_w);
+/* CBConvLayer::forward, layers.cpp:55-131. x: host CHW [in_c][in_h][in_w];
+ * up_map: nullable host uint8 [in_h][in_w] (the UpstreamChange map);
+ * up_rowcol: nullable host int32 pairs (UpstreamChange indexes, in the
+ * upstream frame). eff_ops_out: nullable. Flags: CBG_FWD_FORCE_FULL,
+ * CBG_FWD_RECORD_WORST_CASE. */
+int cbg_conv_forward(cbg_conv layer, const float* x, const uint8_t* up_map,
+                     const int32_t* up_rowcol, int64_t up_count, unsigned flags,
+                     int64_t* eff_ops_out);
+int cbg_conv_read_output(cbg_conv layer, float* out_chw);
+int cbg_conv_read_state(cbg_conv layer, float* out_chw);
+int cbg_conv_read_changes(cbg_conv layer, uint8_t* map_out, int32_t* rowcol_out,
+                          int64_t* count_out);
+int cbg_conv_read_worst_case(cbg_conv layer, uint8_t* map_out, int64_t* count_out);
+int cbg_conv_set_tau(cbg_conv layer, float tau);
+
+/* CBPoolLayer ctor, layers.cpp:133-146. */
+int cbg_pool_create(cbg_ctx ctx, int size, int stride, int channels, int in_h, int in_w,
+                    int out_h, int out_w, cbg_pool* out);
+void cbg_pool_destroy(cbg_pool layer);
+/* CBPoolLayer::forward, layers.cpp:148-179. */
+int cbg_pool_forward(cbg_pool layer, const float* x, const uint8_t* up_map,
+                     const int32_t* up_rowcol, int64_t up_count, int force_full_update);
+int cbg_pool_read_output(cbg_pool layer, float* out_chw);
+int cbg_pool_read_changes(cbg_pool layer, uint8_t* map_out, int32_t* rowcol_out,
+                          int64_t* count_out);
+
+/* ---- instrumentation / async I/O (bench, profiling) ----------------------- */
+/* Kernel launches enqueued per cbg_net_forward (one frame of every stream). */
+int cbg_net_last_launches(cbg_net net, int* launches);
+/* Per-kernel CUDA-event timing: while enabled, forwards launch eagerly with an
+ * event pair around every kernel; the report is a JSON object
+ * {"frames": F, "kernels": {"<node>.<kernel>": [total_ms, launches], ...}}.
+ * Enabling (or disabling) clears the accumulators. */
+int cbg_net_set_kernel_timing(cbg_net net, int enabled);
+int cbg_net_timing_report(cbg_net net, char* buf, int len);
+/* Asynchronous D2H copy of a node's retained output in the device layout
+ * (NHWC fp32, channel stride round_up(C,4), all streams) on the ctx stream. */
+int cbg_net_copy_output_async(cbg_net net, int node, void* host_dst);
+int cbg_net_output_bytes(cbg_net net, int node, int64_t* bytes);
+/* Asynchronous D2H copy of the per-frame change counts [slot][n_streams]
+ * (int32) into host memory; node_slot (nullable) receives each node's slot. */
+int cbg_net_copy_counts_async(cbg_net net, int32_t* host_dst, int32_t* node_slot);
+int cbg_net_count_slots(cbg_net net, int* slots);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CBG_H_ */

@@ -1,0 +1,643 @@
+/*
+ * cbi_oracle.c — TEST INFRASTRUCTURE ONLY. Plain-C restatement of the reference
+ * CBinfer hot path; see cbi_oracle.h for scope and the pinning strategy.
+ *
+ * Reference files restated (all under /root/reference/proj):
+ *   src/tensor.cpp   derived_dim / output_height / validate   (:9-43)
+ *   src/change.cpp   detect_changes, dilate_window, propagate_changes,
+ *                    extract_indexes                           (:20-84)
+ *   src/dense.cpp    conv2d_dense, im2col, gemm, maxpool_to    (:8-145)
+ *   src/layers.cpp   update_output, CBConvLayer::forward,
+ *                    CBPoolLayer::forward                      (:10-179)
+ *   src/network.cpp  resolve, convert_to_cb, forward_frame,
+ *                    reset, set_thresholds                     (:37-503)
+ * Built with -ffp-contract=off so every fp32 multiply and add rounds separately,
+ * matching the reference's non-FMA SSE code at its own flags.
+ */
+#include "cbi_oracle.h"
+
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+static _Thread_local char g_err[512];
+
+static int fail(int code, const char* msg) {
+  snprintf(g_err, sizeof g_err, "%s", msg);
+  return code;
+}
+
+const char* cbo_last_error(void) { return g_err; }
+
+/* common.hpp:50-56 */
+static int floor_div(int a, int b) {
+  int q = a / b, r = a % b;
+  return (r != 0 && ((r < 0) != (b < 0))) ? q - 1 : q;
+}
+static int ceil_div(int a, int b) { return -floor_div(-a, b); }
+static int imax(int a, int b) { return a > b ? a : b; }
+static int imin(int a, int b) { return a < b ? a : b; }
+
+/* tensor.cpp:9-28 */
+int cbo_out_dim(int in_dim, int kernel, int stride, int padding, int pinned) {
+  if (pinned > 0) return pinned;
+  int v = (in_dim + 2 * padding - kernel) / stride + 1;
+  if (in_dim + 2 * padding - kernel < 0 || v < 1) return -1;
+  return v;
+}
+
+/* tensor.cpp:30-43 (size checks of weights/bias are the caller's contract) */
+static int validate_spec(const cbg_conv_spec* s) {
+  if (s->in_channels < 1 || s->out_channels < 1 || s->kernel_h < 1 || s->kernel_w < 1)
+    return fail(CBG_ERR_INVALID_INPUT, "conv spec: channel and kernel dims must be >= 1");
+  if (s->stride < 1) return fail(CBG_ERR_INVALID_INPUT, "conv spec: stride must be >= 1");
+  if (s->padding < 0) return fail(CBG_ERR_INVALID_INPUT, "conv spec: padding must be >= 0");
+  if (s->out_h < 0 || s->out_w < 0 || (s->out_h > 0) != (s->out_w > 0))
+    return fail(CBG_ERR_INVALID_INPUT, "conv spec: explicit output dims must both be set and >= 1");
+  return CBG_OK;
+}
+
+/* change.cpp:20-43 */
+int cbo_detect_changes(const float* x, float* state, int c, int h, int w, float tau, int mode,
+                       uint8_t* m) {
+  if (tau < 0.0f) return fail(CBG_ERR_INVALID_INPUT, "detect_changes: tau must be >= 0");
+  const size_t plane = (size_t)h * w;
+  for (size_t px = 0; px < plane; ++px) {
+    int changed = 0;
+    for (int ch = 0; ch < c && !changed; ++ch)
+      changed = fabsf(x[ch * plane + px] - state[ch * plane + px]) > tau;
+    m[px] = (uint8_t)changed;
+    if (changed && mode == CBG_MODE_CLOSEDLOOP)
+      for (int ch = 0; ch < c; ++ch) state[ch * plane + px] = x[ch * plane + px];
+  }
+  if (mode == CBG_MODE_FEEDFORWARD) memcpy(state, x, (size_t)c * plane * sizeof(float));
+  return CBG_OK;
+}
+
+/* change.cpp:45-61 */
+int cbo_dilate_window(const uint8_t* m, int h, int w, int kh, int kw, int stride, int pad,
+                      int oh, int ow, uint8_t* out) {
+  memset(out, 0, (size_t)oh * ow);
+  for (int j = 0; j < h; ++j)
+    for (int i = 0; i < w; ++i) {
+      if (!m[(size_t)j * w + i]) continue;
+      const int jo0 = imax(0, ceil_div(j + pad - kh + 1, stride));
+      const int jo1 = imin(oh - 1, floor_div(j + pad, stride));
+      const int io0 = imax(0, ceil_div(i + pad - kw + 1, stride));
+      const int io1 = imin(ow - 1, floor_div(i + pad, stride));
+      for (int jo = jo0; jo <= jo1; ++jo)
+        for (int io = io0; io <= io1; ++io) out[(size_t)jo * ow + io] = 1;
+    }
+  return CBG_OK;
+}
+
+/* change.cpp:63-75 */
+int cbo_propagate_changes(const uint8_t* m, int h, int w, const cbg_conv_spec* s, uint8_t* out,
+                          int* oh, int* ow) {
+  const int H = cbo_out_dim(h, s->kernel_h, s->stride, s->padding, s->out_h);
+  const int W = cbo_out_dim(w, s->kernel_w, s->stride, s->padding, s->out_w);
+  if (H < 1 || W < 1) return fail(CBG_ERR_INVALID_INPUT, "conv output dim < 1");
+  *oh = H;
+  *ow = W;
+  if (!out) return CBG_OK;
+  if (s->kernel_h == 1 && s->kernel_w == 1 && s->stride == 1 && H == h && W == w) {
+    memcpy(out, m, (size_t)h * w);
+    return CBG_OK;
+  }
+  return cbo_dilate_window(m, h, w, s->kernel_h, s->kernel_w, s->stride, s->padding, H, W, out);
+}
+
+/* change.cpp:77-84 */
+int cbo_extract_indexes(const uint8_t* m, int h, int w, int32_t* rc, int64_t* n) {
+  int64_t k = 0;
+  for (int j = 0; j < h; ++j)
+    for (int i = 0; i < w; ++i)
+      if (m[(size_t)j * w + i]) {
+        if (rc) {
+          rc[2 * k] = j;
+          rc[2 * k + 1] = i;
+        }
+        ++k;
+      }
+  *n = k;
+  return CBG_OK;
+}
+
+/* one im2col column, dense.cpp:71-81 */
+static void im2col_column(const float* x, int c, int h, int w, const cbg_conv_spec* s, int jo,
+                          int io, float* dst) {
+  for (int ch = 0; ch < c; ++ch)
+    for (int kj = 0; kj < s->kernel_h; ++kj) {
+      const int jj = jo * s->stride - s->padding + kj;
+      for (int ki = 0; ki < s->kernel_w; ++ki) {
+        const int ii = io * s->stride - s->padding + ki;
+        *dst++ = (jj >= 0 && jj < h && ii >= 0 && ii < w) ? x[((size_t)ch * h + jj) * w + ii] : 0.0f;
+      }
+    }
+}
+
+/* dense.cpp:44-83 */
+int cbo_im2col(const float* x, int c, int h, int w, const cbg_conv_spec* s, const int32_t* rc,
+               int64_t n, float* cols) {
+  int r = validate_spec(s);
+  if (r) return r;
+  if (c != s->in_channels) return fail(CBG_ERR_INVALID_INPUT, "im2col: input/spec channel mismatch");
+  const int oh = cbo_out_dim(h, s->kernel_h, s->stride, s->padding, s->out_h);
+  const int ow = cbo_out_dim(w, s->kernel_w, s->stride, s->padding, s->out_w);
+  if (oh < 1 || ow < 1) return fail(CBG_ERR_INVALID_INPUT, "conv output dim < 1");
+  const size_t rows = (size_t)s->in_channels * s->kernel_h * s->kernel_w;
+  const int64_t ncols = rc ? n : (int64_t)oh * ow;
+  for (int64_t col = 0; col < ncols; ++col) {
+    int jo, io;
+    if (rc) {
+      jo = rc[2 * col];
+      io = rc[2 * col + 1];
+      if (jo < 0 || jo >= oh || io < 0 || io >= ow)
+        return fail(CBG_ERR_INVALID_INPUT, "im2col: selected pixel outside output");
+    } else {
+      jo = (int)(col / ow);
+      io = (int)(col % ow);
+    }
+    im2col_column(x, c, h, w, s, jo, io, cols + (size_t)col * rows);
+  }
+  return CBG_OK;
+}
+
+/* dense.cpp:85-112: per (o, col), one sequential fp32 reduction over r, from 0.0f */
+int cbo_gemm(const cbg_conv_spec* s, const float* cols, int64_t n, float* y) {
+  const size_t rows = (size_t)s->in_channels * s->kernel_h * s->kernel_w;
+  for (int64_t col = 0; col < n; ++col) {
+    const float* xc = cols + (size_t)col * rows;
+    for (int o = 0; o < s->out_channels; ++o) {
+      const float* k = s->weights + (size_t)o * rows; /* K == weights (tensor.cpp:45-56) */
+      float acc = 0.0f;
+      for (size_t r = 0; r < rows; ++r) acc += k[r] * xc[r];
+      y[(size_t)o * n + col] = acc;
+    }
+  }
+  return CBG_OK;
+}
+
+/* layers.cpp:10-31 */
+int cbo_update_output(float* prev, int cout, int oh, int ow, const float* y, const int32_t* rc,
+                      int64_t n, const float* bias, int fuse_relu) {
+  for (int64_t k = 0; k < n; ++k)
+    if (rc[2 * k] < 0 || rc[2 * k] >= oh || rc[2 * k + 1] < 0 || rc[2 * k + 1] >= ow)
+      return fail(CBG_ERR_INVALID_INPUT, "update_output: index outside the output tensor");
+  for (int o = 0; o < cout; ++o) {
+    const float b = bias[o];
+    for (int64_t k = 0; k < n; ++k) {
+      float v = y[(size_t)o * n + k] + b;
+      if (fuse_relu) v = (v < 0.0f) ? 0.0f : v; /* std::max(v, 0.f) */
+      prev[((size_t)o * oh + rc[2 * k]) * ow + rc[2 * k + 1]] = v;
+    }
+  }
+  return CBG_OK;
+}
+
+/* dense.cpp:8-42 */
+int cbo_conv2d_dense(const float* x, int c, int h, int w, const cbg_conv_spec* s, float* y) {
+  int r = validate_spec(s);
+  if (r) return r;
+  if (c != s->in_channels) return fail(CBG_ERR_INVALID_INPUT, "conv2d_dense: channel mismatch");
+  const int oh = cbo_out_dim(h, s->kernel_h, s->stride, s->padding, s->out_h);
+  const int ow = cbo_out_dim(w, s->kernel_w, s->stride, s->padding, s->out_w);
+  if (oh < 1 || ow < 1) return fail(CBG_ERR_INVALID_INPUT, "conv output dim < 1");
+  for (int o = 0; o < s->out_channels; ++o) {
+    const float* wo = s->weights + (size_t)o * s->in_channels * s->kernel_h * s->kernel_w;
+    for (int jo = 0; jo < oh; ++jo)
+      for (int io = 0; io < ow; ++io) {
+        float acc = 0.0f;
+        const float* wk = wo;
+        for (int ch = 0; ch < c; ++ch)
+          for (int kj = 0; kj < s->kernel_h; ++kj) {
+            const int jj = jo * s->stride - s->padding + kj;
+            for (int ki = 0; ki < s->kernel_w; ++ki, ++wk) {
+              const int ii = io * s->stride - s->padding + ki;
+              const float v =
+                  (jj >= 0 && jj < h && ii >= 0 && ii < w) ? x[((size_t)ch * h + jj) * w + ii] : 0.0f;
+              acc += *wk * v;
+            }
+          }
+        y[((size_t)o * oh + jo) * ow + io] = acc + s->bias[o];
+      }
+  }
+  return CBG_OK;
+}
+
+/* max over the clipped window anchored at (j0,i0), dense.cpp:135-141, layers.cpp:166-177 */
+static float window_max(const float* plane, int h, int w, int j0, int i0, int size) {
+  const int j1 = imin(j0 + size, h), i1 = imin(i0 + size, w);
+  float m = plane[(size_t)j0 * w + i0];
+  for (int j = j0; j < j1; ++j)
+    for (int i = i0; i < i1; ++i) {
+      const float v = plane[(size_t)j * w + i];
+      m = (m < v) ? v : m; /* std::max(m, v) */
+    }
+  return m;
+}
+
+/* dense.cpp:125-145 */
+int cbo_maxpool_to(const float* x, int c, int h, int w, int size, int stride, int oh, int ow,
+                   float* y) {
+  if (oh < 1 || ow < 1) return fail(CBG_ERR_INVALID_INPUT, "maxpool: output dims must be >= 1");
+  if ((oh - 1) * stride >= h || (ow - 1) * stride >= w)
+    return fail(CBG_ERR_INVALID_INPUT, "maxpool: output dims leave an empty window");
+  for (int ch = 0; ch < c; ++ch)
+    for (int jo = 0; jo < oh; ++jo)
+      for (int io = 0; io < ow; ++io)
+        y[((size_t)ch * oh + jo) * ow + io] =
+            window_max(x + (size_t)ch * h * w, h, w, jo * stride, io * stride, size);
+  return CBG_OK;
+}
+
+/* ------------------------------------------------------------------------ */
+/* network restatement                                                       */
+/* ------------------------------------------------------------------------ */
+#define MAXIN 8
+typedef struct {
+  int kind;
+  char name[64];
+  int n_in, in[MAXIN];
+  int oc, oh, ow;       /* out shape */
+  int ic, ih, iw;       /* in shape (conv/pool: producer shape) */
+  cbg_conv_spec spec;   /* conv: owns weights/bias */
+  float tau;
+  int policy, relu;
+  float* state;         /* conv Detect */
+  float* prev;          /* retained output */
+  int psize, pstride;   /* pool */
+  uint8_t* map;         /* this frame's output-frame map */
+  int32_t* idx;
+  int64_t nidx;
+} onode;
+
+struct cbo_net {
+  int C, H, W;
+  int mode;
+  int boot;
+  int n;
+  onode* nodes;
+};
+
+static size_t tsize(int c, int h, int w) { return (size_t)c * h * w; }
+
+void cbo_net_destroy(cbo_net* n) {
+  if (!n) return;
+  for (int i = 0; i < n->n; ++i) {
+    onode* d = &n->nodes[i];
+    free((void*)d->spec.weights);
+    free((void*)d->spec.bias);
+    free(d->state);
+    free(d->prev);
+    free(d->map);
+    free(d->idx);
+  }
+  free(n->nodes);
+  free(n);
+}
+
+static const char* label(const cbg_layer_desc* d, int i, char* buf) {
+  if (d->name && d->name[0]) return d->name;
+  snprintf(buf, 64, "L%d", i + 1);
+  return buf;
+}
+
+/* resolve (network.cpp:37-133) + convert_to_cb (network.cpp:416-503) */
+int cbo_net_create(const cbg_network_spec* spec, const float* taus, int n_taus,
+                   const int* policies, int mode, cbo_net** out) {
+  char buf[64], msg[256];
+  const int L = spec->n_layers;
+  if (spec->in_channels < 1 || spec->in_height < 1 || spec->in_width < 1)
+    return fail(CBG_ERR_INVALID_INPUT, "network spec: input resolution must be positive");
+  if (L < 1) return fail(CBG_ERR_INVALID_INPUT, "network spec: no layers");
+  int* inputs = calloc((size_t)L * MAXIN, sizeof(int));
+  int* n_in = calloc((size_t)L, sizeof(int));
+  int* shp = calloc((size_t)L * 3, sizeof(int));
+  int* new_id = malloc((size_t)L * sizeof(int));
+  int* consumers = calloc((size_t)L, sizeof(int));
+  cbo_net* net = calloc(1, sizeof(cbo_net));
+  net->nodes = calloc((size_t)L, sizeof(onode));
+  net->C = spec->in_channels;
+  net->H = spec->in_height;
+  net->W = spec->in_width;
+  net->mode = mode;
+  net->boot = 1;
+  int rc = CBG_OK;
+#define BAIL(code, ...)                       \
+  do {                                        \
+    snprintf(msg, sizeof msg, __VA_ARGS__);   \
+    rc = fail(code, msg);                     \
+    goto done;                                \
+  } while (0)
+  for (int i = 0; i < L; ++i) {
+    const cbg_layer_desc* d = &spec->layers[i];
+    if (d->n_from == 0) {
+      inputs[i * MAXIN] = i - 1;
+      n_in[i] = 1;
+    } else {
+      for (int k = 0; k < d->n_from; ++k) {
+        int id = -2;
+        if (strcmp(d->from[k], "input") == 0) id = -1;
+        else
+          for (int q = 0; q < i; ++q)
+            if (spec->layers[q].name && strcmp(spec->layers[q].name, d->from[k]) == 0) id = q;
+        if (id == -2) BAIL(CBG_ERR_INVALID_INPUT, "layer %d (%s): unknown or later producer '%s'", i, label(d, i, buf), d->from[k]);
+        inputs[i * MAXIN + n_in[i]++] = id;
+      }
+    }
+    const int* in = &inputs[i * MAXIN];
+    int sc = spec->in_channels, sh = spec->in_height, sw = spec->in_width;
+    if (in[0] >= 0) {
+      sc = shp[in[0] * 3];
+      sh = shp[in[0] * 3 + 1];
+      sw = shp[in[0] * 3 + 2];
+    }
+    switch (d->kind) {
+      case CBG_LAYER_CONV: {
+        if (n_in[i] != 1) BAIL(CBG_ERR_INVALID_INPUT, "layer %d (%s): conv takes exactly one producer", i, label(d, i, buf));
+        if (validate_spec(&d->conv)) { rc = CBG_ERR_INVALID_INPUT; goto done; }
+        if (sc != d->conv.in_channels) BAIL(CBG_ERR_INVALID_INPUT, "layer %d (%s): channel mismatch", i, label(d, i, buf));
+        shp[i * 3] = d->conv.out_channels;
+        shp[i * 3 + 1] = cbo_out_dim(sh, d->conv.kernel_h, d->conv.stride, d->conv.padding, d->conv.out_h);
+        shp[i * 3 + 2] = cbo_out_dim(sw, d->conv.kernel_w, d->conv.stride, d->conv.padding, d->conv.out_w);
+        if (shp[i * 3 + 1] < 1 || shp[i * 3 + 2] < 1) BAIL(CBG_ERR_INVALID_INPUT, "layer %d (%s): conv output dim < 1", i, label(d, i, buf));
+        break;
+      }
+      case CBG_LAYER_ACT:
+        shp[i * 3] = sc;
+        shp[i * 3 + 1] = sh;
+        shp[i * 3 + 2] = sw;
+        break;
+      case CBG_LAYER_POOL: {
+        if (d->pool_size < 1 || d->pool_stride < 1) BAIL(CBG_ERR_INVALID_INPUT, "layer %d: pool size/stride must be >= 1", i);
+        int dims[2] = {sh, sw}, pin[2] = {d->pool_out_h, d->pool_out_w}, o[2];
+        for (int a = 0; a < 2; ++a) {
+          if (pin[a] > 0) {
+            if ((pin[a] - 1) * d->pool_stride >= dims[a]) BAIL(CBG_ERR_INVALID_INPUT, "layer %d: pool output dim leaves an empty window", i);
+            o[a] = pin[a];
+          } else {
+            if (dims[a] < d->pool_size) BAIL(CBG_ERR_INVALID_INPUT, "layer %d: pool window larger than input", i);
+            o[a] = (dims[a] - d->pool_size) / d->pool_stride + 1;
+          }
+        }
+        shp[i * 3] = sc;
+        shp[i * 3 + 1] = o[0];
+        shp[i * 3 + 2] = o[1];
+        break;
+      }
+      case CBG_LAYER_ADD:
+      case CBG_LAYER_CONCAT: {
+        if (n_in[i] < 2) BAIL(CBG_ERR_INVALID_INPUT, "layer %d: join takes at least two producers", i);
+        int ch = 0;
+        for (int k = 0; k < n_in[i]; ++k) {
+          int q = in[k];
+          int c2 = q < 0 ? spec->in_channels : shp[q * 3], h2 = q < 0 ? spec->in_height : shp[q * 3 + 1],
+              w2 = q < 0 ? spec->in_width : shp[q * 3 + 2];
+          if (h2 != sh || w2 != sw || (d->kind == CBG_LAYER_ADD && c2 != sc)) BAIL(CBG_ERR_INVALID_INPUT, "layer %d: join producers differ in shape", i);
+          ch += c2;
+        }
+        shp[i * 3] = d->kind == CBG_LAYER_ADD ? sc : ch;
+        shp[i * 3 + 1] = sh;
+        shp[i * 3 + 2] = sw;
+        break;
+      }
+      default:
+        BAIL(CBG_ERR_INVALID_INPUT, "layer %d: unknown kind", i);
+    }
+  }
+  /* convert_to_cb */
+  {
+    int conv_rows = 0;
+    for (int i = 0; i < L; ++i) conv_rows += spec->layers[i].kind == CBG_LAYER_CONV;
+    if (n_taus != conv_rows) BAIL(CBG_ERR_INVALID_INPUT, "convert_to_cb: expected %d thresholds, got %d", conv_rows, n_taus);
+    for (int k = 0; k < n_taus; ++k)
+      if (taus[k] < 0.0f) BAIL(CBG_ERR_INVALID_INPUT, "convert_to_cb: tau must be >= 0");
+    for (int i = 0; i < L; ++i)
+      for (int k = 0; k < n_in[i]; ++k)
+        if (inputs[i * MAXIN + k] >= 0) ++consumers[inputs[i * MAXIN + k]];
+    int conv_idx = 0;
+    for (int i = 0; i < L; ++i) {
+      const cbg_layer_desc* d = &spec->layers[i];
+      const int src0 = inputs[i * MAXIN];
+      if (d->kind == CBG_LAYER_ACT) {
+        if (src0 < 0 || spec->layers[src0].kind != CBG_LAYER_CONV) BAIL(CBG_ERR_CONFIG, "layer %d: standalone activation can only be absorbed into a conv", i);
+        if (consumers[src0] != 1) BAIL(CBG_ERR_CONFIG, "layer %d: cannot absorb activation, conv output has other consumers", i);
+        net->nodes[new_id[src0]].relu = 1;
+        new_id[i] = new_id[src0];
+        continue;
+      }
+      onode* nd = &net->nodes[net->n];
+      nd->kind = d->kind;
+      snprintf(nd->name, sizeof nd->name, "%s", label(d, i, buf));
+      nd->n_in = n_in[i];
+      for (int k = 0; k < n_in[i]; ++k) nd->in[k] = inputs[i * MAXIN + k] < 0 ? -1 : new_id[inputs[i * MAXIN + k]];
+      nd->oc = shp[i * 3];
+      nd->oh = shp[i * 3 + 1];
+      nd->ow = shp[i * 3 + 2];
+      nd->ic = src0 < 0 ? spec->in_channels : shp[src0 * 3];
+      nd->ih = src0 < 0 ? spec->in_height : shp[src0 * 3 + 1];
+      nd->iw = src0 < 0 ? spec->in_width : shp[src0 * 3 + 2];
+      if (d->kind == CBG_LAYER_CONV) {
+        const int pol = policies ? policies[conv_idx] : CBG_POLICY_DETECT;
+        if (pol != CBG_POLICY_DETECT && nd->in[0] < 0) BAIL(CBG_ERR_CONFIG, "layer %d: policy needs an upstream change-based layer", i);
+        if (pol == CBG_POLICY_REUSE1X1 && !(d->conv.kernel_h == 1 && d->conv.kernel_w == 1 && d->conv.stride == 1 && nd->oh == nd->ih && nd->ow == nd->iw))
+          BAIL(CBG_ERR_CONFIG, "layer %d: reuse_1x1 policy requires a 1x1 stride-1 shape-preserving layer", i);
+        nd->spec = d->conv;
+        const size_t nw = (size_t)d->conv.out_channels * d->conv.in_channels * d->conv.kernel_h * d->conv.kernel_w;
+        float* w = malloc(nw * sizeof(float));
+        float* b = malloc((size_t)d->conv.out_channels * sizeof(float));
+        memcpy(w, d->conv.weights, nw * sizeof(float));
+        memcpy(b, d->conv.bias, (size_t)d->conv.out_channels * sizeof(float));
+        nd->spec.weights = w;
+        nd->spec.bias = b;
+        nd->tau = taus[conv_idx];
+        nd->policy = pol;
+        nd->relu = d->fuse_relu != 0;
+        if (pol == CBG_POLICY_DETECT) nd->state = calloc(tsize(nd->ic, nd->ih, nd->iw), sizeof(float));
+        ++conv_idx;
+      } else if (d->kind == CBG_LAYER_POOL) {
+        if (nd->in[0] < 0) BAIL(CBG_ERR_CONFIG, "layer %d: change-based pooling needs an upstream layer", i);
+        nd->psize = d->pool_size;
+        nd->pstride = d->pool_stride;
+      } else {
+        for (int k = 0; k < nd->n_in; ++k)
+          if (nd->in[k] < 0) BAIL(CBG_ERR_CONFIG, "layer %d: change-based joins need upstream layers, not the input", i);
+      }
+      nd->prev = calloc(tsize(nd->oc, nd->oh, nd->ow), sizeof(float));
+      nd->map = calloc((size_t)nd->oh * nd->ow, 1);
+      nd->idx = malloc((size_t)nd->oh * nd->ow * 2 * sizeof(int32_t));
+      new_id[i] = net->n++;
+    }
+  }
+done:
+#undef BAIL
+  free(inputs);
+  free(n_in);
+  free(shp);
+  free(new_id);
+  free(consumers);
+  if (rc) {
+    cbo_net_destroy(net);
+    return rc;
+  }
+  *out = net;
+  return CBG_OK;
+}
+
+int cbo_net_node_count(const cbo_net* n) { return n->n; }
+int cbo_net_node_shape(const cbo_net* n, int node, int* kind, int* c, int* h, int* w) {
+  const onode* d = &n->nodes[node];
+  *kind = d->kind;
+  *c = d->oc;
+  *h = d->oh;
+  *w = d->ow;
+  return CBG_OK;
+}
+
+/* CBConvLayer::forward, layers.cpp:55-131 (stats-free subset) */
+static int conv_forward(cbo_net* net, onode* nd, const float* x, const onode* up, int boot) {
+  const cbg_conv_spec* s = &nd->spec;
+  const float* column_src = x;
+  const size_t HWo = (size_t)nd->oh * nd->ow;
+  if (boot) {
+    if (nd->policy == CBG_POLICY_DETECT) {
+      memcpy(nd->state, x, tsize(nd->ic, nd->ih, nd->iw) * sizeof(float));
+      column_src = nd->state;
+    }
+    memset(nd->map, 1, HWo);
+  } else if (nd->policy == CBG_POLICY_DETECT) {
+    uint8_t* m = malloc((size_t)nd->ih * nd->iw);
+    cbo_detect_changes(x, nd->state, nd->ic, nd->ih, nd->iw, nd->tau, net->mode, m);
+    cbo_dilate_window(m, nd->ih, nd->iw, s->kernel_h, s->kernel_w, s->stride, s->padding, nd->oh, nd->ow, nd->map);
+    free(m);
+    column_src = net->mode == CBG_MODE_CLOSEDLOOP ? nd->state : x;
+  } else if (nd->policy == CBG_POLICY_PROPAGATE) {
+    if (!up) return fail(CBG_ERR_CONFIG, "propagate policy requires an upstream change map");
+    int oh, ow;
+    cbo_propagate_changes(up->map, nd->ih, nd->iw, s, nd->map, &oh, &ow);
+  } else {
+    if (!up) return fail(CBG_ERR_CONFIG, "reuse_1x1 policy requires upstream map and indexes");
+    memcpy(nd->map, up->map, HWo);
+  }
+  cbo_extract_indexes(nd->map, nd->oh, nd->ow, nd->idx, &nd->nidx);
+  const size_t rows = (size_t)s->in_channels * s->kernel_h * s->kernel_w;
+  float* col = malloc(rows * sizeof(float));
+  for (int64_t k = 0; k < nd->nidx; ++k) {
+    const int jo = nd->idx[2 * k], io = nd->idx[2 * k + 1];
+    im2col_column(column_src, nd->ic, nd->ih, nd->iw, s, jo, io, col);
+    for (int o = 0; o < s->out_channels; ++o) {
+      const float* kr = s->weights + (size_t)o * rows;
+      float acc = 0.0f;
+      for (size_t r = 0; r < rows; ++r) acc += kr[r] * col[r];
+      float v = acc + s->bias[o];
+      if (nd->relu) v = (v < 0.0f) ? 0.0f : v;
+      nd->prev[(size_t)o * HWo + (size_t)jo * nd->ow + io] = v;
+    }
+  }
+  free(col);
+  return CBG_OK;
+}
+
+static const float* node_out(const cbo_net* net, int id, const float* frame) {
+  return id < 0 ? frame : net->nodes[id].prev;
+}
+
+/* forward_frame, network.cpp:309-414 */
+int cbo_net_forward(cbo_net* net, const float* frame) {
+  const int boot = net->boot;
+  for (int i = 0; i < net->n; ++i) {
+    onode* nd = &net->nodes[i];
+    const size_t HWo = (size_t)nd->oh * nd->ow;
+    if (nd->kind == CBG_LAYER_CONV) {
+      const int src = nd->in[0];
+      int r = conv_forward(net, nd, node_out(net, src, frame), src >= 0 ? &net->nodes[src] : NULL, boot);
+      if (r) return r;
+    } else if (nd->kind == CBG_LAYER_POOL) {
+      const onode* up = &net->nodes[nd->in[0]];
+      if (boot) memset(nd->map, 1, HWo);
+      else cbo_dilate_window(up->map, nd->ih, nd->iw, nd->psize, nd->psize, nd->pstride, 0, nd->oh, nd->ow, nd->map);
+      cbo_extract_indexes(nd->map, nd->oh, nd->ow, nd->idx, &nd->nidx);
+      for (int64_t k = 0; k < nd->nidx; ++k) {
+        const int jo = nd->idx[2 * k], io = nd->idx[2 * k + 1];
+        for (int c = 0; c < nd->oc; ++c)
+          nd->prev[(size_t)c * HWo + (size_t)jo * nd->ow + io] =
+              window_max(up->prev + (size_t)c * nd->ih * nd->iw, nd->ih, nd->iw, jo * nd->pstride, io * nd->pstride, nd->psize);
+      }
+    } else { /* Add / Concat, network.cpp:364-398 */
+      if (boot) memset(nd->map, 1, HWo);
+      else {
+        memset(nd->map, 0, HWo);
+        for (int k = 0; k < nd->n_in; ++k)
+          for (size_t b = 0; b < HWo; ++b) nd->map[b] |= net->nodes[nd->in[k]].map[b];
+      }
+      cbo_extract_indexes(nd->map, nd->oh, nd->ow, nd->idx, &nd->nidx);
+      for (int64_t k = 0; k < nd->nidx; ++k) {
+        const size_t p = (size_t)nd->idx[2 * k] * nd->ow + nd->idx[2 * k + 1];
+        if (nd->kind == CBG_LAYER_ADD) {
+          for (int c = 0; c < nd->oc; ++c) {
+            float v = 0.0f;
+            for (int q = 0; q < nd->n_in; ++q) v += net->nodes[nd->in[q]].prev[(size_t)c * HWo + p];
+            nd->prev[(size_t)c * HWo + p] = v;
+          }
+        } else {
+          int off = 0;
+          for (int q = 0; q < nd->n_in; ++q) {
+            const onode* t = &net->nodes[nd->in[q]];
+            for (int c = 0; c < t->oc; ++c) nd->prev[(size_t)(off + c) * HWo + p] = t->prev[(size_t)c * HWo + p];
+            off += t->oc;
+          }
+        }
+      }
+    }
+  }
+  net->boot = 0;
+  return CBG_OK;
+}
+
+/* network.cpp:274-290 */
+int cbo_net_reset(cbo_net* net) {
+  for (int i = 0; i < net->n; ++i) {
+    onode* nd = &net->nodes[i];
+    memset(nd->prev, 0, tsize(nd->oc, nd->oh, nd->ow) * sizeof(float));
+    if (nd->state) memset(nd->state, 0, tsize(nd->ic, nd->ih, nd->iw) * sizeof(float));
+  }
+  net->boot = 1;
+  return CBG_OK;
+}
+
+/* network.cpp:263-272 */
+int cbo_net_set_thresholds(cbo_net* net, const float* taus, int n_taus) {
+  int convs = 0;
+  for (int i = 0; i < net->n; ++i) convs += net->nodes[i].kind == CBG_LAYER_CONV;
+  if (n_taus != convs) return fail(CBG_ERR_INVALID_INPUT, "set_thresholds: expected one tau per conv layer");
+  int k = 0;
+  for (int i = 0; i < net->n; ++i) {
+    if (net->nodes[i].kind != CBG_LAYER_CONV) continue;
+    if (taus[k] < 0.0f) return fail(CBG_ERR_INVALID_INPUT, "set_thresholds: tau must be >= 0");
+    net->nodes[i].tau = taus[k++];
+  }
+  return CBG_OK;
+}
+
+int cbo_net_read_output(const cbo_net* net, int node, float* y) {
+  const onode* nd = &net->nodes[node < 0 ? net->n - 1 : node];
+  memcpy(y, nd->prev, tsize(nd->oc, nd->oh, nd->ow) * sizeof(float));
+  return CBG_OK;
+}
+
+int cbo_net_read_state(const cbo_net* net, int node, float* y) {
+  const onode* nd = &net->nodes[node];
+  if (!nd->state) return fail(CBG_ERR_INVALID_INPUT, "node has no input state");
+  memcpy(y, nd->state, tsize(nd->ic, nd->ih, nd->iw) * sizeof(float));
+  return CBG_OK;
+}
+
+int cbo_net_read_changes(const cbo_net* net, int node, uint8_t* map, int32_t* rc, int64_t* count) {
+  const onode* nd = &net->nodes[node];
+  if (map) memcpy(map, nd->map, (size_t)nd->oh * nd->ow);
+  if (rc) memcpy(rc, nd->idx, (size_t)nd->nidx * 2 * sizeof(int32_t));
+  *count = nd->nidx;
+  return CBG_OK;
+}

@@ -1,0 +1,330 @@
+// conv_tcgen05.cu — change-based convolution update on the 5th-gen tensor cores.
+//
+// Replaces, in one persistent kernel, the reference's partial im2col + GEMM +
+// output update (dense.cpp:44-112, layers.cpp:10-31, layers.cpp:112-114):
+//
+//   for every changed output pixel p (row-major index list, count on device)
+//     Y[p, :] = act( sum_k X[p, k] * K[:, k] + bias )      scattered into
+//     prev_output[p, :]  (NHWC: one contiguous Cout vector per pixel)
+//
+// GEMM orientation: M = changed pixels (128-row tiles), N = Cout (NPAD <= 256),
+// K = kh*kw*Cs ordered (kj, ki, c) so one 16-B chunk of a K-row is one
+// contiguous run of a source pixel's channel vector.
+//
+// Precision: 3xTF32 (x = hi + lo; D += Ahi*Bhi + Ahi*Blo + Alo*Bhi) on
+// tcgen05.mma kind::tf32 with fp32 accumulation in TMEM — near-fp32 accuracy,
+// the same precision on the sparse and the dense (full-update) path.
+//
+// Warp roles (288 threads, 1 CTA/SM, persistent over (stream, m-tile, n-tile)):
+//   warps 0-3  epilogue: tcgen05.ld TMEM -> +bias -> ReLU -> scatter (lane = row)
+//   warps 4-7  producers: gather the A tile (changed pixels' receptive fields)
+//              with 16-B loads, split hi/lo, st.shared into the UMMA SW128
+//              K-major layout; thread 128 also streams the pre-swizzled B
+//              (weight) image of the K-block with a bulk copy on the TMA engine
+//   warp 8     TMEM allocator + single-thread tcgen05.mma issuer
+// Pipelines: smem stages full/empty (producers <-> MMA), two TMEM accumulators
+// full/empty (MMA <-> epilogue) so tile t's epilogue overlaps tile t+1's MMAs.
+#include <climits>
+#include <cstdio>
+
+#include "common.cuh"
+#include "kernels.hpp"
+
+namespace cbg {
+
+namespace {
+
+constexpr int kThreads = 288;
+constexpr int kBM = 128;                 // UMMA M
+constexpr int kBK = 32;                  // fp32 elements per K-block (= one 128-B swizzle row)
+constexpr int kABytes = kBM * kBK * 4;   // one of A_hi / A_lo: 16 KB
+constexpr int kMaxS = 1024;
+
+template <int NPAD>
+struct Cfg {
+  static constexpr int kBBytes = NPAD * kBK * 4;
+  static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
+  static constexpr int kStages = NPAD >= 256 ? 2 : NPAD >= 128 ? 3 : NPAD >= 64 ? 4 : 5;
+  static constexpr uint32_t kTmemCols = (2 * NPAD <= 32) ? 32 : (2 * NPAD <= 64) ? 64 : (2 * NPAD <= 128) ? 128
+                                        : (2 * NPAD <= 256) ? 256 : 512;
+};
+
+__host__ __device__ constexpr int tail_bytes(int stages, int KB, int S) {
+  return 8 * (2 * stages + 4) + 16 + kBM * 8 + KB * 8 * 4 + (S + 1) * 4;
+}
+
+template <int NPAD>
+__global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) {
+  using C = Cfg<NPAD>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* tail = smem + C::kStages * C::kStageBytes;
+  uint64_t* full = reinterpret_cast<uint64_t*>(tail);
+  uint64_t* empty = full + C::kStages;
+  uint64_t* tfull = empty + C::kStages;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
+  int2* rowinfo = reinterpret_cast<int2*>(tmem_holder + 4);
+  uint32_t* ktab = reinterpret_cast<uint32_t*>(rowinfo + kBM);
+  int* tprefix = reinterpret_cast<int*>(ktab + a.KB * 8);
+
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5, lane = tid & 31;
+  const long long HWin = static_cast<long long>(a.Hin) * a.Win;
+  const long long HWout = static_cast<long long>(a.Hout) * a.Wout;
+
+  // ---- setup -----------------------------------------------------------------
+  if (tid == 0) {
+    for (int i = 0; i < C::kStages; ++i) {
+      mbar_init(&full[i], 4 + 1);  // 4 producer warps + 1 expect_tx arrive
+      mbar_init(&empty[i], 1);     // tcgen05.commit
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tfull[i], 1);
+      mbar_init(&tempty[i], 4);    // 4 epilogue warps
+    }
+    fence_mbar_init();
+  }
+  if (warp == 8) tmem_alloc(tmem_holder, C::kTmemCols);
+  for (int i = tid; i < a.KB * 8; i += kThreads) ktab[i] = a.ktab[i];
+  if (warp == 0) {
+    int carry = 0;
+    if (lane == 0) tprefix[0] = 0;
+    for (int s0 = 0; s0 < a.S; s0 += 32) {
+      const int s = s0 + lane;
+      const int v = s < a.S ? ((a.count[s] + kBM - 1) / kBM) * a.n_tiles : 0;
+      int inc = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const int u = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += u;
+      }
+      if (s < a.S) tprefix[s + 1] = carry + inc;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+  const int total = tprefix[a.S];
+
+  auto decode = [&](int w, int& s, int& mt, int& nt) {
+    int lo = 0, hi = a.S;  // find s with tprefix[s] <= w < tprefix[s+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (tprefix[mid] <= w) lo = mid;
+      else hi = mid;
+    }
+    s = lo;
+    const int local = w - tprefix[s];
+    mt = local / a.n_tiles;
+    nt = local - mt * a.n_tiles;
+  };
+
+  if (warp >= 4 && warp < 8) {
+    // ========================= producers =========================
+    const int ptid = tid - 128;
+    const int q = ptid & 7;
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int s, mt, nt;
+      decode(w, s, mt, nt);
+      const int cnt = a.count[s];
+      named_bar_sync(1, 128);  // every producer is done reading the previous tile's rowinfo
+      {
+        const int k = mt * kBM + ptid;
+        if (k < cnt) {
+          const int p = a.idx[s * HWout + k];
+          const int jo = p / a.Wout, io = p - jo * a.Wout;
+          rowinfo[ptid] = make_int2(jo * a.stride - a.pad, io * a.stride - a.pad);
+        } else {
+          rowinfo[ptid] = make_int2(INT_MIN / 2, INT_MIN / 2);
+        }
+      }
+      named_bar_sync(1, 128);
+      const float* src = a.src + s * HWin * a.Cs;
+      const uint8_t* bimg = a.wimg + static_cast<long long>(nt) * a.KB * 2 * C::kBBytes;
+      for (int kb = 0; kb < a.KB; ++kb) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sA = smem + stage * C::kStageBytes;
+        if (ptid == 0) {
+          mbar_arrive_expect_tx(&full[stage], 2 * C::kBBytes);
+          bulk_g2s(sA + 2 * kABytes, bimg + static_cast<long long>(kb) * 2 * C::kBBytes, 2 * C::kBBytes,
+                   &full[stage]);
+        }
+        const uint32_t tab = ktab[kb * 8 + q];
+        const int dj = tab & 0xFF, di = (tab >> 8) & 0xFF, c0 = (tab >> 16) & 0x7FFF;
+        const bool tap_ok = (tab >> 31) == 0;
+        float4 v[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = i * 16 + (ptid >> 3);
+          const int2 ri = rowinfo[r];
+          const int jj = ri.x + dj, ii = ri.y + di;
+          const bool ok = tap_ok && static_cast<unsigned>(jj) < static_cast<unsigned>(a.Hin) &&
+                          static_cast<unsigned>(ii) < static_cast<unsigned>(a.Win);
+          v[i] = ok ? ldg_nc_f4(src + (static_cast<long long>(jj) * a.Win + ii) * a.Cs + c0)
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const int r = i * 16 + (ptid >> 3);
+          const uint32_t off = r * 128 + ((q ^ (r & 7)) << 4);
+          const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
+          uint32_t h[4], l[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            h[j] = tf32_rna(x[j]);
+            l[j] = tf32_rna(x[j] - __uint_as_float(h[j]));
+          }
+          const uint32_t dh = smem_u32(sA + off), dl = smem_u32(sA + kABytes + off);
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dh), "r"(h[0]), "r"(h[1]), "r"(h[2]),
+                       "r"(h[3])
+                       : "memory");
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dl), "r"(l[0]), "r"(l[1]), "r"(l[2]),
+                       "r"(l[3])
+                       : "memory");
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+        if (++stage == C::kStages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 8) {
+    // ========================= MMA issuer =========================
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_tf32(kBM, NPAD);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int w = blockIdx.x; w < total; w += gridDim.x) {
+        mbar_wait(&tempty[acc], acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem_base + acc * NPAD;
+        for (int kb = 0; kb < a.KB; ++kb) {
+          mbar_wait(&full[stage], phase);
+          tc_fence_after();
+          const uint32_t a_hi = smem_u32(smem + stage * C::kStageBytes);
+          const uint32_t a_lo = a_hi + kABytes;
+          const uint32_t b_hi = a_hi + 2 * kABytes;
+          const uint32_t b_lo = b_hi + C::kBBytes;
+#pragma unroll
+          for (int k = 0; k < kBK / 8; ++k) {
+            const uint32_t ko = k * 32;  // 8 tf32 = 32 B along K inside the swizzle row
+            umma_tf32(d, umma_desc_sw128(a_lo + ko), umma_desc_sw128(b_hi + ko), idesc, (kb | k) != 0);
+            umma_tf32(d, umma_desc_sw128(a_hi + ko), umma_desc_sw128(b_lo + ko), idesc, 1);
+            umma_tf32(d, umma_desc_sw128(a_hi + ko), umma_desc_sw128(b_hi + ko), idesc, 1);
+          }
+          umma_commit(&empty[stage]);  // smem slot free once these MMAs retire
+          if (++stage == C::kStages) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+    __syncwarp();
+  } else if (warp < 4) {
+    // ========================= epilogue =========================
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int s, mt, nt;
+      decode(w, s, mt, nt);
+      const int cnt = a.count[s];
+      const int k = mt * kBM + warp * 32 + lane;
+      const bool valid = k < cnt;
+      const int p = valid ? a.idx[s * HWout + k] : 0;
+      float* orow = a.out + (s * HWout + p) * a.Co4;
+      const int nbase = nt * NPAD;
+      mbar_wait(&tfull[acc], acc_phase);
+      tc_fence_after();
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + acc * NPAD;
+#pragma unroll 1
+      for (int n0 = 0; n0 < NPAD; n0 += 16) {
+        uint32_t r[16];
+        tmem_ld16(tb + n0, r);
+        tmem_ld_wait();
+        if (valid) {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int n = nbase + n0 + 4 * j;
+            if (n < a.Co4) {
+              float o[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                float y = __uint_as_float(r[4 * j + u]) + __ldg(a.bias + n + u);
+                if (a.relu) y = (y < 0.0f) ? 0.0f : y;  // std::max(v, 0.f)
+                o[u] = y;
+              }
+              *reinterpret_cast<float4*>(orow + n) = make_float4(o[0], o[1], o[2], o[3]);
+            }
+          }
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 8) {
+    tc_fence_after();
+    tmem_dealloc(tmem_base, C::kTmemCols);
+  }
+}
+
+template <int NPAD>
+void launch_impl(const ConvGemmArgs& a, cudaStream_t st) {
+  const int smem = conv_gemm_smem_bytes(NPAD, a.KB, a.S);
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(conv_gemm_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    configured = true;
+  }
+  conv_gemm_kernel<NPAD><<<a.grid, kThreads, smem, st>>>(a);
+}
+
+}  // namespace
+
+int conv_gemm_stages(int npad) {
+  switch (npad) {
+    case 16: return Cfg<16>::kStages;
+    case 32: return Cfg<32>::kStages;
+    case 64: return Cfg<64>::kStages;
+    case 128: return Cfg<128>::kStages;
+    default: return Cfg<256>::kStages;
+  }
+}
+
+int conv_gemm_smem_bytes(int npad, int KB, int S) {
+  const int stages = conv_gemm_stages(npad);
+  const int stage_bytes = 2 * kABytes + 2 * npad * kBK * 4;
+  return 1024 + stages * stage_bytes + tail_bytes(stages, KB, S);
+}
+
+void launch_conv_gemm(const ConvGemmArgs& a, cudaStream_t st) {
+  switch (a.npad) {
+    case 16: launch_impl<16>(a, st); break;
+    case 32: launch_impl<32>(a, st); break;
+    case 64: launch_impl<64>(a, st); break;
+    case 128: launch_impl<128>(a, st); break;
+    default: launch_impl<256>(a, st); break;
+  }
+}
+
+}  // namespace cbg

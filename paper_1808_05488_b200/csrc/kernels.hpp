@@ -1,0 +1,136 @@
+// kernels.hpp — launch interface of the CBinfer sm_100a kernels (host side).
+//
+// Device data layout (per node, S = streams of the stream set, all contiguous
+// [S][...] with per-stream strides):
+//   feature maps / states : NHWC fp32, channel stride Cs = round_up(C, 4), so
+//                           a pixel's channel vector is one 16-B aligned run;
+//                           padded channels hold 0 forever.
+//   network input frame   : CHW fp32 (the reference Tensor3 layout), read only
+//                           by the first layer's fused ingest+detect kernel.
+//   change maps           : uint8 [H][W], epoch-tagged (see common.cuh).
+//   index lists           : int32 pixel ids p = row*W + col, row-major
+//                           ascending; count in a device int32 per stream.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace cbg {
+
+// Fused change detection on the network-input frame (CHW) against a
+// closed-loop / feed-forward state (NHWC), reference change.cpp:20-43.
+struct DetectFrameArgs {
+  const float* const* x_slot;  // device slot holding the frame pointer [S][C][H][W]
+  float* state;        // [S][H][W][Cs]
+  uint8_t* map;        // [S][H][W] epoch-tagged input-frame map
+  const uint32_t* frame;     // device frame counter
+  const uint8_t* boot;       // [S] full-update flags for this frame
+  int C, Cs, H, W, S;
+  const float* tau;    // device scalar (set_thresholds needs no re-capture)
+  int closed_loop;
+};
+void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st);
+
+// Change detection on an NHWC input produced by a change-based node. Only the
+// producer's update set can differ from the state (exact), so
+// the kernel walks the producer's index list. dense != 0 (or boot) walks all pixels.
+struct DetectListArgs {
+  const float* x;            // [S][H][W][Cs]
+  float* state;              // [S][H][W][Cs]
+  uint8_t* map;              // [S][H][W]
+  const int32_t* prod_idx;   // [S][H*W]  (nullable when dense)
+  const int32_t* prod_count; // [S]
+  const uint32_t* frame;
+  const uint8_t* boot;
+  const uint8_t* dense;      // device flag (nullable = 0): rescan every pixel
+  int Cs, H, W, S;
+  const float* tau;
+  int closed_loop;
+};
+void launch_detect_list(const DetectListArgs& a, cudaStream_t st);
+
+// Window dilation (reference change.cpp:45-67, also CB pooling's map,
+// layers.cpp:163) fused with the ordered stream compaction of the output map
+// into the row-major index list (reference extract_indexes, change.cpp:77-84).
+// Up to 4 input maps are OR-ed first (join nodes, network.cpp:366-373).
+struct DilateCompactArgs {
+  const uint8_t* in_map[4];  // [S][Hin][Win] epoch-tagged
+  int n_in;
+  uint8_t* out_map;          // [S][Hout][Wout] epoch-tagged
+  int32_t* idx;              // [S][Hout*Wout]
+  int32_t* count;            // [S]
+  uint64_t* tile_status;     // [S][n_tiles] look-back state
+  const uint32_t* frame;
+  const uint8_t* boot;
+  int Hin, Win, Hout, Wout, kh, kw, stride, pad;
+  int rows_per_tile, n_tiles, S;
+  int smem_bytes;
+};
+void launch_dilate_compact(const DilateCompactArgs& a, cudaStream_t st);
+int dilate_compact_smem(int Win, int Wout, int rows_per_tile, int kh, int stride);
+
+// Change-based max pooling at the pool's index list (reference layers.cpp:148-179).
+struct PoolArgs {
+  const float* x;        // [S][Hin][Win][Cs]
+  float* out;            // [S][Hout][Wout][Cs]
+  const int32_t* idx;    // [S][Hout*Wout]
+  const int32_t* count;  // [S]
+  int Cs, Hin, Win, Hout, Wout, size, stride, S;
+};
+void launch_pool(const PoolArgs& a, cudaStream_t st);
+
+// Add / Concat joins at the join's index list (reference network.cpp:364-398).
+struct JoinArgs {
+  const float* in[8];
+  int in_cs[8];          // channel stride of each parent
+  int in_c[8];           // real channels of each parent
+  int n_in;
+  int is_add;
+  float* out;            // [S][H][W][Cs_out]
+  int Cs_out;
+  const int32_t* idx;
+  const int32_t* count;
+  int HW, S;
+};
+void launch_join(const JoinArgs& a, cudaStream_t st);
+
+// Gather + 3xTF32 tcgen05 GEMM + bias/ReLU scatter (reference im2col + gemm +
+// update_output: dense.cpp:44-112, layers.cpp:10-31).
+struct ConvGemmArgs {
+  const float* src;        // [S][Hin][Win][Cs] column source (state or producer output)
+  float* out;              // [S][Hout][Wout][Co4]
+  const int32_t* idx;      // [S][Hout*Wout]
+  const int32_t* count;    // [S]
+  const uint8_t* wimg;     // pre-swizzled tf32 hi/lo weight images [n_tiles][KB][2][NPAD][128B]
+  const uint32_t* ktab;    // [KB*8] (kj | ki<<8 | c0<<16 | invalid<<31) per 16-B chunk
+  const float* bias;       // [n_tiles*NPAD]
+  int Cs, Hin, Win, Hout, Wout, Co4;
+  int stride, pad;
+  int KB;                  // K blocks of 32 fp32
+  int npad;                // N tile: 16, 32, 64, 128 or 256
+  int n_tiles;             // ceil(Co4 / npad)
+  int relu;
+  int S;
+  int grid;                // persistent CTAs (<= SM count)
+};
+void launch_conv_gemm(const ConvGemmArgs& a, cudaStream_t st);
+int conv_gemm_smem_bytes(int npad, int KB, int S);
+int conv_gemm_stages(int npad);
+
+// Device frame-counter advance + per-stream boot flags for this frame.
+struct BeginFrameArgs {
+  uint32_t* frame;
+  uint8_t* boot_now;     // [S] out
+  uint8_t* boot_req;     // [S] in, cleared
+  const uint8_t* dense;  // device flag: every frame is a full update
+  uint8_t* rescan_now;   // [n_nodes] out: dense re-detection after a tau change
+  uint8_t* rescan_req;   // [n_nodes] in, cleared
+  int S, n_nodes;
+};
+void launch_begin_frame(const BeginFrameArgs& a, cudaStream_t st);
+
+// Layout conversions for the synchronising readers and standalone uploads.
+void launch_nhwc_to_chw(const float* src, float* dst, int C, int Cs, int HW, cudaStream_t st);
+void launch_chw_to_nhwc(const float* src, float* dst, int C, int Cs, int HW, cudaStream_t st);
+
+}  // namespace cbg

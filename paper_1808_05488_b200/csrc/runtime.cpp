@@ -1,0 +1,929 @@
+// runtime.cpp — host runtime of the B200 CBinfer path (see runtime.hpp).
+#include "runtime.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <numeric>
+#include <unordered_map>
+
+#include "kernels.hpp"
+
+namespace cbg {
+
+[[noreturn]] void throw_invalid(const std::string& m) { throw Error(CBG_ERR_INVALID_INPUT, m); }
+[[noreturn]] void throw_config(const std::string& m) { throw Error(CBG_ERR_CONFIG, m); }
+void cuda_check(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  if (e == cudaErrorMemoryAllocation) throw Error(CBG_ERR_OOM, std::string(what) + ": " + cudaGetErrorString(e));
+  throw Error(CBG_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+#define CK(x) cuda_check((x), #x)
+
+// ---- shapes / validation (tensor.cpp:9-43) ------------------------------------
+int conv_out_dim(int in_dim, int kernel, int stride, int padding, int pinned) {
+  if (pinned > 0) return pinned;
+  const int v = (in_dim + 2 * padding - kernel) / stride + 1;
+  if (in_dim + 2 * padding - kernel < 0 || v < 1)
+    throw_invalid("conv output dim < 1 (input " + std::to_string(in_dim) + ", kernel " + std::to_string(kernel) +
+                  ", stride " + std::to_string(stride) + ", padding " + std::to_string(padding) + ")");
+  return v;
+}
+
+void validate_conv(const ConvDesc& c) {
+  if (c.in_channels < 1 || c.out_channels < 1 || c.kernel_h < 1 || c.kernel_w < 1)
+    throw_invalid("conv spec: channel and kernel dims must be >= 1");
+  if (c.stride < 1) throw_invalid("conv spec: stride must be >= 1");
+  if (c.padding < 0) throw_invalid("conv spec: padding must be >= 0");
+  if (c.out_h < 0 || c.out_w < 0 || (c.out_h > 0) != (c.out_w > 0))
+    throw_invalid("conv spec: explicit output dims must both be set and >= 1");
+  const size_t wc = static_cast<size_t>(c.out_channels) * c.in_channels * c.kernel_h * c.kernel_w;
+  if (c.weights.size() != wc)
+    throw_invalid("conv spec: weight count " + std::to_string(c.weights.size()) + " != out*in*kh*kw = " +
+                  std::to_string(wc));
+  if (c.bias.size() != static_cast<size_t>(c.out_channels))
+    throw_invalid("conv spec: bias count " + std::to_string(c.bias.size()) + " != out_channels = " +
+                  std::to_string(c.out_channels));
+}
+
+ConvDesc conv_from_c(const cbg_conv_spec& s) {
+  ConvDesc c;
+  c.in_channels = s.in_channels;
+  c.out_channels = s.out_channels;
+  c.kernel_h = s.kernel_h;
+  c.kernel_w = s.kernel_w;
+  c.stride = s.stride;
+  c.padding = s.padding;
+  c.out_h = s.out_h;
+  c.out_w = s.out_w;
+  if (s.in_channels > 0 && s.out_channels > 0 && s.kernel_h > 0 && s.kernel_w > 0) {
+    const size_t wc = static_cast<size_t>(s.out_channels) * s.in_channels * s.kernel_h * s.kernel_w;
+    if (!s.weights || !s.bias) throw_invalid("conv spec: weights and bias must be given");
+    c.weights.assign(s.weights, s.weights + wc);
+    c.bias.assign(s.bias, s.bias + s.out_channels);
+  }
+  return c;
+}
+
+// ---- resolve + convert_to_cb (network.cpp:37-133, 416-503) ----------------------
+namespace {
+std::string layer_label(const cbg_layer_desc& d, int i) {
+  return (d.name && d.name[0]) ? std::string(d.name) : "L" + std::to_string(i + 1);
+}
+std::string where_label(const cbg_layer_desc& d, int i) {
+  return "layer " + std::to_string(i) + " (" + layer_label(d, i) + ")";
+}
+int pool_out_dim(int in_dim, int size, int stride, int explicit_dim, const std::string& where) {
+  if (explicit_dim > 0) {
+    if ((explicit_dim - 1) * stride >= in_dim)
+      throw_invalid(where + ": pool output dim " + std::to_string(explicit_dim) + " leaves an empty window");
+    return explicit_dim;
+  }
+  if (in_dim < size) throw_invalid(where + ": pool window larger than input dim " + std::to_string(in_dim));
+  return (in_dim - size) / stride + 1;
+}
+struct Shape {
+  int c = 0, h = 0, w = 0;
+  bool operator==(const Shape& o) const { return c == o.c && h == o.h && w == o.w; }
+};
+}  // namespace
+
+Topology convert(const cbg_network_spec& spec, const float* taus, int n_taus, const int* policies, int mode) {
+  if (spec.in_channels < 1 || spec.in_height < 1 || spec.in_width < 1)
+    throw_invalid("network spec: input resolution must be positive");
+  if (spec.n_layers < 1 || spec.layers == nullptr) throw_invalid("network spec: no layers");
+  if (mode != CBG_MODE_CLOSEDLOOP && mode != CBG_MODE_FEEDFORWARD) throw_invalid("unknown detect mode");
+  const int n = spec.n_layers;
+  std::unordered_map<std::string, int> by_name;
+  for (int i = 0; i < n; ++i) {
+    const cbg_layer_desc& d = spec.layers[i];
+    if (!d.name || !d.name[0]) continue;
+    const std::string name = d.name;
+    if (name == "input" || !by_name.emplace(name, i).second)
+      throw_invalid(where_label(d, i) + ": duplicate or reserved name");
+  }
+  std::vector<std::vector<int>> inputs(n);
+  std::vector<Shape> shape(n);
+  const Shape in_shape{spec.in_channels, spec.in_height, spec.in_width};
+  auto shape_of = [&](int id) { return id < 0 ? in_shape : shape[id]; };
+  std::vector<ConvDesc> convs(n);
+
+  for (int i = 0; i < n; ++i) {
+    const cbg_layer_desc& d = spec.layers[i];
+    const std::string where = where_label(d, i);
+    std::vector<int>& in = inputs[i];
+    if (d.n_from <= 0) {
+      in.push_back(i - 1);
+    } else {
+      for (int k = 0; k < d.n_from; ++k) {
+        const std::string src = d.from[k] ? d.from[k] : "";
+        if (src == "input") {
+          in.push_back(-1);
+          continue;
+        }
+        auto it = by_name.find(src);
+        if (it == by_name.end() || it->second >= i)
+          throw_invalid(where + ": unknown or later producer '" + src + "'");
+        in.push_back(it->second);
+      }
+    }
+    try {
+      switch (d.kind) {
+        case CBG_LAYER_CONV: {
+          if (in.size() != 1) throw_invalid("conv takes exactly one producer");
+          convs[i] = conv_from_c(d.conv);
+          validate_conv(convs[i]);
+          const Shape s = shape_of(in[0]);
+          if (s.c != d.conv.in_channels)
+            throw_invalid("expects " + std::to_string(d.conv.in_channels) + " input channels, producer has " +
+                          std::to_string(s.c));
+          shape[i] = {d.conv.out_channels,
+                      conv_out_dim(s.h, d.conv.kernel_h, d.conv.stride, d.conv.padding, d.conv.out_h),
+                      conv_out_dim(s.w, d.conv.kernel_w, d.conv.stride, d.conv.padding, d.conv.out_w)};
+          break;
+        }
+        case CBG_LAYER_ACT:
+          if (in.size() != 1) throw_invalid("act takes exactly one producer");
+          shape[i] = shape_of(in[0]);
+          break;
+        case CBG_LAYER_POOL: {
+          if (in.size() != 1) throw_invalid("pool takes exactly one producer");
+          if (d.pool_size < 1 || d.pool_stride < 1) throw_invalid("pool size/stride must be >= 1");
+          const Shape s = shape_of(in[0]);
+          shape[i] = {s.c, pool_out_dim(s.h, d.pool_size, d.pool_stride, d.pool_out_h, "h"),
+                      pool_out_dim(s.w, d.pool_size, d.pool_stride, d.pool_out_w, "w")};
+          break;
+        }
+        case CBG_LAYER_ADD: {
+          if (in.size() < 2) throw_invalid("add takes at least two producers");
+          const Shape s = shape_of(in[0]);
+          for (int id : in)
+            if (!(shape_of(id) == s)) throw_invalid("add producers differ in shape");
+          shape[i] = s;
+          break;
+        }
+        case CBG_LAYER_CONCAT: {
+          if (in.size() < 2) throw_invalid("concat takes at least two producers");
+          const Shape s = shape_of(in[0]);
+          int ch = 0;
+          for (int id : in) {
+            const Shape si = shape_of(id);
+            if (si.h != s.h || si.w != s.w) throw_invalid("concat producers differ in spatial dims");
+            ch += si.c;
+          }
+          shape[i] = {ch, s.h, s.w};
+          break;
+        }
+        default:
+          throw_invalid("unknown layer kind " + std::to_string(d.kind));
+      }
+    } catch (const Error& e) {
+      if (e.code != CBG_ERR_INVALID_INPUT) throw;
+      throw_invalid(where + ": " + e.what());
+    }
+  }
+
+  int conv_rows = 0;
+  for (int i = 0; i < n; ++i) conv_rows += spec.layers[i].kind == CBG_LAYER_CONV;
+  if (n_taus != conv_rows)
+    throw_invalid("convert_to_cb: expected " + std::to_string(conv_rows) + " thresholds, got " +
+                  std::to_string(n_taus));
+  for (int k = 0; k < n_taus; ++k)
+    if (!(taus[k] >= 0.0f)) throw_invalid("convert_to_cb: tau must be >= 0");
+  if (policies)
+    for (int k = 0; k < n_taus; ++k)
+      if (policies[k] < CBG_POLICY_DETECT || policies[k] > CBG_POLICY_REUSE1X1) throw_invalid("unknown policy");
+
+  std::vector<int> consumers(n, 0);
+  for (int i = 0; i < n; ++i)
+    for (int id : inputs[i])
+      if (id >= 0) ++consumers[id];
+
+  Topology topo;
+  topo.C = spec.in_channels;
+  topo.H = spec.in_height;
+  topo.W = spec.in_width;
+  topo.mode = mode;
+  std::vector<int> new_id(n, -1);
+  int conv_idx = 0;
+  for (int i = 0; i < n; ++i) {
+    const cbg_layer_desc& d = spec.layers[i];
+    const std::string where = where_label(d, i);
+    const Shape ish = shape_of(inputs[i][0]);
+    if (d.kind == CBG_LAYER_ACT) {
+      const int src = inputs[i][0];
+      if (src < 0 || spec.layers[src].kind != CBG_LAYER_CONV)
+        throw_config(where + ": standalone activation can only be absorbed into a conv");
+      if (consumers[src] != 1) throw_config(where + ": cannot absorb activation, conv output has other consumers");
+      topo.nodes[new_id[src]].relu = true;
+      new_id[i] = new_id[src];
+      continue;
+    }
+    NodeDesc nd;
+    nd.kind = d.kind;
+    nd.name = layer_label(d, i);
+    nd.C = shape[i].c;
+    nd.H = shape[i].h;
+    nd.W = shape[i].w;
+    nd.Ci = ish.c;
+    nd.Hi = ish.h;
+    nd.Wi = ish.w;
+    for (int id : inputs[i]) nd.inputs.push_back(id < 0 ? -1 : new_id[id]);
+    if (d.kind == CBG_LAYER_CONV) {
+      const int policy = policies ? policies[conv_idx] : CBG_POLICY_DETECT;
+      if (policy != CBG_POLICY_DETECT && nd.inputs[0] < 0)
+        throw_config(where + ": " + (policy == CBG_POLICY_PROPAGATE ? "propagate" : "reuse_1x1") +
+                     " policy needs an upstream change-based layer");
+      nd.conv = convs[i];
+      nd.tau = taus[conv_idx];
+      nd.policy = policy;
+      nd.relu = d.fuse_relu != 0;
+      if (policy == CBG_POLICY_REUSE1X1 &&
+          !(nd.conv.kernel_h == 1 && nd.conv.kernel_w == 1 && nd.conv.stride == 1 && nd.H == nd.Hi && nd.W == nd.Wi))
+        throw_config(where + ": reuse_1x1 policy requires a 1x1 stride-1 shape-preserving layer");
+      ++conv_idx;
+    } else if (d.kind == CBG_LAYER_POOL) {
+      if (nd.inputs[0] < 0) throw_config(where + ": change-based pooling needs an upstream layer");
+      nd.pool_size = d.pool_size;
+      nd.pool_stride = d.pool_stride;
+    } else {
+      for (int id : nd.inputs)
+        if (id < 0) throw_config(where + ": change-based joins need upstream layers, not the input");
+      if (nd.inputs.size() > 4) throw Error(CBG_ERR_UNSUPPORTED, where + ": joins support at most 4 producers");
+    }
+    new_id[i] = static_cast<int>(topo.nodes.size());
+    topo.nodes.push_back(std::move(nd));
+  }
+  return topo;
+}
+
+// ---- device resources --------------------------------------------------------------
+DevBuf& DevBuf::operator=(DevBuf&& o) noexcept {
+  if (this != &o) {
+    if (p) cudaFree(p);
+    p = o.p;
+    bytes = o.bytes;
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  return *this;
+}
+DevBuf::~DevBuf() {
+  if (p) cudaFree(p);
+}
+void DevBuf::alloc(size_t n) {
+  if (p) cudaFree(p);
+  p = nullptr;
+  bytes = n;
+  if (n == 0) return;
+  CK(cudaMalloc(&p, n));
+  CK(cudaMemset(p, 0, n));
+}
+
+Ctx::Ctx(int dev) : device(dev) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) throw Error(CBG_ERR_UNSUPPORTED, "no CUDA device visible");
+  if (dev < 0 || dev >= n) throw_invalid("device index out of range");
+  CK(cudaSetDevice(dev));
+  cudaDeviceProp prop;
+  CK(cudaGetDeviceProperties(&prop, dev));
+  if (prop.major != 10)
+    throw Error(CBG_ERR_UNSUPPORTED, std::string("kernels are built for sm_100a; device is ") + prop.name);
+  sm_count = prop.multiProcessorCount;
+  CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+}
+Ctx::~Ctx() {
+  if (stream) cudaStreamDestroy(stream);
+}
+
+// ---- Net ------------------------------------------------------------------------------
+namespace {
+int round4(int c) { return (c + 3) & ~3; }
+
+uint32_t tf32_round(float x) {  // round-to-nearest-away into the top 19 bits (cvt.rna.tf32.f32)
+  uint32_t u;
+  std::memcpy(&u, &x, 4);
+  if ((u & 0x7f800000u) == 0x7f800000u) return u & 0xffffe000u;
+  u += 0x1000u;
+  return u & 0xffffe000u;
+}
+
+// Pre-swizzled UMMA SW128 K-major images of the (kj, ki, c)-ordered weight
+// matrix, split into tf32 hi / lo: [n_tile][kb][hi|lo][npad rows][128 B].
+void build_weight_image(const NodeRT& n, std::vector<uint8_t>& img, std::vector<uint32_t>& ktab,
+                        std::vector<float>& bias) {
+  const ConvDesc& c = n.d.conv;
+  const int taps = c.kernel_h * c.kernel_w;
+  const int Kreal = taps * n.Csi;
+  const int Bbytes = n.npad * 128;
+  img.assign(static_cast<size_t>(n.n_tiles) * n.KB * 2 * Bbytes, 0);
+  auto wval = [&](int o, int k) -> float {
+    if (o >= c.out_channels || k >= Kreal) return 0.0f;
+    const int t = k / n.Csi, ch = k % n.Csi;
+    if (ch >= c.in_channels) return 0.0f;
+    const int kj = t / c.kernel_w, ki = t % c.kernel_w;
+    return c.weights[((static_cast<size_t>(o) * c.in_channels + ch) * c.kernel_h + kj) * c.kernel_w + ki];
+  };
+  for (int nt = 0; nt < n.n_tiles; ++nt)
+    for (int kb = 0; kb < n.KB; ++kb) {
+      uint8_t* base = img.data() + (static_cast<size_t>(nt) * n.KB + kb) * 2 * Bbytes;
+      for (int r = 0; r < n.npad; ++r)
+        for (int q = 0; q < 8; ++q)
+          for (int j = 0; j < 4; ++j) {
+            const float w = wval(nt * n.npad + r, kb * 32 + q * 4 + j);
+            const uint32_t hi = tf32_round(w);
+            float hf;
+            std::memcpy(&hf, &hi, 4);
+            const uint32_t lo = tf32_round(w - hf);
+            const size_t off = static_cast<size_t>(r) * 128 + ((q ^ (r & 7)) << 4) + j * 4;
+            std::memcpy(base + off, &hi, 4);
+            std::memcpy(base + Bbytes + off, &lo, 4);
+          }
+    }
+  ktab.assign(static_cast<size_t>(n.KB) * 8, 0);
+  for (int kb = 0; kb < n.KB; ++kb)
+    for (int q = 0; q < 8; ++q) {
+      const int k0 = kb * 32 + q * 4;
+      const int t = k0 / n.Csi, c0 = k0 % n.Csi;
+      if (t >= taps) {
+        ktab[kb * 8 + q] = 0x80000000u;
+      } else {
+        const int kj = t / c.kernel_w, ki = t % c.kernel_w;
+        ktab[kb * 8 + q] = static_cast<uint32_t>(kj) | (static_cast<uint32_t>(ki) << 8) |
+                           (static_cast<uint32_t>(c0) << 16);
+      }
+    }
+  bias.assign(static_cast<size_t>(n.n_tiles) * n.npad, 0.0f);
+  for (int o = 0; o < c.out_channels; ++o) bias[o] = c.bias[o];
+}
+
+void dc_tiling(int Hin, int Win, int Hout, int Wout, int kh, int stride, int S, int* rows, int* tiles,
+               int* smem) {
+  if (Wout > 8192) throw Error(CBG_ERR_UNSUPPORTED, "output width > 8192 not supported by the compaction kernel");
+  int r = std::max(1, std::min(Hout, 4096 / std::max(1, Wout)));
+  // enough tiles to spread a single stream over the SMs
+  while (r > 1 && static_cast<long long>((Hout + r - 1) / r) * S < 296) r = (r + 1) / 2;
+  while (r > 1 && dilate_compact_smem(Win, Wout, r, kh, stride) > 48 * 1024) --r;
+  *rows = r;
+  *tiles = (Hout + r - 1) / r;
+  *smem = dilate_compact_smem(Win, Wout, r, kh, stride);
+  (void)Hin;
+  if (*smem > 48 * 1024) throw Error(CBG_ERR_UNSUPPORTED, "compaction tile exceeds 48 KB of shared memory");
+}
+}  // namespace
+
+Net::Net(Ctx* ctx, Topology topo, int n_streams) : ctx_(ctx), topo_(std::move(topo)), S_(n_streams) {
+  if (S_ < 1 || S_ > 1024) throw_invalid("n_streams must be in [1, 1024]");
+  build();
+}
+
+Net::~Net() {
+  for (auto& g : graphs_) cudaGraphExecDestroy(g.second);
+  for (auto& e : ev_pool_) cudaEventDestroy(e);
+}
+
+std::unique_ptr<Net> Net::clone() const {
+  auto c = std::make_unique<Net>(ctx_, topo_, S_);
+  CK(cudaStreamSynchronize(ctx_->stream));
+  for (size_t i = 0; i < nodes_.size(); ++i) {
+    const NodeRT& a = nodes_[i];
+    NodeRT& b = c->nodes_[i];
+    if (a.out.bytes) CK(cudaMemcpy(b.out.p, a.out.p, a.out.bytes, cudaMemcpyDeviceToDevice));
+    if (a.state.bytes) CK(cudaMemcpy(b.state.p, a.state.p, a.state.bytes, cudaMemcpyDeviceToDevice));
+  }
+  CK(cudaMemcpy(c->boot_req_.p, boot_req_.p, S_, cudaMemcpyDeviceToDevice));
+  c->host_taus_ = host_taus_;
+  CK(cudaMemcpy(c->taus_.p, taus_.p, taus_.bytes, cudaMemcpyDeviceToDevice));
+  CK(cudaMemcpy(c->rescan_req_.p, rescan_req_.p, rescan_req_.bytes, cudaMemcpyDeviceToDevice));
+  c->set_dense(dense_);
+  return c;
+}
+
+void Net::build() {
+  CK(cudaSetDevice(ctx_->device));
+  const int n = static_cast<int>(topo_.nodes.size());
+  nodes_.resize(n);
+  n_slots_ = 0;
+  for (int i = 0; i < n; ++i) {
+    NodeRT& r = nodes_[i];
+    r.d = topo_.nodes[i];
+    const NodeDesc& d = r.d;
+    r.Cs = round4(d.C);
+    r.Csi = round4(d.Ci);
+    const size_t HWo = static_cast<size_t>(d.H) * d.W;
+    const size_t HWi = static_cast<size_t>(d.Hi) * d.Wi;
+    r.out.alloc(static_cast<size_t>(S_) * HWo * r.Cs * sizeof(float));
+    const bool reuse = d.kind == CBG_LAYER_CONV && d.policy == CBG_POLICY_REUSE1X1;
+    if (reuse) {
+      const NodeRT& prod = nodes_[d.inputs[0]];
+      r.outmap = prod.outmap;
+      r.idx = prod.idx;
+      r.count_slot = prod.count_slot;
+    } else {
+      r.outmap_own.alloc(static_cast<size_t>(S_) * HWo);
+      r.idx_own.alloc(static_cast<size_t>(S_) * HWo * sizeof(int32_t));
+      r.outmap = r.outmap_own.as<uint8_t>();
+      r.idx = r.idx_own.as<int32_t>();
+      r.count_slot = n_slots_++;
+    }
+    if (d.kind == kExternal) continue;
+    if (d.kind == CBG_LAYER_CONV) {
+      const ConvDesc& c = d.conv;
+      if (c.kernel_h > 255 || c.kernel_w > 255) throw Error(CBG_ERR_UNSUPPORTED, "kernel dims > 255");
+      const int Co4 = r.Cs;
+      r.npad = Co4 <= 16 ? 16 : Co4 <= 32 ? 32 : Co4 <= 64 ? 64 : Co4 <= 128 ? 128 : 256;
+      r.n_tiles = (Co4 + r.npad - 1) / r.npad;
+      const int K = c.kernel_h * c.kernel_w * r.Csi;
+      r.KB = (K + 31) / 32;
+      if (r.KB > 512) throw Error(CBG_ERR_UNSUPPORTED, "Cin*kh*kw too large for the GEMM kernel (K > 16384)");
+      if (r.Csi >= 32768) throw Error(CBG_ERR_UNSUPPORTED, "too many input channels");
+      std::vector<uint8_t> img;
+      std::vector<uint32_t> ktab;
+      std::vector<float> bias;
+      build_weight_image(r, img, ktab, bias);
+      r.wimg.alloc(img.size());
+      CK(cudaMemcpy(r.wimg.p, img.data(), img.size(), cudaMemcpyHostToDevice));
+      r.ktab.alloc(ktab.size() * 4);
+      CK(cudaMemcpy(r.ktab.p, ktab.data(), ktab.size() * 4, cudaMemcpyHostToDevice));
+      r.bias.alloc(bias.size() * 4);
+      CK(cudaMemcpy(r.bias.p, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
+      if (d.policy == CBG_POLICY_DETECT) {
+        r.state.alloc(static_cast<size_t>(S_) * HWi * r.Csi * sizeof(float));
+        r.inmap.alloc(static_cast<size_t>(S_) * HWi);
+      }
+      if (!reuse) {
+        if (d.policy == CBG_POLICY_DETECT || d.policy == CBG_POLICY_PROPAGATE)
+          dc_tiling(d.Hi, d.Wi, d.H, d.W, c.kernel_h, c.stride, S_, &r.dc_rows, &r.dc_tiles, &r.dc_smem);
+        r.tilestat.alloc(static_cast<size_t>(S_) * r.dc_tiles * 8);
+      }
+      // worst-case map buffers (record_worst_case, layers.cpp:108-117)
+      if (d.inputs[0] >= 0) {
+        dc_tiling(d.Hi, d.Wi, d.H, d.W, c.kernel_h, c.stride, S_, &r.dc_wc_rows, &r.dc_wc_tiles, &r.dc_wc_smem);
+        r.wc_map.alloc(static_cast<size_t>(S_) * HWo);
+        r.wc_idx.alloc(static_cast<size_t>(S_) * HWo * sizeof(int32_t));
+        r.wc_tilestat.alloc(static_cast<size_t>(S_) * r.dc_wc_tiles * 8);
+      }
+      r.wc_slot = n_slots_++;
+    } else if (d.kind == CBG_LAYER_POOL) {
+      dc_tiling(d.Hi, d.Wi, d.H, d.W, d.pool_size, d.pool_stride, S_, &r.dc_rows, &r.dc_tiles, &r.dc_smem);
+      r.tilestat.alloc(static_cast<size_t>(S_) * r.dc_tiles * 8);
+    } else {  // joins: OR of the parents' maps, 1x1 identity window
+      dc_tiling(d.H, d.W, d.H, d.W, 1, 1, S_, &r.dc_rows, &r.dc_tiles, &r.dc_smem);
+      r.tilestat.alloc(static_cast<size_t>(S_) * r.dc_tiles * 8);
+    }
+  }
+  frame_.alloc(static_cast<size_t>(S_) * topo_.C * topo_.H * topo_.W * sizeof(float));
+  frame_slot_.alloc(sizeof(void*));
+  {
+    const float* p = frame_.as<float>();
+    CK(cudaMemcpy(frame_slot_.p, &p, sizeof(p), cudaMemcpyHostToDevice));
+    slot_value_ = p;
+  }
+  frame_ctr_.alloc(4);
+  boot_req_.alloc(S_);
+  CK(cudaMemset(boot_req_.p, 1, S_));
+  boot_now_.alloc(S_);
+  dense_flag_.alloc(1);
+  rescan_req_.alloc(std::max(1, n));
+  rescan_now_.alloc(std::max(1, n));
+  taus_.alloc(std::max(1, n) * sizeof(float));
+  host_taus_.assign(n, 0.0f);
+  for (int i = 0; i < n; ++i) host_taus_[i] = nodes_[i].d.tau;
+  CK(cudaMemcpy(taus_.p, host_taus_.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+  counts_.alloc(static_cast<size_t>(std::max(1, n_slots_)) * S_ * sizeof(int32_t));
+}
+
+void Net::clear_maps() {
+  for (NodeRT& r : nodes_) {
+    if (r.inmap.bytes) CK(cudaMemsetAsync(r.inmap.p, 0, r.inmap.bytes, ctx_->stream));
+    if (r.outmap_own.bytes) CK(cudaMemsetAsync(r.outmap_own.p, 0, r.outmap_own.bytes, ctx_->stream));
+    if (r.wc_map.bytes) CK(cudaMemsetAsync(r.wc_map.p, 0, r.wc_map.bytes, ctx_->stream));
+  }
+}
+
+int Net::launch_count(unsigned flags) const {
+  int k = 1;  // begin_frame
+  for (const NodeRT& r : nodes_) {
+    const NodeDesc& d = r.d;
+    if (d.kind == kExternal) continue;
+    if (d.kind == CBG_LAYER_CONV) {
+      k += (d.policy == CBG_POLICY_DETECT) + (d.policy != CBG_POLICY_REUSE1X1) + 1;
+      if ((flags & CBG_FWD_RECORD_WORST_CASE) && d.inputs[0] >= 0) k += 1;
+    } else {
+      k += 2;
+    }
+  }
+  return k;
+}
+
+void Net::enqueue_frame(unsigned flags) {
+  cudaStream_t st = ctx_->stream;
+  int32_t* counts = counts_.as<int32_t>();
+  const uint32_t* frame = frame_ctr_.as<uint32_t>();
+  const uint8_t* boot = boot_now_.as<uint8_t>();
+  const int n = static_cast<int>(nodes_.size());
+  {
+    BeginFrameArgs b{frame_ctr_.as<uint32_t>(), boot_now_.as<uint8_t>(), boot_req_.as<uint8_t>(),
+                     dense_flag_.as<uint8_t>(), rescan_now_.as<uint8_t>(), rescan_req_.as<uint8_t>(), S_, n};
+    timed("frame.begin", [&] { launch_begin_frame(b, st); });
+  }
+  for (int i = 0; i < n; ++i) {
+    NodeRT& r = nodes_[i];
+    const NodeDesc& d = r.d;
+    if (d.kind == kExternal) continue;
+    const int src = d.inputs[0];
+    const NodeRT* prod = src >= 0 ? &nodes_[src] : nullptr;
+    if (d.kind == CBG_LAYER_CONV) {
+      const ConvDesc& c = d.conv;
+      const float* column_src = prod ? prod->out.as<float>() : nullptr;
+      if (d.policy == CBG_POLICY_DETECT) {
+        if (!prod) {
+          DetectFrameArgs a{frame_slot_.as<const float*>(), r.state.as<float>(), r.inmap.as<uint8_t>(), frame, boot,
+                            d.Ci, r.Csi, d.Hi, d.Wi, S_, taus_.as<float>() + i,
+                            topo_.mode == CBG_MODE_CLOSEDLOOP};
+          timed(d.name + ".detect", [&] { launch_detect_frame(a, st); });
+        } else {
+          const bool ext = prod->d.kind == kExternal;  // standalone layer: arbitrary x, dense detect
+          DetectListArgs a{prod->out.as<float>(), r.state.as<float>(), r.inmap.as<uint8_t>(),
+                           ext ? nullptr : prod->idx, counts + prod->count_slot * S_, frame, boot,
+                           rescan_now_.as<uint8_t>() + i, r.Csi, d.Hi, d.Wi, S_, taus_.as<float>() + i,
+                           topo_.mode == CBG_MODE_CLOSEDLOOP};
+          timed(d.name + ".detect", [&] { launch_detect_list(a, st); });
+        }
+        // ClosedLoop reads the state; FeedForward's state equals x after detection.
+        column_src = r.state.as<float>();
+        DilateCompactArgs dc{};
+        dc.in_map[0] = r.inmap.as<uint8_t>();
+        dc.n_in = 1;
+        dc.out_map = r.outmap;
+        dc.idx = r.idx;
+        dc.count = counts + r.count_slot * S_;
+        dc.tile_status = r.tilestat.as<uint64_t>();
+        dc.frame = frame;
+        dc.boot = boot;
+        dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
+        dc.kh = c.kernel_h, dc.kw = c.kernel_w, dc.stride = c.stride, dc.pad = c.padding;
+        dc.rows_per_tile = r.dc_rows, dc.n_tiles = r.dc_tiles, dc.S = S_, dc.smem_bytes = r.dc_smem;
+        timed(d.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
+      } else if (d.policy == CBG_POLICY_PROPAGATE) {
+        DilateCompactArgs dc{};
+        dc.in_map[0] = prod->outmap;
+        dc.n_in = 1;
+        dc.out_map = r.outmap;
+        dc.idx = r.idx;
+        dc.count = counts + r.count_slot * S_;
+        dc.tile_status = r.tilestat.as<uint64_t>();
+        dc.frame = frame;
+        dc.boot = boot;
+        dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
+        dc.kh = c.kernel_h, dc.kw = c.kernel_w, dc.stride = c.stride, dc.pad = c.padding;
+        dc.rows_per_tile = r.dc_rows, dc.n_tiles = r.dc_tiles, dc.S = S_, dc.smem_bytes = r.dc_smem;
+        timed(d.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
+      }
+      if ((flags & CBG_FWD_RECORD_WORST_CASE) && prod) {
+        DilateCompactArgs dc{};
+        dc.in_map[0] = prod->outmap;
+        dc.n_in = 1;
+        dc.out_map = r.wc_map.as<uint8_t>();
+        dc.idx = r.wc_idx.as<int32_t>();
+        dc.count = counts + r.wc_slot * S_;
+        dc.tile_status = r.wc_tilestat.as<uint64_t>();
+        dc.frame = frame;
+        dc.boot = boot;
+        dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
+        dc.kh = c.kernel_h, dc.kw = c.kernel_w, dc.stride = c.stride, dc.pad = c.padding;
+        dc.rows_per_tile = r.dc_wc_rows, dc.n_tiles = r.dc_wc_tiles, dc.S = S_, dc.smem_bytes = r.dc_wc_smem;
+        timed(d.name + ".worstcase", [&] { launch_dilate_compact(dc, st); });
+      }
+      ConvGemmArgs g{};
+      g.src = column_src;
+      g.out = r.out.as<float>();
+      g.idx = r.idx;
+      g.count = counts + r.count_slot * S_;
+      g.wimg = r.wimg.as<uint8_t>();
+      g.ktab = r.ktab.as<uint32_t>();
+      g.bias = r.bias.as<float>();
+      g.Cs = r.Csi, g.Hin = d.Hi, g.Win = d.Wi, g.Hout = d.H, g.Wout = d.W, g.Co4 = r.Cs;
+      g.stride = c.stride, g.pad = c.padding;
+      g.KB = r.KB, g.npad = r.npad, g.n_tiles = r.n_tiles;
+      g.relu = d.relu;
+      g.S = S_;
+      g.grid = ctx_->sm_count;
+      timed(d.name + ".gemm", [&] { launch_conv_gemm(g, st); });
+    } else if (d.kind == CBG_LAYER_POOL) {
+      DilateCompactArgs dc{};
+      dc.in_map[0] = prod->outmap;
+      dc.n_in = 1;
+      dc.out_map = r.outmap;
+      dc.idx = r.idx;
+      dc.count = counts + r.count_slot * S_;
+      dc.tile_status = r.tilestat.as<uint64_t>();
+      dc.frame = frame;
+      dc.boot = boot;
+      dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
+      dc.kh = d.pool_size, dc.kw = d.pool_size, dc.stride = d.pool_stride, dc.pad = 0;
+      dc.rows_per_tile = r.dc_rows, dc.n_tiles = r.dc_tiles, dc.S = S_, dc.smem_bytes = r.dc_smem;
+      timed(d.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
+      PoolArgs pa{prod->out.as<float>(), r.out.as<float>(), r.idx, counts + r.count_slot * S_, r.Cs, d.Hi, d.Wi,
+                  d.H, d.W, d.pool_size, d.pool_stride, S_};
+      timed(d.name + ".pool", [&] { launch_pool(pa, st); });
+    } else {  // Add / Concat
+      DilateCompactArgs dc{};
+      for (size_t k = 0; k < d.inputs.size(); ++k) dc.in_map[k] = nodes_[d.inputs[k]].outmap;
+      dc.n_in = static_cast<int>(d.inputs.size());
+      dc.out_map = r.outmap;
+      dc.idx = r.idx;
+      dc.count = counts + r.count_slot * S_;
+      dc.tile_status = r.tilestat.as<uint64_t>();
+      dc.frame = frame;
+      dc.boot = boot;
+      dc.Hin = d.H, dc.Win = d.W, dc.Hout = d.H, dc.Wout = d.W;
+      dc.kh = 1, dc.kw = 1, dc.stride = 1, dc.pad = 0;
+      dc.rows_per_tile = r.dc_rows, dc.n_tiles = r.dc_tiles, dc.S = S_, dc.smem_bytes = r.dc_smem;
+      timed(d.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
+      JoinArgs ja{};
+      for (size_t k = 0; k < d.inputs.size(); ++k) {
+        const NodeRT& p = nodes_[d.inputs[k]];
+        ja.in[k] = p.out.as<float>();
+        ja.in_cs[k] = p.Cs;
+        ja.in_c[k] = p.d.C;
+      }
+      ja.n_in = static_cast<int>(d.inputs.size());
+      ja.is_add = d.kind == CBG_LAYER_ADD;
+      ja.out = r.out.as<float>();
+      ja.Cs_out = r.Cs;
+      ja.idx = r.idx;
+      ja.count = counts + r.count_slot * S_;
+      ja.HW = d.H * d.W;
+      ja.S = S_;
+      timed(d.name + ".join", [&] { launch_join(ja, st); });
+    }
+  }
+}
+
+void Net::forward(const float* frames, unsigned flags) {
+  cudaStream_t st = ctx_->stream;
+  CK(cudaSetDevice(ctx_->device));
+  const bool ext = !nodes_.empty() && nodes_[0].d.kind == kExternal;
+  if (!ext) {
+    if (frames == nullptr) throw_invalid("forward_frame: null frame");
+    const float* want = (flags & CBG_FWD_INPUT_ON_DEVICE) ? frames : frame_.as<float>();
+    if (want != slot_value_) {
+      // zero-copy for device inputs: the ingest kernel reads through a device
+      // pointer slot, so the captured graph stays valid (pageable source: the
+      // value is consumed before cudaMemcpyAsync returns)
+      const float* v = want;
+      CK(cudaMemcpyAsync(frame_slot_.p, &v, sizeof(v), cudaMemcpyHostToDevice, st));
+      slot_value_ = want;
+    }
+    if (!(flags & CBG_FWD_INPUT_ON_DEVICE))
+      CK(cudaMemcpyAsync(frame_.p, frames, frame_.bytes, cudaMemcpyHostToDevice, st));
+  }
+  if (flags & CBG_FWD_FORCE_FULL) CK(cudaMemsetAsync(boot_req_.p, 1, S_, st));
+  ++host_frame_;
+  if (host_frame_ > 1 && (host_frame_ - 1) % 255 == 0) clear_maps();  // epoch8 wraps
+  const unsigned gflags = flags & CBG_FWD_RECORD_WORST_CASE;
+  last_flags_ = flags;
+  last_launches_ = launch_count(gflags);
+  if (timing_) {
+    enqueue_frame(gflags);
+    CK(cudaStreamSynchronize(st));
+    size_t k = 0;
+    for (auto& p : pending_) {
+      float ms = 0;
+      CK(cudaEventElapsedTime(&ms, p.second.first, p.second.second));
+      auto& acc = times_[p.first];
+      acc.first += ms;
+      acc.second += 1;
+      ev_pool_[k++] = p.second.first;
+      ev_pool_[k++] = p.second.second;
+    }
+    pending_.clear();
+    ++timed_frames_;
+    CK(cudaGetLastError());
+    return;
+  }
+  auto it = graphs_.find(gflags);
+  if (it == graphs_.end()) {
+    cudaGraph_t g;
+    CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    try {
+      enqueue_frame(gflags);
+    } catch (...) {
+      cudaStreamEndCapture(st, &g);
+      throw;
+    }
+    CK(cudaStreamEndCapture(st, &g));
+    cudaGraphExec_t ge;
+    CK(cudaGraphInstantiate(&ge, g, 0));
+    cudaGraphDestroy(g);
+    it = graphs_.emplace(gflags, ge).first;
+  }
+  CK(cudaGraphLaunch(it->second, st));
+  CK(cudaGetLastError());
+}
+
+template <class F>
+void Net::timed(const std::string& label, F&& launch) {
+  if (!timing_) {
+    launch();
+    return;
+  }
+  const size_t need = 2 * (pending_.size() + 1);
+  while (ev_pool_.size() < need) {
+    cudaEvent_t e;
+    CK(cudaEventCreate(&e));
+    ev_pool_.push_back(e);
+  }
+  cudaEvent_t a = ev_pool_[need - 2], b = ev_pool_[need - 1];
+  CK(cudaEventRecord(a, ctx_->stream));
+  launch();
+  CK(cudaEventRecord(b, ctx_->stream));
+  pending_.push_back({label, {a, b}});
+}
+
+void Net::set_timing(bool on) {
+  timing_ = on;
+  times_.clear();
+  timed_frames_ = 0;
+}
+
+std::string Net::timing_report() const {
+  std::string js = "{\"frames\": " + std::to_string(timed_frames_) + ", \"kernels\": {";
+  bool first = true;
+  for (const auto& kv : times_) {
+    char buf[256];
+    std::snprintf(buf, sizeof buf, "%s\"%s\": [%.6f, %lld]", first ? "" : ", ", kv.first.c_str(), kv.second.first,
+                  kv.second.second);
+    js += buf;
+    first = false;
+  }
+  return js + "}}";
+}
+
+void Net::copy_counts_async(int32_t* host_dst) {
+  CK(cudaMemcpyAsync(host_dst, counts_.p, static_cast<size_t>(std::max(1, n_slots_)) * S_ * sizeof(int32_t),
+                     cudaMemcpyDeviceToHost, ctx_->stream));
+}
+
+void Net::copy_output_async(int node, void* host_dst) {
+  if (node < 0) node = static_cast<int>(nodes_.size()) - 1;
+  if (node >= static_cast<int>(nodes_.size())) throw_invalid("copy_output_async: bad node");
+  const NodeRT& r = nodes_[node];
+  CK(cudaMemcpyAsync(host_dst, r.out.p, r.out.bytes, cudaMemcpyDeviceToHost, ctx_->stream));
+}
+
+void Net::set_external(const float* x_chw, const uint8_t* map, const int32_t* rowcol, int64_t n, bool full) {
+  NodeRT& e = nodes_[0];
+  const NodeDesc& d = e.d;
+  cudaStream_t st = ctx_->stream;
+  const size_t HW = static_cast<size_t>(d.H) * d.W;
+  // the frame of the external node is a CHW staging copy
+  CK(cudaMemcpyAsync(frame_.p, x_chw, static_cast<size_t>(d.C) * HW * sizeof(float), cudaMemcpyHostToDevice, st));
+  launch_chw_to_nhwc(frame_.as<float>(), e.out.as<float>(), d.C, e.Cs, static_cast<int>(HW), st);
+  // map / indexes tagged with the epoch of the coming frame
+  const uint32_t next = host_frame_ + 1;
+  const uint8_t tag = static_cast<uint8_t>((next - 1) % 255 + 1);
+  // full: a forced full update sees every upstream pixel as changed (a
+  // Reuse1x1 layer then recomputes everything, layers.cpp:64-71)
+  std::vector<uint8_t> m(HW, full ? tag : 0);
+  if (map && !full)
+    for (size_t i = 0; i < HW; ++i) m[i] = map[i] ? tag : 0;
+  CK(cudaMemcpy(e.outmap, m.data(), HW, cudaMemcpyHostToDevice));
+  std::vector<int32_t> idx;
+  if (full) {
+    idx.resize(HW);
+    for (size_t k = 0; k < HW; ++k) idx[k] = static_cast<int32_t>(k);
+    CK(cudaMemcpy(e.idx, idx.data(), HW * sizeof(int32_t), cudaMemcpyHostToDevice));
+  } else if (rowcol) {
+    idx.resize(static_cast<size_t>(n));
+    for (int64_t k = 0; k < n; ++k) idx[k] = rowcol[2 * k] * d.W + rowcol[2 * k + 1];
+    if (n) CK(cudaMemcpy(e.idx, idx.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  const int32_t cnt = static_cast<int32_t>(full ? HW : rowcol ? n : 0);
+  CK(cudaMemcpy(counts_.as<int32_t>() + e.count_slot * S_, &cnt, sizeof(cnt), cudaMemcpyHostToDevice));
+}
+
+void Net::reset(int stream) {
+  if (stream < -1 || stream >= S_) throw_invalid("reset: stream out of range");
+  cudaStream_t st = ctx_->stream;
+  const int s0 = stream < 0 ? 0 : stream, s1 = stream < 0 ? S_ : stream + 1;
+  for (NodeRT& r : nodes_) {
+    if (r.d.kind == kExternal) continue;
+    const size_t per_out = r.out.bytes / S_;
+    CK(cudaMemsetAsync(static_cast<uint8_t*>(r.out.p) + per_out * s0, 0, per_out * (s1 - s0), st));
+    if (r.state.bytes) {
+      const size_t per = r.state.bytes / S_;
+      CK(cudaMemsetAsync(static_cast<uint8_t*>(r.state.p) + per * s0, 0, per * (s1 - s0), st));
+    }
+  }
+  CK(cudaMemsetAsync(boot_req_.as<uint8_t>() + s0, 1, s1 - s0, st));
+}
+
+void Net::set_thresholds(const std::vector<float>& taus) {
+  std::vector<int> conv_nodes;
+  for (size_t i = 0; i < nodes_.size(); ++i)
+    if (nodes_[i].d.kind == CBG_LAYER_CONV) conv_nodes.push_back(static_cast<int>(i));
+  if (taus.size() != conv_nodes.size()) throw_invalid("set_thresholds: expected one tau per conv layer");
+  for (float t : taus)
+    if (!(t >= 0.0f)) throw_invalid("set_thresholds: tau must be >= 0");
+  std::vector<uint8_t> rescan(nodes_.size(), 0);
+  for (size_t k = 0; k < conv_nodes.size(); ++k) {
+    const int i = conv_nodes[k];
+    // Sparse detection is exact only while tau does not decrease:
+    // a lowered threshold re-detects every pixel once.
+    if (taus[k] < host_taus_[i]) rescan[i] = 1;
+    host_taus_[i] = taus[k];
+    nodes_[i].d.tau = taus[k];
+  }
+  cudaStream_t st = ctx_->stream;
+  CK(cudaStreamSynchronize(st));
+  CK(cudaMemcpy(taus_.p, host_taus_.data(), host_taus_.size() * sizeof(float), cudaMemcpyHostToDevice));
+  std::vector<uint8_t> cur(nodes_.size());
+  CK(cudaMemcpy(cur.data(), rescan_req_.p, nodes_.size(), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < cur.size(); ++i) cur[i] |= rescan[i];
+  CK(cudaMemcpy(rescan_req_.p, cur.data(), nodes_.size(), cudaMemcpyHostToDevice));
+}
+
+std::vector<float> Net::thresholds() const {
+  std::vector<float> t;
+  for (const NodeRT& r : nodes_)
+    if (r.d.kind == CBG_LAYER_CONV) t.push_back(host_taus_[&r - nodes_.data()]);
+  return t;
+}
+
+void Net::set_dense(bool dense) {
+  dense_ = dense;
+  const uint8_t v = dense ? 1 : 0;
+  CK(cudaMemcpyAsync(dense_flag_.p, &v, 1, cudaMemcpyHostToDevice, ctx_->stream));
+  CK(cudaStreamSynchronize(ctx_->stream));
+}
+
+void Net::read_output(int node, int stream, float* out_chw) {
+  if (node < 0) node = static_cast<int>(nodes_.size()) - 1;
+  if (node >= static_cast<int>(nodes_.size()) || stream < 0 || stream >= S_) throw_invalid("read_output: bad node/stream");
+  const NodeRT& r = nodes_[node];
+  const size_t HW = static_cast<size_t>(r.d.H) * r.d.W;
+  DevBuf tmp;
+  tmp.alloc(static_cast<size_t>(r.d.C) * HW * sizeof(float));
+  launch_nhwc_to_chw(r.out.as<float>() + static_cast<size_t>(stream) * HW * r.Cs, tmp.as<float>(), r.d.C, r.Cs,
+                     static_cast<int>(HW), ctx_->stream);
+  CK(cudaMemcpyAsync(out_chw, tmp.p, tmp.bytes, cudaMemcpyDeviceToHost, ctx_->stream));
+  CK(cudaStreamSynchronize(ctx_->stream));
+}
+
+void Net::read_state(int node, int stream, float* out_chw) {
+  if (node < 0 || node >= static_cast<int>(nodes_.size()) || stream < 0 || stream >= S_)
+    throw_invalid("read_state: bad node/stream");
+  const NodeRT& r = nodes_[node];
+  if (!r.state.bytes) throw_invalid("read_state: node has no input state (not a detect-policy conv)");
+  const size_t HW = static_cast<size_t>(r.d.Hi) * r.d.Wi;
+  DevBuf tmp;
+  tmp.alloc(static_cast<size_t>(r.d.Ci) * HW * sizeof(float));
+  launch_nhwc_to_chw(r.state.as<float>() + static_cast<size_t>(stream) * HW * r.Csi, tmp.as<float>(), r.d.Ci, r.Csi,
+                     static_cast<int>(HW), ctx_->stream);
+  CK(cudaMemcpyAsync(out_chw, tmp.p, tmp.bytes, cudaMemcpyDeviceToHost, ctx_->stream));
+  CK(cudaStreamSynchronize(ctx_->stream));
+}
+
+void Net::read_counts(std::vector<int32_t>& counts) {
+  counts.resize(static_cast<size_t>(std::max(1, n_slots_)) * S_);
+  CK(cudaMemcpyAsync(counts.data(), counts_.p, counts.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx_->stream));
+  CK(cudaStreamSynchronize(ctx_->stream));
+}
+
+int64_t Net::count_of(const std::vector<int32_t>& counts, int node, int stream, bool worst) const {
+  const NodeRT& r = nodes_[node];
+  const int slot = worst ? r.wc_slot : r.count_slot;
+  if (slot < 0) return -1;
+  return counts[static_cast<size_t>(slot) * S_ + stream];
+}
+
+void Net::read_changes(int node, int stream, uint8_t* map, int32_t* rowcol, int64_t* count, bool worst) {
+  if (node < 0 || node >= static_cast<int>(nodes_.size()) || stream < 0 || stream >= S_)
+    throw_invalid("read_changes: bad node/stream");
+  const NodeRT& r = nodes_[node];
+  std::vector<int32_t> counts;
+  read_counts(counts);
+  const size_t HW = static_cast<size_t>(r.d.H) * r.d.W;
+  int64_t n = count_of(counts, node, stream, worst);
+  if (worst && r.d.inputs[0] < 0) n = count_of(counts, node, stream, false);  // first layer: own map
+  const int32_t* didx = (worst && r.d.inputs[0] >= 0) ? r.wc_idx.as<int32_t>() : r.idx;
+  std::vector<int32_t> idx(static_cast<size_t>(std::max<int64_t>(n, 0)));
+  if (n > 0)
+    CK(cudaMemcpy(idx.data(), didx + static_cast<size_t>(stream) * HW, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  if (count) *count = n;
+  if (map) {
+    std::memset(map, 0, HW);
+    for (int32_t p : idx) map[p] = 1;
+  }
+  if (rowcol)
+    for (int64_t k = 0; k < n; ++k) {
+      rowcol[2 * k] = idx[k] / r.d.W;
+      rowcol[2 * k + 1] = idx[k] % r.d.W;
+    }
+}
+
+}  // namespace cbg

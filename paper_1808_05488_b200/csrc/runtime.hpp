@@ -1,0 +1,176 @@
+// runtime.hpp — host runtime of the B200 CBinfer path.
+//
+// Mirrors the reference network layer (network.hpp:91-195) with device-resident,
+// multi-stream state:
+//   * Topology   = resolve() + convert_to_cb() (network.cpp:37-133, 416-503),
+//                  host-only, same rules and error categories.
+//   * Net        = CBNetwork for S independent camera streams that share the
+//                  immutable weights; one launch per kernel step covers every
+//                  stream (grid.y = stream), one CUDA graph per frame.
+//   * standalone CBConvLayer / CBPoolLayer are a Net whose producer is an
+//     "external" node fed from host buffers (layers.hpp:45-91).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cbg.h"
+
+namespace cbg {
+
+// Error carrying a cbg status code (cbi::InvalidInputError / ConfigError / ...).
+struct Error : std::runtime_error {
+  int code;
+  Error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] void throw_invalid(const std::string& m);
+[[noreturn]] void throw_config(const std::string& m);
+void cuda_check(cudaError_t e, const char* what);
+
+struct ConvDesc {
+  int in_channels = 0, out_channels = 0, kernel_h = 0, kernel_w = 0, stride = 1, padding = 0;
+  int out_h = 0, out_w = 0;
+  std::vector<float> weights, bias;
+};
+int conv_out_dim(int in_dim, int kernel, int stride, int padding, int pinned);  // tensor.cpp:9-28
+void validate_conv(const ConvDesc& c);                                          // tensor.cpp:30-43
+ConvDesc conv_from_c(const cbg_conv_spec& s);
+
+// One CB node after conversion (CBNode, network.hpp:129-137).
+struct NodeDesc {
+  int kind = CBG_LAYER_CONV;  // CONV / POOL / ADD / CONCAT, or kExternal
+  std::string name;
+  std::vector<int> inputs;    // node ids, -1 = network input
+  int C = 0, H = 0, W = 0;    // out shape
+  int Ci = 0, Hi = 0, Wi = 0; // shape of inputs[0]
+  ConvDesc conv;
+  float tau = 0.0f;
+  int policy = CBG_POLICY_DETECT;
+  bool relu = false;
+  int pool_size = 0, pool_stride = 0;
+};
+constexpr int kExternal = -100;
+
+struct Topology {
+  int C = 0, H = 0, W = 0;  // network input
+  int mode = CBG_MODE_CLOSEDLOOP;
+  std::vector<NodeDesc> nodes;
+};
+// resolve + convert_to_cb, throwing Error with the reference's categories.
+Topology convert(const cbg_network_spec& spec, const float* taus, int n_taus, const int* policies, int mode);
+
+// ---- device resources ---------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept;
+  ~DevBuf();
+  void alloc(size_t n);  // zero-initialised
+  template <class T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct Ctx {
+  int device = 0;
+  int sm_count = 148;
+  cudaStream_t stream = nullptr;
+  explicit Ctx(int dev);
+  ~Ctx();
+};
+
+struct NodeRT {
+  NodeDesc d;
+  int Cs = 0, Csi = 0;           // padded channel strides (out / in)
+  // conv
+  int npad = 0, n_tiles = 0, KB = 0;
+  DevBuf wimg, ktab, bias;
+  DevBuf state, inmap;           // Detect policy
+  // every node
+  DevBuf out;                    // [S][H][W][Cs]
+  DevBuf outmap_own, idx_own, tilestat;
+  uint8_t* outmap = nullptr;     // may alias the producer (Reuse1x1)
+  int32_t* idx = nullptr;
+  int count_slot = 0;            // index into Net::counts ([slot][S])
+  int dc_rows = 1, dc_tiles = 1, dc_smem = 0;
+  // worst-case map (record_worst_case)
+  DevBuf wc_map, wc_idx, wc_tilestat;
+  int wc_slot = -1;
+  int dc_wc_rows = 1, dc_wc_tiles = 1, dc_wc_smem = 0;
+};
+
+class Net {
+ public:
+  Net(Ctx* ctx, Topology topo, int n_streams);
+  ~Net();
+  Net(const Net&) = delete;
+  Net& operator=(const Net&) = delete;
+  std::unique_ptr<Net> clone() const;
+
+  int streams() const { return S_; }
+  const Topology& topology() const { return topo_; }
+  const std::vector<NodeRT>& nodes() const { return nodes_; }
+
+  void forward(const float* frames, unsigned flags);
+  // standalone layers: external producer contents (node 0 must be kExternal)
+  void set_external(const float* x_chw, const uint8_t* map, const int32_t* rowcol, int64_t n, bool full = false);
+  void reset(int stream);
+  void set_thresholds(const std::vector<float>& taus);
+  std::vector<float> thresholds() const;
+  void set_dense(bool dense);
+
+  void read_output(int node, int stream, float* out_chw);
+  void read_state(int node, int stream, float* out_chw);
+  void read_changes(int node, int stream, uint8_t* map, int32_t* rowcol, int64_t* count, bool worst = false);
+  void read_counts(std::vector<int32_t>& counts);  // [slot][S]
+  int64_t count_of(const std::vector<int32_t>& counts, int node, int stream, bool worst = false) const;
+  bool has_worst_case(int node) const { return nodes_[node].wc_slot >= 0 && last_flags_ & CBG_FWD_RECORD_WORST_CASE; }
+
+  int last_launches() const { return last_launches_; }
+  // Per-kernel CUDA-event timing (eager launches, one sync per frame): label
+  // "<node>.<kernel>" -> accumulated ms and launch count. Instrumentation only.
+  void set_timing(bool on);
+  std::string timing_report() const;  // JSON object
+  void copy_output_async(int node, void* host_dst);  // raw NHWC [S][H][W][Cs] on the ctx stream
+  void copy_counts_async(int32_t* host_dst);         // [slot][S] on the ctx stream
+  int count_slots() const { return n_slots_; }
+  int node_slot(int node) const { return nodes_[node].count_slot; }
+
+ private:
+  void build();
+  void enqueue_frame(unsigned flags);  // kernels of one frame (graph body)
+  int launch_count(unsigned flags) const;
+  void clear_maps();
+
+  Ctx* ctx_;
+  Topology topo_;
+  int S_;
+  std::vector<NodeRT> nodes_;
+  DevBuf frame_, frame_slot_, frame_ctr_, boot_req_, boot_now_, dense_flag_, rescan_req_, rescan_now_,
+      taus_, counts_;
+  int n_slots_ = 0;
+  uint32_t host_frame_ = 0;
+  unsigned last_flags_ = 0;
+  int last_launches_ = 0;
+  std::map<unsigned, cudaGraphExec_t> graphs_;
+  std::vector<float> host_taus_;
+  bool dense_ = false;
+  // kernel timing (bench instrumentation)
+  template <class F> void timed(const std::string& label, F&& launch);
+  bool timing_ = false;
+  std::vector<cudaEvent_t> ev_pool_;
+  std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending_;
+  std::map<std::string, std::pair<double, long long>> times_;
+  int timed_frames_ = 0;
+  const float* slot_value_ = nullptr;
+};
+
+}  // namespace cbg

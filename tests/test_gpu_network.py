@@ -1,0 +1,136 @@
+"""GPU parity: CBNetwork (multi-stream, CUDA-graph frame step) vs the reference
+CBNetwork on identical gen_synthetic sequences.
+
+Parity contract: layer-1 change maps / index lists bit-exact
+frame by frame; per-layer mask agreement reported for deeper layers; final
+maps within max_rel_err <= TOL_NET.
+"""
+import numpy as np
+import pytest
+
+from paper_1808_05488_b200 import cbi
+from tests import oracle
+
+pytestmark = pytest.mark.gpu
+
+TOL_NET = 1e-4
+
+
+def seq(h, w, n=6, seed=7, objects=3, size=10, vel=3, noise=0.0, c=3):
+    return cbi.gen_synthetic(cbi.SyntheticConfig(h, w, c, n, objects, size, vel, vel, noise, seed))
+
+
+def compare_run(spec, taus, frames, policies=None, mode=cbi.DetectMode.ClosedLoop, tol=TOL_NET):
+    net = cbi.convert_to_cb(spec, taus, policies, mode)
+    ref = oracle.RefNet(spec, taus, policies, mode)
+    agree = []
+    for t, f in enumerate(frames):
+        got = net.forward_frame(f)
+        want = ref.forward(f)
+        for i in range(len(net.nodes())):
+            gm, gi = net.node_changes(i)
+            st = ref.stats(i)
+            if i == 0:
+                assert np.array_equal(gm, st["map"]), f"frame {t}: layer-1 map differs"
+                assert len(gi) == st["changed_px"]
+            agree.append(float(np.mean(gm == st["map"])))
+        err = oracle.max_rel_err(got, want)
+        assert err <= tol, f"frame {t}: max_rel_err {err}"
+    return net, ref, agree
+
+
+def test_seg_net_small_resolution(gpu):
+    spec = cbi.make_seg_spec(1, 96, 128)
+    net, ref, agree = compare_run(spec, [0.05] * 5, seq(96, 128))
+    assert min(agree) >= 0.999
+
+
+def test_seg_net_every_node_matches(gpu):
+    spec = cbi.make_seg_spec(3, 80, 96)
+    taus = [0.04, 0.05, 0.05, 0.03, 0.02]
+    net = cbi.convert_to_cb(spec, taus)
+    ref = oracle.RefNet(spec, taus)
+    for t, f in enumerate(seq(80, 96, n=5, seed=11, noise=0.004)):
+        net.forward_frame(f)
+        ref.forward(f)
+        for i, n in enumerate(net.nodes()):
+            assert oracle.max_rel_err(net.node_output(i), ref.output(i)) <= TOL_NET, (t, n.name)
+        gm, gi = net.node_changes(0)
+        wm = ref.stats(0)["map"]
+        assert np.array_equal(gm, wm)
+        assert np.array_equal(gi, np.argwhere(wm).astype(np.int32))
+
+
+def test_zero_threshold_equivalence_to_dense(gpu):
+    """acceptance C1: tau = 0 => CB output == dense output (within TOL)."""
+    rng = np.random.default_rng(101)
+    for rnd in range(6):
+        h, w = int(rng.integers(12, 33)), int(rng.integers(12, 33))
+        spec = cbi.make_small_spec(int(rng.integers(1, 1000)), 2, h, w)
+        net = cbi.convert_to_cb(spec, [0.0] * 3)
+        ref = oracle.RefNet(spec, [0.0] * 3)
+        x = rng.uniform(0, 1, (2, h, w)).astype(np.float32)
+        for t in range(6):
+            got = net.forward_frame(x)
+            assert oracle.max_rel_err(got, ref.dense_forward(x)) <= 2e-5
+            x = x.copy()
+            n = int(rng.integers(0, h * w // 8 + 1))
+            x[:, rng.integers(0, h, n), rng.integers(0, w, n)] = rng.uniform(0, 1, (2, n)).astype(np.float32)
+
+
+def test_multi_stream_matches_independent_references(gpu):
+    """S streams in one stream set == S independent reference CBNetworks."""
+    S, H, W = 3, 64, 80
+    spec = cbi.make_seg_spec(5, H, W)
+    taus = [0.05] * 5
+    seqs = [seq(H, W, n=4, seed=1000 + s) for s in range(S)]
+    net = cbi.convert_to_cb(spec, taus, n_streams=S)
+    refs = [oracle.RefNet(spec, taus) for _ in range(S)]
+    for t in range(4):
+        batch = np.stack([seqs[s][t] for s in range(S)])
+        net.enqueue(batch)
+        counts = net.counts()
+        for s in range(S):
+            want = refs[s].forward(seqs[s][t])
+            assert oracle.max_rel_err(net.output(s), want) <= TOL_NET
+            assert counts[0, s] == refs[s].stats(0)["changed_px"]
+
+
+def test_reset_and_thresholds(gpu):
+    spec = cbi.make_small_spec(6, 2, 32, 32)
+    frames = seq(32, 32, n=6, seed=9, objects=1, size=6, vel=1, noise=0.01, c=2)
+    net = cbi.convert_to_cb(spec, [0.02] * 3)
+    a = [net.forward_frame(f).copy() for f in frames]
+    ca = [net.counts().copy() for _ in range(1)]
+    net.reset()
+    b = [net.forward_frame(f).copy() for f in frames]
+    for x, y in zip(a, b):
+        assert np.array_equal(x, y)
+    # thresholds: lower tau without reset must re-detect exactly like the reference
+    ref = oracle.RefNet(spec, [0.02] * 3)
+    net2 = cbi.convert_to_cb(spec, [0.02] * 3)
+    for f in frames[:3]:
+        ref.forward(f)
+        net2.forward_frame(f)
+    ref.set_thresholds([0.001, 0.001, 0.001])
+    net2.set_thresholds([0.001, 0.001, 0.001])
+    assert net2.thresholds() == pytest.approx([0.001] * 3)
+    for f in frames[3:]:
+        want = ref.forward(f)
+        got = net2.forward_frame(f)
+        for i in range(len(net2.nodes())):
+            assert len(net2.node_changes(i)[1]) == ref.stats(i)["changed_px"]
+        assert oracle.max_rel_err(got, want) <= TOL_NET
+    del ca
+
+
+def test_identical_second_frame_changes_nothing(gpu):
+    """test_network.cpp:108-128 at pinned seg7 dims (776x1040)."""
+    spec = cbi.make_seg7_spec(3)
+    net = cbi.convert_to_cb(spec, [0.0] * 5)
+    rng = np.random.default_rng(41)
+    frame = rng.uniform(0, 1, (3, 776, 1040)).astype(np.float32)
+    out = net.forward_frame(frame)
+    assert out.shape == (8, 136, 218) and np.all(np.isfinite(out))
+    net.forward_frame(frame)
+    assert np.all(net.counts() == 0)
