@@ -118,45 +118,65 @@ def reference_arm(a, rank, world):
 # clocks
 # ---------------------------------------------------------------------------
 class ClockSampler:
-    def __init__(self, index):
-        self.index = index
+    """Polls NVML (SM clock, max clock, clock-event reasons) every ~1 ms in a
+    thread while the timed region runs (nvidia-smi -lms cannot resolve a
+    region of a few tens of ms)."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown",
+               0x4: "sw_power_cap"}
+
+    def __init__(self, local_rank):
+        self.local = local_rank
         self.rows = []
-        self.proc = None
+        self.stop = threading.Event()
+        self.handle = None
+        self.max_mhz = None
+
+    def _open(self):
+        import pynvml
+        pynvml.nvmlInit()
+        self.nv = pynvml
+        try:
+            import torch
+            pr = torch.cuda.get_device_properties(self.local)
+            bus = f"{pr.pci_domain_id:08x}:{pr.pci_bus_id:02x}:{pr.pci_device_id:02x}.0"
+            self.handle = pynvml.nvmlDeviceGetHandleByPciBusId(bus)
+        except Exception:
+            self.handle = pynvml.nvmlDeviceGetHandleByIndex(self.local)
+        self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.handle, pynvml.NVML_CLOCK_SM)
+
+    def _poll(self):
+        nv = self.nv
+        get_reasons = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+            nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop.is_set():
+            try:
+                self.rows.append((nv.nvmlDeviceGetClockInfo(self.handle, nv.NVML_CLOCK_SM),
+                                  get_reasons(self.handle)))
+            except Exception:
+                pass
+            time.sleep(0.001)
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,utilization.gpu")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
-                                          "--format=csv,noheader,nounits", "-lms", "100"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.thread = threading.Thread(target=self._read, daemon=True)
+            self._open()
+            self.thread = threading.Thread(target=self._poll, daemon=True)
             self.thread.start()
-        except OSError:
-            self.proc = None
+        except Exception:
+            self.handle = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
-
     def __exit__(self, *exc):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        self.stop.set()
+        if self.handle is not None:
+            self.thread.join(timeout=2)
 
     def summary(self):
         if not self.rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 2 + i and r[2 + i] == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": ["unsampled"], "samples": 0}
+        reasons = sorted({name for _, r in self.rows for bit, name in self.REASONS.items() if r & bit})
+        return {"sm_mhz": statistics.median(c for c, _ in self.rows), "sm_max_mhz": self.max_mhz,
+                "reasons": reasons, "samples": len(self.rows), "source": "nvml, ~1 ms polling in the timed region"}
 
 
 # ---------------------------------------------------------------------------
@@ -168,8 +188,8 @@ def kernel_work(node, kernel, n_out, n_up, S_counts):
     kind, name, cin, hin, win, cout, hout, wout, k, ops_pp = node
     b = f = 0.0
     for s in range(S_counts):
-        no = n_out[s]
-        nu = n_up[s] if n_up is not None else None
+        no = int(n_out[s])
+        nu = int(n_up[s]) if n_up is not None else None
         if kernel == "detect":
             if nu is None:  # dense scan of the network input: read x and state
                 b += 8.0 * cin * hin * win
@@ -289,7 +309,7 @@ def main():
             kk = 0
             if n.kind == cbi.LayerKind.Conv:
                 kk = int(round((n.ops_per_pixel / (2 * cout * max(1, cin))) ** 0.5))
-            desc = (n.kind, n.name, cin, hin, win, cout, hout, wout, kk, n.ops_per_pixel)
+            desc = (n.kind, n.name, cin, hin, win, cout, hout, wout, kk, int(n.ops_per_pixel))
             n_out = c[node_slot[i]]
             n_up = c[node_slot[src]] if src >= 0 else None
             for kern in ("detect", "dilcomp", "gemm", "pool"):

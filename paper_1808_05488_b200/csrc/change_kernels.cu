@@ -46,6 +46,7 @@ int sm_count() {
 // detect on the network-input frame. One thread per pixel: the C channel
 // planes are read coalesced, the NHWC state as one 16-B vector per 4 channels.
 // ---------------------------------------------------------------------------
+template <bool kVec4>
 __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs a) {
   const int s = blockIdx.y;
   const uint8_t e = epoch8(*a.frame);
@@ -56,6 +57,45 @@ __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs 
   uint8_t* m = a.map + static_cast<long long>(s) * HW;
   const bool write_all = boot || !a.closed_loop;
   const float tau = *a.tau;
+  if constexpr (kVec4) {
+    // C <= 4 (Cs == 4), HW % 4 == 0: one thread = 4 consecutive pixels; the C
+    // planes are read as float4, the 4 NHWC state vectors as 4 float4.
+    const long long n4 = HW >> 2;
+    for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
+         q += static_cast<long long>(gridDim.x) * blockDim.x) {
+      const long long p0 = q << 2;
+      float4 xv[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        xv[c] = c < a.C ? ldg_nc_f4(x + c * HW + p0) : make_float4(0.f, 0.f, 0.f, 0.f);
+      float4 sv[4];
+      if (!boot) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sv[j] = *reinterpret_cast<const float4*>(st + (p0 + j) * 4);
+      }
+      uint32_t mark = 0;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float px[4] = {(&xv[0].x)[j], (&xv[1].x)[j], (&xv[2].x)[j], (&xv[3].x)[j]};
+        bool changed = false;
+        if (!boot) {
+          const float sp[4] = {sv[j].x, sv[j].y, sv[j].z, sv[j].w};
+#pragma unroll
+          for (int c = 0; c < 4; ++c)
+            if (c < a.C) changed |= fabsf(px[c] - sp[c]) > tau;
+        }
+        if (changed || write_all)
+          *reinterpret_cast<float4*>(st + (p0 + j) * 4) = make_float4(px[0], px[1], px[2], px[3]);
+        if (changed) mark |= static_cast<uint32_t>(e) << (8 * j);
+      }
+      if (mark) {  // only changed pixels get the epoch tag; others keep stale tags
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if ((mark >> (8 * j)) & 0xffu) m[p0 + j] = e;
+      }
+    }
+    return;
+  }
   for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < HW;
        p += static_cast<long long>(gridDim.x) * blockDim.x) {
     float* sp = st + p * a.Cs;
@@ -171,93 +211,186 @@ constexpr uint64_t kFlagAgg = 1ull << 30;
 constexpr uint64_t kFlagInc = 2ull << 30;
 constexpr uint64_t kValMask = (1ull << 30) - 1;
 
+CBG_DEV uint64_t ld_relaxed_u64(const uint64_t* p) {
+  uint64_t v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+
+// 32 bits of a bit-row starting at bit position B (bits outside [0, 32*nw) are 0).
+CBG_DEV uint32_t bits_at(const uint32_t* row, int nw, int B) {
+  const int w = B >> 5, o = B & 31;  // arithmetic shift: floor for negative B
+  const uint32_t lo = (w >= 0 && w < nw) ? row[w] : 0u;
+  if (o == 0) return lo;
+  const uint32_t hi = (w + 1 >= 0 && w + 1 < nw) ? row[w + 1] : 0u;
+  return __funnelshift_r(lo, hi, o);
+}
+
+// even bits of a 64-bit value (hi:lo) compacted into 32 bits
+CBG_DEV uint32_t even_bits(uint32_t lo, uint32_t hi) {
+  auto squeeze = [](uint32_t x) {
+    x &= 0x55555555u;
+    x = (x | (x >> 1)) & 0x33333333u;
+    x = (x | (x >> 2)) & 0x0F0F0F0Fu;
+    x = (x | (x >> 4)) & 0x00FF00FFu;
+    x = (x | (x >> 8)) & 0x0000FFFFu;
+    return x;
+  };
+  return squeeze(lo) | (squeeze(hi) << 16);
+}
+
+// Tile = rows_per_tile output rows. Maps are staged as bit-rows (32 pixels per
+// word, built with warp ballots), dilated separably in the bit domain
+// (horizontal: funnel-shift ORs, vertical: word ORs), counted with popc and
+// compacted in row-major order with a single-pass decoupled look-back.
 __global__ void __launch_bounds__(kThreads) dilate_compact_kernel(DilateCompactArgs a) {
-  extern __shared__ __align__(16) uint8_t sm[];
+  extern __shared__ __align__(16) uint32_t smw[];
   __shared__ int s_warp[33];
   __shared__ int s_prefix;
   const int s = blockIdx.y, t = blockIdx.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
   const uint32_t f = *a.frame;
   const uint8_t e = epoch8(f);
   const bool boot = a.boot[s] != 0;
   const int r0 = t * a.rows_per_tile;
   const int r1 = min(r0 + a.rows_per_tile, a.Hout);
-  const int npix = (r1 - r0) * a.Wout;
+  const int nrows = r1 - r0;
   const long long HWin = static_cast<long long>(a.Hin) * a.Win;
   const long long HWout = static_cast<long long>(a.Hout) * a.Wout;
-
+  const int nwi = (a.Win + 31) >> 5, nwo = (a.Wout + 31) >> 5;
   const int in_lo = max(0, r0 * a.stride - a.pad);
   const int in_hi = min(a.Hin, (r1 - 1) * a.stride - a.pad + a.kh);
   const int nin = max(0, in_hi - in_lo);
-  uint8_t* s_in = sm;
-  uint8_t* s_h = sm + ((nin * a.Win + 15) & ~15);
-  if (!boot && nin > 0) {
-    for (int i = threadIdx.x; i < nin * a.Win; i += blockDim.x) {
-      const long long g = static_cast<long long>(in_lo) * a.Win + i;
-      uint8_t v = 0;
-      for (int q = 0; q < a.n_in; ++q) v |= (a.in_map[q][s * HWin + g] == e);
-      s_in[i] = v;
+  uint32_t* s_in = smw;                 // [nin][nwi]
+  uint32_t* s_h = smw + nin * nwi;      // [nin][nwo]
+  uint32_t* s_out = s_h + nin * nwo;    // [nrows][nwo]
+  const int nout = nrows * nwo;
+
+  if (boot) {
+    for (int i = threadIdx.x; i < nout; i += blockDim.x) {
+      const int wo = i % nwo;
+      const int valid = min(32, a.Wout - wo * 32);
+      s_out[i] = valid >= 32 ? 0xffffffffu : ((1u << valid) - 1u);
+    }
+  } else {
+    // 1. stage input rows as bits: one thread per 32-pixel word, 32
+    //    independent byte loads in flight per thread
+    for (int i = threadIdx.x; i < nin * nwi; i += blockDim.x) {
+      const int r = i / nwi, w = i - r * nwi;
+      const long long rowoff = static_cast<long long>(s) * HWin + static_cast<long long>(in_lo + r) * a.Win;
+      const int c0 = w * 32, n = min(32, a.Win - c0);
+      uint32_t word = 0;
+      for (int q = 0; q < a.n_in; ++q) {
+        const uint8_t* src = a.in_map[q] + rowoff + c0;
+        uint8_t v[32];
+#pragma unroll
+        for (int b = 0; b < 32; ++b) v[b] = b < n ? src[b] : 0;
+#pragma unroll
+        for (int b = 0; b < 32; ++b) word |= static_cast<uint32_t>(v[b] == e) << b;
+      }
+      s_in[i] = word;
     }
     __syncthreads();
-    for (int i = threadIdx.x; i < nin * a.Wout; i += blockDim.x) {
-      const int r = i / a.Wout, io = i - r * a.Wout;
-      const int c0 = io * a.stride - a.pad;
-      const int ca = max(c0, 0), cb = min(c0 + a.kw, a.Win);
-      uint8_t v = 0;
-      for (int c = ca; c < cb; ++c) v |= s_in[r * a.Win + c];
+    // 2. horizontal dilation (+ stride subsampling) per staged row
+    for (int i = threadIdx.x; i < nin * nwo; i += blockDim.x) {
+      const int r = i / nwo, wo = i - r * nwo;
+      const uint32_t* row = s_in + r * nwi;
+      uint32_t v = 0;
+      if (a.stride == 1) {
+        for (int ki = 0; ki < a.kw; ++ki) v |= bits_at(row, nwi, wo * 32 - a.pad + ki);
+      } else if (a.stride == 2) {
+        uint32_t lo = 0, hi = 0;
+        const int B0 = wo * 64 - a.pad;
+        for (int ki = 0; ki < a.kw; ++ki) {
+          lo |= bits_at(row, nwi, B0 + ki);
+          hi |= bits_at(row, nwi, B0 + 32 + ki);
+        }
+        v = even_bits(lo, hi);
+      } else {
+        for (int b = 0; b < 32; ++b) {
+          const int io = wo * 32 + b;
+          bool hit = false;
+          for (int ki = 0; ki < a.kw && !hit; ++ki) {
+            const int c = io * a.stride - a.pad + ki;
+            hit = c >= 0 && c < a.Win && ((row[c >> 5] >> (c & 31)) & 1u);
+          }
+          v |= static_cast<uint32_t>(hit) << b;
+        }
+      }
+      const int valid = a.Wout - wo * 32;  // clear bits past the row end
+      if (valid < 32) v &= (1u << max(valid, 0)) - 1u;
       s_h[i] = v;
     }
     __syncthreads();
-  }
-
-  // this thread's run of consecutive tile pixels
-  const int per = (npix + blockDim.x - 1) / blockDim.x;
-  const int my0 = min(threadIdx.x * per, npix), my1 = min(my0 + per, npix);
-  uint32_t bits = 0;
-  for (int q = my0; q < my1; ++q) {
-    bool set = boot;
-    if (!boot && nin > 0) {
-      const int jo = r0 + q / a.Wout, io = q % a.Wout;
+    // 3. vertical dilation
+    for (int i = threadIdx.x; i < nout; i += blockDim.x) {
+      const int rr = i / nwo, wo = i - rr * nwo;
+      const int jo = r0 + rr;
       const int ja = max(jo * a.stride - a.pad, 0), jb = min(jo * a.stride - a.pad + a.kh, a.Hin);
-      for (int jj = ja; jj < jb && !set; ++jj) set = s_h[(jj - in_lo) * a.Wout + io] != 0;
+      uint32_t v = 0;
+      for (int jj = ja; jj < jb; ++jj) v |= s_h[(jj - in_lo) * nwo + wo];
+      s_out[i] = v;
     }
-    bits |= static_cast<uint32_t>(set) << (q - my0);
-  }
-  int agg = 0;
-  const int off = block_exclusive_scan(__popc(bits), s_warp, agg);
-
-  // decoupled look-back over the tiles of this stream
-  uint64_t* stat = a.tile_status + static_cast<long long>(s) * a.n_tiles;
-  const uint64_t tag = static_cast<uint64_t>(f) << 32;
-  if (threadIdx.x == 0) {
-    int prefix = 0;
-    if (t == 0) {
-      st_release_u64(&stat[0], tag | kFlagInc | static_cast<uint64_t>(agg));
-    } else {
-      st_release_u64(&stat[t], tag | kFlagAgg | static_cast<uint64_t>(agg));
-      for (int j = t - 1; j >= 0; --j) {
-        uint64_t v;
-        do {
-          v = ld_acquire_u64(&stat[j]);
-        } while ((v >> 32) != f);
-        prefix += static_cast<int>(v & kValMask);
-        if ((v & kFlagInc) == kFlagInc) break;
-      }
-      st_release_u64(&stat[t], tag | kFlagInc | static_cast<uint64_t>(prefix + agg));
-    }
-    s_prefix = prefix;
-    if (t == a.n_tiles - 1) a.count[s] = prefix + agg;
   }
   __syncthreads();
+
+  // 4. count (contiguous run of words per thread) + block scan
+  const int per = (nout + blockDim.x - 1) / blockDim.x;
+  const int w0 = min(static_cast<int>(threadIdx.x) * per, nout), w1 = min(w0 + per, nout);
+  int mine = 0;
+  for (int i = w0; i < w1; ++i) mine += __popc(s_out[i]);
+  int agg = 0;
+  const int off = block_exclusive_scan(mine, s_warp, agg);
+
+  // 5. decoupled look-back (one warp, 32 predecessors per step). The status
+  //    word carries its value, so relaxed polling suffices (no L1 invalidation).
+  uint64_t* stat = a.tile_status + static_cast<long long>(s) * a.n_tiles;
+  const uint64_t tag = static_cast<uint64_t>(f) << 32;
+  if (warp == 0) {
+    int prefix = 0;
+    if (t == 0) {
+      if (lane == 0) st_release_u64(&stat[0], tag | kFlagInc | static_cast<uint64_t>(agg));
+    } else {
+      if (lane == 0) st_release_u64(&stat[t], tag | kFlagAgg | static_cast<uint64_t>(agg));
+      for (int j = t - 1;; j -= 32) {
+        const int q = j - lane;
+        uint64_t v = 0;
+        if (q >= 0) {
+          do {
+            v = ld_relaxed_u64(&stat[q]);
+          } while ((v >> 32) != f);
+        }
+        const unsigned inc = __ballot_sync(0xffffffffu, q >= 0 && (v & kFlagInc) == kFlagInc);
+        int val = q >= 0 ? static_cast<int>(v & kValMask) : 0;
+        if (inc) val = lane <= (__ffs(inc) - 1) ? val : 0;  // up to the nearest inclusive predecessor
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        prefix += val;
+        if (inc) break;  // tile 0 is always inclusive, so this terminates
+      }
+      if (lane == 0) st_release_u64(&stat[t], tag | kFlagInc | static_cast<uint64_t>(prefix + agg));
+    }
+    if (lane == 0) {
+      s_prefix = prefix;
+      if (t == a.n_tiles - 1) a.count[s] = prefix + agg;
+    }
+  }
+  __syncthreads();
+
+  // 6. scatter the row-major index list and tag the output map
   int pos = s_prefix + off;
   int32_t* idx = a.idx + s * HWout;
   uint8_t* om = a.out_map + s * HWout;
-  const int gbase = r0 * a.Wout;
-  while (bits) {
-    const int q = __ffs(bits) - 1;
-    bits &= bits - 1;
-    const int p = gbase + my0 + q;
-    idx[pos++] = p;
-    om[p] = e;
+  for (int i = w0; i < w1; ++i) {
+    uint32_t bits = s_out[i];
+    const int rr = i / nwo, wo = i - rr * nwo;
+    const int base = (r0 + rr) * a.Wout + wo * 32;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      idx[pos++] = base + b;
+      om[base + b] = e;
+    }
   }
 }
 
@@ -370,8 +503,13 @@ int group_log2(int Cs) {
 
 void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
   const long long HW = static_cast<long long>(a.H) * a.W;
-  dim3 grid(blocks_for(HW, kThreads, a.S, sm_count()), a.S);
-  detect_frame_kernel<<<grid, kThreads, 0, st>>>(a);
+  if (a.Cs == 4 && HW % 4 == 0) {
+    dim3 grid(blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
+    detect_frame_kernel<true><<<grid, kThreads, 0, st>>>(a);
+  } else {
+    dim3 grid(blocks_for(HW, kThreads, a.S, sm_count()), a.S);
+    detect_frame_kernel<false><<<grid, kThreads, 0, st>>>(a);
+  }
 }
 
 void launch_detect_list(const DetectListArgs& a, cudaStream_t st) {
@@ -384,7 +522,8 @@ void launch_detect_list(const DetectListArgs& a, cudaStream_t st) {
 
 int dilate_compact_smem(int Win, int Wout, int rows_per_tile, int kh, int stride) {
   const int nin = (rows_per_tile - 1) * stride + kh;
-  return ((nin * Win + 15) & ~15) + nin * Wout;
+  const int nwi = (Win + 31) / 32, nwo = (Wout + 31) / 32;
+  return 4 * (nin * nwi + nin * nwo + rows_per_tile * nwo);
 }
 
 void launch_dilate_compact(const DilateCompactArgs& a, cudaStream_t st) {

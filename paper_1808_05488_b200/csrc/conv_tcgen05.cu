@@ -15,13 +15,15 @@
 // tcgen05.mma kind::tf32 with fp32 accumulation in TMEM — near-fp32 accuracy,
 // the same precision on the sparse and the dense (full-update) path.
 //
-// Warp roles (288 threads, 1 CTA/SM, persistent over (stream, m-tile, n-tile)):
-//   warps 0-3  epilogue: tcgen05.ld TMEM -> +bias -> ReLU -> scatter (lane = row)
-//   warps 4-7  producers: gather the A tile (changed pixels' receptive fields)
-//              with 16-B loads, split hi/lo, st.shared into the UMMA SW128
-//              K-major layout; thread 128 also streams the pre-swizzled B
-//              (weight) image of the K-block with a bulk copy on the TMA engine
-//   warp 8     TMEM allocator + single-thread tcgen05.mma issuer
+// Warp roles (416 threads, 1 CTA/SM, persistent over (stream, m-tile, n-tile)):
+//   warps 0-3   epilogue: tcgen05.ld TMEM -> +bias -> ReLU -> scatter (lane = row)
+//   warps 4-11  producers: gather the A tile (changed pixels' receptive fields)
+//               with 16-B loads, split hi/lo, st.shared into the UMMA SW128
+//               K-major layout. Loads of K-block kb+1 are issued before the
+//               split/stores of kb (register double buffering) so the gather
+//               latency overlaps. Producer 0 also streams the pre-swizzled B
+//               (weight) image of each K-block with a bulk copy on the TMA engine.
+//   warp 12     TMEM allocator + single-thread tcgen05.mma issuer
 // Pipelines: smem stages full/empty (producers <-> MMA), two TMEM accumulators
 // full/empty (MMA <-> epilogue) so tile t's epilogue overlaps tile t+1's MMAs.
 #include <climits>
@@ -34,7 +36,11 @@ namespace cbg {
 
 namespace {
 
-constexpr int kThreads = 288;
+constexpr int kProdWarps = 8;
+constexpr int kProd = kProdWarps * 32;
+constexpr int kMmaWarp = 4 + kProdWarps;
+constexpr int kThreads = (kMmaWarp + 1) * 32;
+constexpr int kChunks = 128 * 8 / kProd;  // 16-B A chunks per producer thread per K-block
 constexpr int kBM = 128;                 // UMMA M
 constexpr int kBK = 32;                  // fp32 elements per K-block (= one 128-B swizzle row)
 constexpr int kABytes = kBM * kBK * 4;   // one of A_hi / A_lo: 16 KB
@@ -76,7 +82,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   // ---- setup -----------------------------------------------------------------
   if (tid == 0) {
     for (int i = 0; i < C::kStages; ++i) {
-      mbar_init(&full[i], 4 + 1);  // 4 producer warps + 1 expect_tx arrive
+      mbar_init(&full[i], kProdWarps + 1);  // producer warps + 1 expect_tx arrive
       mbar_init(&empty[i], 1);     // tcgen05.commit
     }
     for (int i = 0; i < 2; ++i) {
@@ -85,7 +91,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     }
     fence_mbar_init();
   }
-  if (warp == 8) tmem_alloc(tmem_holder, C::kTmemCols);
+  if (warp == kMmaWarp) tmem_alloc(tmem_holder, C::kTmemCols);
   for (int i = tid; i < a.KB * 8; i += kThreads) ktab[i] = a.ktab[i];
   if (warp == 0) {
     int carry = 0;
@@ -122,18 +128,19 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     nt = local - mt * a.n_tiles;
   };
 
-  if (warp >= 4 && warp < 8) {
+  if (warp >= 4 && warp < kMmaWarp) {
     // ========================= producers =========================
     const int ptid = tid - 128;
     const int q = ptid & 7;
     int stage = 0;
     uint32_t phase = 0;
+    float4 v[2][kChunks];
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int s, mt, nt;
       decode(w, s, mt, nt);
       const int cnt = a.count[s];
-      named_bar_sync(1, 128);  // every producer is done reading the previous tile's rowinfo
-      {
+      named_bar_sync(1, kProd);  // every producer is done reading the previous tile's rowinfo
+      if (ptid < kBM) {
         const int k = mt * kBM + ptid;
         if (k < cnt) {
           const int p = a.idx[s * HWout + k];
@@ -143,10 +150,32 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
           rowinfo[ptid] = make_int2(INT_MIN / 2, INT_MIN / 2);
         }
       }
-      named_bar_sync(1, 128);
+      named_bar_sync(1, kProd);
       const float* src = a.src + s * HWin * a.Cs;
       const uint8_t* bimg = a.wimg + static_cast<long long>(nt) * a.KB * 2 * C::kBBytes;
+      auto gather = [&](int kb, float4 (&dst)[kChunks]) {
+        const uint32_t tab = ktab[kb * 8 + q];
+        const int dj = tab & 0xFF, di = (tab >> 8) & 0xFF, c0 = (tab >> 16) & 0x7FFF;
+        const bool tap_ok = (tab >> 31) == 0;
+#pragma unroll
+        for (int i = 0; i < kChunks; ++i) {
+          const int r = i * (kProd / 8) + (ptid >> 3);
+          const int2 ri = rowinfo[r];
+          const int jj = ri.x + dj, ii = ri.y + di;
+          const bool ok = tap_ok && static_cast<unsigned>(jj) < static_cast<unsigned>(a.Hin) &&
+                          static_cast<unsigned>(ii) < static_cast<unsigned>(a.Win);
+          dst[i] = ok ? ldg_nc_f4(src + (static_cast<long long>(jj) * a.Win + ii) * a.Cs + c0)
+                      : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      };
+      gather(0, v[0]);
+#pragma unroll 1
       for (int kb = 0; kb < a.KB; ++kb) {
+        const int cur = kb & 1;
+        if (kb + 1 < a.KB) {  // prefetch the next K-block's chunks into the other buffer
+          if (cur == 0) gather(kb + 1, v[1]);
+          else gather(kb + 1, v[0]);
+        }
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sA = smem + stage * C::kStageBytes;
         if (ptid == 0) {
@@ -154,39 +183,29 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
           bulk_g2s(sA + 2 * kABytes, bimg + static_cast<long long>(kb) * 2 * C::kBBytes, 2 * C::kBBytes,
                    &full[stage]);
         }
-        const uint32_t tab = ktab[kb * 8 + q];
-        const int dj = tab & 0xFF, di = (tab >> 8) & 0xFF, c0 = (tab >> 16) & 0x7FFF;
-        const bool tap_ok = (tab >> 31) == 0;
-        float4 v[8];
+        auto store = [&](const float4 (&src4)[kChunks]) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = i * 16 + (ptid >> 3);
-          const int2 ri = rowinfo[r];
-          const int jj = ri.x + dj, ii = ri.y + di;
-          const bool ok = tap_ok && static_cast<unsigned>(jj) < static_cast<unsigned>(a.Hin) &&
-                          static_cast<unsigned>(ii) < static_cast<unsigned>(a.Win);
-          v[i] = ok ? ldg_nc_f4(src + (static_cast<long long>(jj) * a.Win + ii) * a.Cs + c0)
-                    : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
+          for (int i = 0; i < kChunks; ++i) {
+            const int r = i * (kProd / 8) + (ptid >> 3);
+            const uint32_t off = r * 128 + ((q ^ (r & 7)) << 4);
+            const float x[4] = {src4[i].x, src4[i].y, src4[i].z, src4[i].w};
+            uint32_t h[4], l[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const int r = i * 16 + (ptid >> 3);
-          const uint32_t off = r * 128 + ((q ^ (r & 7)) << 4);
-          const float x[4] = {v[i].x, v[i].y, v[i].z, v[i].w};
-          uint32_t h[4], l[4];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            h[j] = tf32_rna(x[j]);
-            l[j] = tf32_rna(x[j] - __uint_as_float(h[j]));
+            for (int j = 0; j < 4; ++j) {
+              h[j] = tf32_rna(x[j]);
+              l[j] = tf32_rna(x[j] - __uint_as_float(h[j]));
+            }
+            const uint32_t dh = smem_u32(sA + off), dl = smem_u32(sA + kABytes + off);
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dh), "r"(h[0]), "r"(h[1]), "r"(h[2]),
+                         "r"(h[3])
+                         : "memory");
+            asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dl), "r"(l[0]), "r"(l[1]), "r"(l[2]),
+                         "r"(l[3])
+                         : "memory");
           }
-          const uint32_t dh = smem_u32(sA + off), dl = smem_u32(sA + kABytes + off);
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dh), "r"(h[0]), "r"(h[1]), "r"(h[2]),
-                       "r"(h[3])
-                       : "memory");
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dl), "r"(l[0]), "r"(l[1]), "r"(l[2]),
-                       "r"(l[3])
-                       : "memory");
-        }
+        };
+        if (cur == 0) store(v[0]);
+        else store(v[1]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[stage]);
@@ -196,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         }
       }
     }
-  } else if (warp == 8) {
+  } else if (warp == kMmaWarp) {
     // ========================= MMA issuer =========================
     if (lane == 0) {
       constexpr uint32_t idesc = umma_idesc_tf32(kBM, NPAD);
@@ -282,7 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
 
   tc_fence_before();
   __syncthreads();
-  if (warp == 8) {
+  if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::kTmemCols);
   }

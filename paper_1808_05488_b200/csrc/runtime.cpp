@@ -361,10 +361,11 @@ void build_weight_image(const NodeRT& n, std::vector<uint8_t>& img, std::vector<
 
 void dc_tiling(int Hin, int Win, int Hout, int Wout, int kh, int stride, int S, int* rows, int* tiles,
                int* smem) {
-  if (Wout > 8192) throw Error(CBG_ERR_UNSUPPORTED, "output width > 8192 not supported by the compaction kernel");
-  int r = std::max(1, std::min(Hout, 4096 / std::max(1, Wout)));
-  // enough tiles to spread a single stream over the SMs
-  while (r > 1 && static_cast<long long>((Hout + r - 1) / r) * S < 296) r = (r + 1) / 2;
+  if (Wout > 65536 || Win > 65536) throw Error(CBG_ERR_UNSUPPORTED, "map width > 65536 not supported");
+  // ~16K output pixels per tile (<= 64 bit-words per thread of a 256-thread
+  // block), but enough tiles to spread the stream set over the SMs
+  int r = std::max(1, std::min(Hout, 16384 / std::max(1, Wout)));
+  while (r > 1 && static_cast<long long>((Hout + r - 1) / r) * S < 148) r = (r + 1) / 2;
   while (r > 1 && dilate_compact_smem(Win, Wout, r, kh, stride) > 48 * 1024) --r;
   *rows = r;
   *tiles = (Hout + r - 1) / r;
