@@ -242,6 +242,10 @@ int cbg_net_output_bytes(cbg_net net, int node, int64_t* bytes);
  * (int32) into host memory; node_slot (nullable) receives each node's slot. */
 int cbg_net_copy_counts_async(cbg_net net, int32_t* host_dst, int32_t* node_slot);
 int cbg_net_count_slots(cbg_net net, int* slots);
+/* Debug builds only (-DCBG_TRACE, libcbg_trace.so): per-K-block clock64 timeline
+ * of CTA 0 of the last GEMM launch, [6][4096]; returns entries copied (0 when
+ * tracing is compiled out). */
+int cbg_debug_gemm_trace(unsigned long long* buf, int n);
 
 #ifdef __cplusplus
 }

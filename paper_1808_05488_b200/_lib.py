@@ -12,7 +12,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libcbg.so")
+# CBG_LIB selects an instrumented build (e.g. libcbg_trace.so) for debugging only
+LIB_PATH = os.path.join(_HERE, os.environ.get("CBG_LIB", "libcbg.so"))
 
 # ---- status codes / enums (include/cbg.h) -----------------------------------
 OK, ERR_INVALID_INPUT, ERR_CONFIG, ERR_CUDA, ERR_OOM, ERR_UNSUPPORTED = range(6)
@@ -132,6 +133,7 @@ SIGNATURES = {
     "cbg_net_output_bytes": (C.c_int, [_vp, C.c_int, _P(C.c_int64)]),
     "cbg_net_copy_counts_async": (C.c_int, [_vp, _vp, _vp]),
     "cbg_net_count_slots": (C.c_int, [_vp, _P(C.c_int)]),
+    "cbg_debug_gemm_trace": (C.c_int, [_vp, C.c_int]),
 }
 
 

@@ -12,6 +12,7 @@
 #include "runtime.hpp"
 
 namespace cbg {
+int conv_gemm_read_trace(unsigned long long* host, int n);
 void gen_synthetic(const cbg_synthetic_config& cfg, float* frames, int32_t* corners);
 void fill_random_weights(const cbg_network_spec& spec, uint32_t seed, float* const* weights, float* const* biases);
 }  // namespace cbg
@@ -329,6 +330,7 @@ int cbg_net_copy_counts_async(cbg_net net, int32_t* host_dst, int32_t* node_slot
     if (host_dst) net->net->copy_counts_async(host_dst);
   });
 }
+int cbg_debug_gemm_trace(unsigned long long* buf, int n) { return cbg::conv_gemm_read_trace(buf, n); }
 int cbg_net_count_slots(cbg_net net, int* slots) {
   return guard([&] {
     need(net, "cbg_net_count_slots");
