@@ -46,7 +46,10 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--streams", type=int, default=16, help="camera streams per GPU")
+    ap.add_argument("--streams", type=int, default=64, help="camera streams per GPU")
+    ap.add_argument("--groups", type=int, default=4,
+                    help="stream groups per GPU, each its own stream set on its own CUDA stream (overlap)")
+    ap.add_argument("--ring", type=int, default=16, help="distinct frames per stream (ping-pong playback)")
     ap.add_argument("--height", type=int, default=480)
     ap.add_argument("--width", type=int, default=640)
     ap.add_argument("--objects", type=int, default=6)
@@ -72,7 +75,8 @@ def config_dict(a, world):
                         f"{a.streams} streams/GPU, gen_synthetic {a.objects}x{a.object_size}px objects "
                         f"v={a.velocity} noise={a.noise}, tau={a.tau}",
             "height": a.height, "width": a.width, "streams_per_gpu": a.streams,
-            "total_streams": a.streams * world, "objects": a.objects, "object_size": a.object_size,
+            "total_streams": a.streams * world, "stream_groups": a.groups, "frame_ring": a.ring,
+            "objects": a.objects, "object_size": a.object_size,
             "velocity": a.velocity, "noise_std": a.noise, "tau": a.tau,
             "parallelism": f"streams sharded over {world} GPU(s), no collective",
             "l2": "inputs larger than L2 (frame ring + per-stream state >> 126 MB)"}
@@ -230,20 +234,30 @@ def main():
             peaks.update(json.load(fh))
         peaks["source"] = "measured (MEASURED_PEAKS.json)"
 
-    S, H, W = a.streams, a.height, a.width
-    ctx = cbi.Context(local)
+    S, H, W, G = a.streams, a.height, a.width, a.groups
+    if S % G:
+        raise SystemExit("--streams must be a multiple of --groups")
+    Sg = S // G
+    ctxs = [cbi.Context(local) for _ in range(G)]
+    ctx = ctxs[0]
     spec = cbi.make_seg_spec(1, H, W)
     taus = [a.tau] * 5
-    n_frames = 1 + a.warmup + a.steps + a.profile_steps + a.dense_steps
-    # frame ring [T][S][C][H][W], pinned on the host and resident in HBM
-    host = torch.empty((n_frames, S, 3, H, W), dtype=torch.float32, pin_memory=True)
+    L = max(3, a.ring)
+    # frame ring [L][S][C][H][W], pinned on the host and resident in HBM; played
+    # ping-pong (1..L-1, L-2..2, ...) so motion stays continuous for any step count
+    host = torch.empty((L, S, 3, H, W), dtype=torch.float32, pin_memory=True)
     hnp = host.numpy()
     for s in range(S):
         g = rank * S + s
-        hnp[:, s] = cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, n_frames, a.objects, a.object_size, a.velocity,
+        hnp[:, s] = cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, L, a.objects, a.object_size, a.velocity,
                                                           a.velocity, a.noise, 1000 + g))
     dev = host.to(f"cuda:{local}")
     torch.cuda.synchronize()
+    order = list(range(1, L)) + list(range(L - 2, 1, -1))
+
+    def frame_at(k):  # frame index of post-bootstrap step k
+        return order[k % len(order)]
+
     frame_bytes = S * 3 * H * W * 4
 
     def barrier():
@@ -257,48 +271,69 @@ def main():
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         return float(t.item())
 
-    ext = torch.cuda.ExternalStream(ctx.stream, device=torch.device("cuda", local))
-    net = cbi.convert_to_cb(spec, taus, n_streams=S, ctx=ctx)
+    exts = [torch.cuda.ExternalStream(c.stream, device=torch.device("cuda", local)) for c in ctxs]
+    ext = exts[0]
+    nets = [cbi.convert_to_cb(spec, taus, n_streams=Sg, ctx=ctxs[g]) for g in range(G)]
+    net = nets[0]
     n_slots, node_slot = net.count_layout()
     nodes = net.nodes()
-    counts_pinned = torch.empty((a.steps + 1, n_slots, S), dtype=torch.int32, pin_memory=True)
+    counts_pinned = torch.empty((G, a.steps + 1, n_slots, Sg), dtype=torch.int32, pin_memory=True)
 
-    def dptr(t):
-        return dev[t].data_ptr()
+    def dptr(t, g):
+        return dev[t, g * Sg].data_ptr()
 
-    # ---- value: frames resident in HBM ---------------------------------------
-    net.enqueue_device(dptr(0))  # bootstrap (untimed)
-    for t in range(1, 1 + a.warmup):
-        net.enqueue_device(dptr(t))
-    ctx.synchronize()
-    barrier()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    with ClockSampler(local) as clocks:
+    def timed_region(step_fn, steps):
+        """device time of `steps` calls of step_fn(k) across all groups (CUDA events)"""
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         t0.record(ext)
-        for k in range(a.steps):
-            net.enqueue_device(dptr(1 + a.warmup + k))
-            net.copy_counts_async(counts_pinned[k].data_ptr())
+        for e in exts[1:]:
+            e.wait_event(t0)
+        for k in range(steps):
+            step_fn(k)
+        for e in exts[1:]:
+            ev = torch.cuda.Event()
+            ev.record(e)
+            ext.wait_event(ev)
         t1.record(ext)
         t1.synchronize()
         torch.cuda.synchronize()
-    ms = max_over_ranks(t0.elapsed_time(t1))
+        return t0.elapsed_time(t1)
+
+    # ---- value: frames resident in HBM ---------------------------------------
+    for g in range(G):
+        nets[g].enqueue_device(dptr(0, g))  # bootstrap (untimed)
+    for k in range(a.warmup):
+        for g in range(G):
+            nets[g].enqueue_device(dptr(frame_at(k), g))
+    for c in ctxs:
+        c.synchronize()
     barrier()
-    launches = net.last_launches()
-    cnt = counts_pinned[:a.steps].numpy()
+    base_k = a.warmup
+
+    def value_step(k):
+        for g in range(G):
+            nets[g].enqueue_device(dptr(frame_at(base_k + k), g))
+            nets[g].copy_counts_async(counts_pinned[g, k].data_ptr())
+
+    with ClockSampler(local) as clocks:
+        ms = max_over_ranks(timed_region(value_step, a.steps))
+    barrier()
+    launches = net.last_launches() * G
+    cnt = np.concatenate([counts_pinned[g, :a.steps].numpy() for g in range(G)], axis=2)
     l1_px = nodes[0].out_shape[1] * nodes[0].out_shape[2]
     l1_frac = float(cnt[:, node_slot[0], :].mean()) / l1_px
     per_layer = {n.name: float(cnt[:, node_slot[i], :].mean()) / (n.out_shape[1] * n.out_shape[2])
                  for i, n in enumerate(nodes)}
     value = S * world * a.steps / (ms / 1000.0)
+    next_k = base_k + a.steps
 
     # ---- roofline: instrumented pass (per-kernel CUDA events) -----------------
     net.set_kernel_timing(True)
     work = {}
-    base_t = 1 + a.warmup + a.steps
-    prof_counts = torch.empty((n_slots, S), dtype=torch.int32, pin_memory=True)
+    prof_counts = torch.empty((n_slots, Sg), dtype=torch.int32, pin_memory=True)
     for k in range(a.profile_steps):
-        net.enqueue_device(dptr(base_t + k))
+        net.enqueue_device(dptr(frame_at(next_k + k), 0))
         net.copy_counts_async(prof_counts.data_ptr())
         ctx.synchronize()
         c = prof_counts.numpy()
@@ -313,7 +348,7 @@ def main():
             n_out = c[node_slot[i]]
             n_up = c[node_slot[src]] if src >= 0 else None
             for kern in ("detect", "dilcomp", "gemm", "pool"):
-                bb, ff = kernel_work(desc, kern, n_out, n_up, S)
+                bb, ff = kernel_work(desc, kern, n_out, n_up, Sg)
                 wsum = work.setdefault(f"{n.name}.{kern}", [0.0, 0.0])
                 wsum[0] += bb
                 wsum[1] += ff
@@ -351,43 +386,47 @@ def main():
     # ---- dense path (same kernels, every frame a full update) -------------------
     dense_fps = None
     if a.dense_steps > 0:
-        dnet = cbi.convert_to_cb(spec, taus, n_streams=S, ctx=ctx)
-        dnet.set_dense(True)
-        dbase = 1 + a.warmup + a.steps + a.profile_steps
-        dnet.enqueue_device(dptr(0))
-        dnet.enqueue_device(dptr(1))
-        ctx.synchronize()
-        t0.record(ext)
-        for k in range(a.dense_steps):
-            dnet.enqueue_device(dptr(dbase + k))
-        t1.record(ext)
-        t1.synchronize()
-        dms = max_over_ranks(t0.elapsed_time(t1))
+        dnets = [cbi.convert_to_cb(spec, taus, n_streams=Sg, ctx=ctxs[g]) for g in range(G)]
+        for g in range(G):
+            dnets[g].set_dense(True)
+            dnets[g].enqueue_device(dptr(0, g))
+            dnets[g].enqueue_device(dptr(1, g))
+        for c in ctxs:
+            c.synchronize()
+
+        def dense_step(k):
+            for g in range(G):
+                dnets[g].enqueue_device(dptr(frame_at(k), g))
+
+        dms = max_over_ranks(timed_region(dense_step, a.dense_steps))
         dense_fps = S * world * a.dense_steps / (dms / 1000.0)
-        del dnet
+        del dnets
 
     # ---- e2e: host frames through the C ABI, H2D + D2H in the timed region -------
     e2e = None
     if not a.no_e2e:
-        enet = cbi.convert_to_cb(spec, taus, n_streams=S, ctx=ctx)
-        out_bytes = enet.output_bytes(-1)
-        out_host = torch.empty(out_bytes // 4, dtype=torch.float32, pin_memory=True)
-        enet.enqueue(hnp[0])
-        for t in range(1, 1 + a.warmup):
-            enet.enqueue(hnp[t])
-        ctx.synchronize()
+        enets = [cbi.convert_to_cb(spec, taus, n_streams=Sg, ctx=ctxs[g]) for g in range(G)]
+        out_bytes = enets[0].output_bytes(-1)
+        out_host = [torch.empty(out_bytes // 4, dtype=torch.float32, pin_memory=True) for _ in range(G)]
+        for g in range(G):
+            enets[g].enqueue(hnp[0, g * Sg:(g + 1) * Sg])
+        for k in range(a.warmup):
+            for g in range(G):
+                enets[g].enqueue(hnp[frame_at(k), g * Sg:(g + 1) * Sg])
+        for c in ctxs:
+            c.synchronize()
         barrier()
-        t0.record(ext)
-        for k in range(a.steps):
-            enet.enqueue(hnp[1 + a.warmup + k])
-            enet.copy_output_async(out_host.data_ptr())
-        t1.record(ext)
-        t1.synchronize()
-        ems = max_over_ranks(t0.elapsed_time(t1))
+
+        def e2e_step(k):
+            for g in range(G):
+                enets[g].enqueue(hnp[frame_at(base_k + k), g * Sg:(g + 1) * Sg])
+                enets[g].copy_output_async(out_host[g].data_ptr())
+
+        ems = max_over_ranks(timed_region(e2e_step, a.steps))
         e2e = {"value": S * world * a.steps / (ems / 1000.0), "unit": "frames/s",
-               "h2d_bytes_per_step": frame_bytes, "d2h_bytes_per_step": out_bytes,
+               "h2d_bytes_per_step": frame_bytes, "d2h_bytes_per_step": out_bytes * G,
                "ms_per_step": ems / a.steps}
-        del enet
+        del enets
 
     # ---- CPU baseline (rank 0, N=1) ---------------------------------------------
     cpu = None

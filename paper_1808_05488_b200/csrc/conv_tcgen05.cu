@@ -42,9 +42,17 @@ namespace cbg {
 
 #ifdef CBG_TRACE
 __device__ unsigned long long g_trace[6][4096];  // [event][g] clock64 of CTA 0
+__device__ unsigned long long g_cta[4][160];     // per CTA: start, setup done, last MMA issued, epilogue done (ns)
+CBG_DEV unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+#define CTA_MARK(ev) do { if (blockIdx.x < 160) g_cta[ev][blockIdx.x] = gtimer(); } while (0)
 #define TRACE(ev, g) do { if (blockIdx.x == 0 && (g) < 4096) g_trace[ev][g] = clock64(); } while (0)
 #else
 #define TRACE(ev, g) do { } while (0)
+#define CTA_MARK(ev) do { } while (0)
 #endif
 
 namespace {
@@ -95,6 +103,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  if (tid == 0) CTA_MARK(0);
   const long long HWin = static_cast<long long>(a.Hin) * a.Win;
   const long long HWout = static_cast<long long>(a.Hout) * a.Wout;
 
@@ -139,6 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
   const int total = tprefix[a.S];
+  if (tid == 0) CTA_MARK(1);
 
   auto decode = [&](int w, int& s, int& mt, int& nt) {
     int lo = 0, hi = a.S;  // find s with tprefix[s] <= w < tprefix[s+1]
@@ -293,6 +303,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (lane == 0) CTA_MARK(2);
   } else if (warp < 4) {
     // ========================= epilogue =========================
     int acc = 0;
@@ -341,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
 
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) CTA_MARK(3);
   if (warp == kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::kTmemCols);
@@ -362,6 +374,9 @@ void launch_impl(const ConvGemmArgs& a, cudaStream_t st) {
 
 int conv_gemm_read_trace(unsigned long long* host, int n) {
 #ifdef CBG_TRACE
+  if (n >= 6 * 4096 + 4 * 160) {
+    if (cudaMemcpyFromSymbol(host + 6 * 4096, g_cta, sizeof(unsigned long long) * 4 * 160) != cudaSuccess) return -1;
+  }
   return cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * 6 * 4096) == cudaSuccess ? 6 * 4096 : -1;
 #else
   (void)host;
