@@ -226,6 +226,8 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     from paper_1808_05488_b200 import cbi
+    from paper_1808_05488_b200.sharding import max_over_ranks as _max_over_ranks
+    from paper_1808_05488_b200.sharding import weak_shard
 
     peaks = {"hbm_gbs": 6538.6, "bf16_tflops": 1661.9, "bf16_tflops_sustained": 1399.9, "source": "fallback"}
     pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -247,10 +249,10 @@ def main():
     # ping-pong (1..L-1, L-2..2, ...) so motion stays continuous for any step count
     host = torch.empty((L, S, 3, H, W), dtype=torch.float32, pin_memory=True)
     hnp = host.numpy()
+    shard = weak_shard(S, rank, world)  # streams rank*S .. rank*S+S-1, seed 1000 + global id
     for s in range(S):
-        g = rank * S + s
         hnp[:, s] = cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, L, a.objects, a.object_size, a.velocity,
-                                                          a.velocity, a.noise, 1000 + g))
+                                                          a.velocity, a.noise, shard.seed(s)))
     dev = host.to(f"cuda:{local}")
     torch.cuda.synchronize()
     order = list(range(1, L)) + list(range(L - 2, 1, -1))
@@ -265,11 +267,7 @@ def main():
             torch.distributed.barrier()
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{local}")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        return float(t.item())
+        return _max_over_ranks(x, device=f"cuda:{local}")
 
     exts = [torch.cuda.ExternalStream(c.stream, device=torch.device("cuda", local)) for c in ctxs]
     ext = exts[0]
