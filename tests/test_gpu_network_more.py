@@ -1,0 +1,160 @@
+"""GPU parity, network level, beyond the basic seg-net runs: detection
+policies, feed-forward mode, joins, worst-case propagation, acceptance
+criteria C1/C2/C8 (acceptance.cpp:85-123, 402-435), clone, pinned seg7 dims.
+Every comparison is against the unmodified reference build on identical inputs.
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+from paper_1808_05488_b200 import cbi
+from tests import oracle
+from tests.oracle import p
+from tests.test_oracle import conv_spec, random_net
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-4
+
+
+def run_pair(spec, taus, frames, policies=None, mode=cbi.DetectMode.ClosedLoop, worst=False):
+    net = cbi.convert_to_cb(spec, taus, policies, mode)
+    ref = oracle.RefNet(spec, taus, policies, mode)
+    cfg = cbi.StatsConfig(record_worst_case=worst, record_maps=True)
+    for t, f in enumerate(frames):
+        fs = cbi.FrameStats()
+        got = net.forward_frame(f, cfg, fs)
+        want = ref.forward(f, record_worst_case=worst)
+        assert oracle.max_rel_err(got, want) <= TOL, f"frame {t}"
+        for i, row in enumerate(fs.layers):
+            st = ref.stats(i)
+            if i == 0:
+                assert np.array_equal(row.map, st["map"]), f"frame {t}: layer-1 map"
+            assert row.changed_px == st["changed_px"], (t, row.layer)
+            assert row.eff_ops == st["eff_ops"], (t, row.layer)
+            if worst and st["propagated_px"] >= 0:
+                assert row.propagated_px == st["propagated_px"], (t, row.layer)
+                assert np.array_equal(row.worst_case_map, st["worst_case_map"]), (t, row.layer)
+                # C8: the detected set is a subset of the worst-case propagation
+                assert not np.any(row.map.astype(bool) & ~row.worst_case_map.astype(bool))
+    return net, ref
+
+
+def frames_for(h, w, n=5, seed=3, c=3, noise=0.0):
+    return cbi.gen_synthetic(cbi.SyntheticConfig(h, w, c, n, 3, 10, 3, 3, noise, seed))
+
+
+def test_policies_propagate_and_reuse(gpu):
+    spec = cbi.make_seg_spec(2, 72, 96)
+    pol = [cbi.DetectionPolicy.Detect, cbi.DetectionPolicy.Propagate, cbi.DetectionPolicy.Detect,
+           cbi.DetectionPolicy.Reuse1x1, cbi.DetectionPolicy.Reuse1x1]
+    run_pair(spec, [0.05] * 5, frames_for(72, 96), pol)
+
+
+def test_feedforward_mode(gpu):
+    spec = cbi.make_seg_spec(4, 64, 80)
+    run_pair(spec, [0.03] * 5, frames_for(64, 80, noise=0.01), mode=cbi.DetectMode.FeedForward)
+
+
+def test_worst_case_stats_and_superset(gpu):
+    spec = cbi.make_seg_spec(5, 64, 80)
+    run_pair(spec, [0.02, 0.05, 0.05, 0.01, 0.01], frames_for(64, 80, noise=0.004), worst=True)
+
+
+@pytest.mark.parametrize("join", [cbi.LayerKind.Add, cbi.LayerKind.Concat])
+def test_joins_match_reference(gpu, join):
+    """test_network.cpp:321-358: re-convergent diamond with Add / Concat."""
+    rng = np.random.default_rng(50 + int(join))
+    stem = conv_spec(rng, 2, cout=6, k=3, stride=1, pad=1)
+    spec = cbi.NetworkSpec(2, 12, 12, [cbi.LayerDesc(cbi.LayerKind.Conv, "stem", [], stem, True)])
+    for nm, cout in (("left", 4), ("right", 4 if join == cbi.LayerKind.Add else 5)):
+        spec.layers.append(cbi.LayerDesc(cbi.LayerKind.Conv, nm, ["stem"],
+                                         conv_spec(rng, 6, cout=cout, k=3, stride=1, pad=1)))
+    spec.layers.append(cbi.LayerDesc(join, "join", ["left", "right"]))
+    spec.layers.append(cbi.LayerDesc(cbi.LayerKind.Conv, "head", [],
+                                     conv_spec(rng, 4 if join == cbi.LayerKind.Add else 9, k=3, stride=1, pad=1)))
+    frames = [rng.uniform(0, 1, (2, 12, 12)).astype(np.float32) for _ in range(5)]
+    frames[3] = frames[2].copy()
+    frames[3][0, 6, 6] += 1.0
+    net, _ = run_pair(spec, [0.0] * 4, frames)
+    # dense equivalence at tau = 0 (test_network.cpp:330-331)
+    ref = oracle.RefNet(spec, [0.0] * 4)
+    assert oracle.max_rel_err(net.output(), ref.dense_forward(frames[-1])) <= TOL
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_c1_zero_threshold_random_networks(gpu, seed):
+    """acceptance C1: tau = 0 => CB output == dense output (random conv/pool chains)."""
+    rng = np.random.default_rng(101 + seed)
+    c, h, w = int(rng.integers(1, 4)), int(rng.integers(12, 33)), int(rng.integers(12, 33))
+    spec = random_net(rng, c, h, w, int(rng.integers(2, 6)))
+    nconv = sum(1 for d in spec.layers if d.kind == cbi.LayerKind.Conv)
+    net = cbi.convert_to_cb(spec, [0.0] * nconv)
+    ref = oracle.RefNet(spec, [0.0] * nconv)
+    x = rng.uniform(0, 1, (c, h, w)).astype(np.float32)
+    for t in range(6):
+        got = net.forward_frame(x)
+        assert oracle.max_rel_err(got, ref.dense_forward(x)) <= TOL
+        x = x.copy()
+        k = int(rng.integers(0, h * w // 8 + 1))
+        x[:, rng.integers(0, h, k), rng.integers(0, w, k)] = rng.uniform(0, 1, (c, k)).astype(np.float32)
+
+
+def test_c2_closed_loop_consistency(gpu):
+    """acceptance C2: every Detect conv's retained output == conv(its input state)."""
+    rng = np.random.default_rng(102)
+    spec = random_net(rng, 2, 24, 28, 4)
+    nconv = sum(1 for d in spec.layers if d.kind == cbi.LayerKind.Conv)
+    net = cbi.convert_to_cb(spec, [float(t) for t in rng.uniform(0.005, 0.08, nconv)])
+    convs = [d.conv for d in spec.layers if d.kind == cbi.LayerKind.Conv]
+    x = rng.uniform(0, 1, (2, 24, 28)).astype(np.float32)
+    for t in range(6):
+        net.forward_frame(x)
+        ci = 0
+        for i, n in enumerate(net.nodes()):
+            if n.kind != cbi.LayerKind.Conv:
+                continue
+            st = net.node_state(i)
+            want = np.zeros(n.out_shape, np.float32)
+            keep = []
+            cs = convs[ci]._c(keep)
+            oracle.ref().ref_conv2d_dense(p(st), *st.shape, C.byref(cs), p(want))
+            if n.fuse_relu:
+                want = np.maximum(want, 0)
+            assert oracle.max_rel_err(net.node_output(i), want) <= TOL, (t, n.name)
+            ci += 1
+        x = (x + rng.uniform(-0.05, 0.05, x.shape) * (rng.random(x.shape) < 0.2)).astype(np.float32)
+
+
+def test_clone_is_an_independent_stream(gpu):
+    spec = cbi.make_small_spec(6, 2, 32, 32)
+    frames = frames_for(32, 32, n=6, c=2, noise=0.01)
+    a = cbi.convert_to_cb(spec, [0.02] * 3)
+    for f in frames[:3]:
+        a.forward_frame(f)
+    b = a.clone()
+    for f in frames[3:]:
+        assert np.array_equal(a.forward_frame(f), b.forward_frame(f))
+    b.forward_frame(frames[0])  # advancing the clone leaves the original untouched
+    ya = a.output().copy()
+    a.forward_frame(frames[-1])
+    assert np.array_equal(a.output(), ya)
+
+
+def test_pinned_seg7_full_resolution_against_reference(gpu):
+    """make_seg7_spec at its pinned 776x1040 dims (crop + ceil-mode pooling):
+    bootstrap + one sparse frame, layer-1 change set bit-exact."""
+    spec = cbi.make_seg7_spec(1)
+    frames = cbi.gen_synthetic(cbi.SyntheticConfig(776, 1040, 3, 2, 2, 24, 4, 4, 0.0, 7))
+    net = cbi.convert_to_cb(spec, [0.05] * 5)
+    ref = oracle.RefNet(spec, [0.05] * 5)
+    for t in range(2):
+        got = net.forward_frame(frames[t])
+        want = ref.forward(frames[t])
+        assert got.shape == (8, 136, 218)
+        assert oracle.max_rel_err(got, want) <= TOL
+        gm, gi = net.node_changes(0)
+        assert np.array_equal(gm, ref.stats(0)["map"])
+        for i in range(len(net.nodes())):
+            assert len(net.node_changes(i)[1]) == ref.stats(i)["changed_px"]
