@@ -164,6 +164,34 @@ CBG_DEV void umma_tf32_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, ui
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// One K=32 block of the 3xTF32 product (K-major SW128 operands): 4 k-steps of
+// 8 tf32 (32 B) x 3 products, 12 tcgen05.mma under a single elect.sync.
+// Descriptor start addresses advance by 2 (16-B units) per k-step.
+CBG_DEV void umma_tf32x3_kblock(uint32_t d_tmem, uint64_t a_hi, uint64_t a_lo, uint64_t b_hi, uint64_t b_lo,
+                                uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b64 ah, al, bh, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "mov.b64 ah, %1;\n\tmov.b64 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, 1;\n\t"
+      "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, 1;\n\t"
+      "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, 1;\n\t"
+      "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, 1;\n\t}" ::"r"(d_tmem),
+      "l"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
 CBG_DEV void umma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

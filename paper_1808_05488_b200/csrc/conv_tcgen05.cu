@@ -227,30 +227,35 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         mbar_wait(&raw[stage], phase);
         if (ctid == 0) TRACE(1, g);
         uint8_t* sA = smem + stage * C::kStageBytes;
+        // all of this thread's loads first, then split + stores (the asm
+        // memory clobbers keep program order, so interleaving would serialize)
+        float x[kConvChunks][4];
+        uint32_t offs[kConvChunks];
 #pragma unroll
         for (int i = 0; i < kConvChunks; ++i) {
           const int r = i * (kConv / 8) + (ctid >> 3);
-          const uint32_t off = r * 128 + ((q ^ (r & 7)) << 4);
-          const uint32_t dh = smem_u32(sA + off), dl = smem_u32(sA + kABytes + off);
-          float x[4];
+          offs[i] = smem_u32(sA) + r * 128 + ((q ^ (r & 7)) << 4);
           asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
-                       : "r"(dh)
+                       : "=f"(x[i][0]), "=f"(x[i][1]), "=f"(x[i][2]), "=f"(x[i][3])
+                       : "r"(offs[i])
                        : "memory");
+        }
+#pragma unroll
+        for (int i = 0; i < kConvChunks; ++i) {
           // hi = x truncated to tf32 (exactly representable), lo = x - hi
           // (exact in fp32); the tensor core reads lo to tf32 precision, so
           // hi + lo carries ~21 significant bits of x.
           uint32_t h[4], l[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            h[j] = __float_as_uint(x[j]) & 0xFFFFE000u;
-            l[j] = __float_as_uint(x[j] - __uint_as_float(h[j]));
+            h[j] = __float_as_uint(x[i][j]) & 0xFFFFE000u;
+            l[j] = __float_as_uint(x[i][j] - __uint_as_float(h[j]));
           }
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dh), "r"(h[0]), "r"(h[1]), "r"(h[2]),
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(offs[i]), "r"(h[0]), "r"(h[1]), "r"(h[2]),
                        "r"(h[3])
                        : "memory");
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(dl), "r"(l[0]), "r"(l[1]), "r"(l[2]),
-                       "r"(l[3])
+          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(offs[i] + kABytes), "r"(l[0]), "r"(l[1]),
+                       "r"(l[2]), "r"(l[3])
                        : "memory");
         }
         fence_proxy_async_smem();
@@ -284,13 +289,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         const uint64_t a_lo = a_hi + (kABytes >> 4);
         const uint64_t b_hi = a_hi + ((2 * kABytes) >> 4);
         const uint64_t b_lo = b_hi + (C::kBBytes >> 4);
-#pragma unroll
-        for (int k = 0; k < kBK / 8; ++k) {
-          const uint64_t ko = (k * 32) >> 4;  // 8 tf32 = 32 B along K inside the swizzle row
-          umma_tf32_elect(d, a_lo + ko, b_hi + ko, idesc, (kb | k) != 0);
-          umma_tf32_elect(d, a_hi + ko, b_lo + ko, idesc, 1);
-          umma_tf32_elect(d, a_hi + ko, b_hi + ko, idesc, 1);
-        }
+        umma_tf32x3_kblock(d, a_hi, a_lo, b_hi, b_lo, idesc, kb != 0);
         umma_commit_elect(&empty[stage]);  // smem slot free once these MMAs retire
         TRACE(3, gm);
         ++gm;
