@@ -64,8 +64,14 @@ constexpr int kConv = kConvWarps * 32;
 constexpr int kFirstConvWarp = 4 + kFetchWarps;
 constexpr int kMmaWarp = kFirstConvWarp + kConvWarps;
 constexpr int kThreads = (kMmaWarp + 1) * 32;
-constexpr int kFetchChunks = 128 * 8 / kFetch;  // 16-B A chunks per fetch thread per K-block
-constexpr int kConvChunks = 128 * 8 / kConv;    // per convert thread
+// Fetch and convert warps each form 2 groups that take alternating K-blocks,
+// so two K-blocks are in flight per role (a single group serialized on the
+// per-K-block latency of its waits, loads and proxy fence).
+constexpr int kGroups = 2;
+constexpr int kFetchG = kFetch / kGroups;        // fetch threads per group
+constexpr int kConvG = kConv / kGroups;          // convert threads per group
+constexpr int kFetchChunks = 128 * 8 / kFetchG;  // 16-B A chunks per fetch thread per K-block
+constexpr int kConvChunks = 128 * 8 / kConvG;    // per convert thread
 constexpr int kBM = 128;                 // UMMA M
 constexpr int kBK = 32;                  // fp32 elements per K-block (= one 128-B swizzle row)
 constexpr int kABytes = kBM * kBK * 4;   // one of A_hi / A_lo: 16 KB
@@ -110,9 +116,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   // ---- setup -----------------------------------------------------------------
   if (tid == 0) {
     for (int i = 0; i < C::kStages; ++i) {
-      mbar_init(&full[i], kConvWarps + 1);  // convert warps + 1 expect_tx arrive (B bulk copy)
+      mbar_init(&full[i], kConvWarps / kGroups + 1);  // one convert group + 1 expect_tx arrive
       mbar_init(&empty[i], 1);              // tcgen05.commit
-      mbar_init(&raw[i], kFetch);           // one cp.async.mbarrier.arrive per fetch thread
+      mbar_init(&raw[i], kFetchG);          // one cp.async.mbarrier.arrive per fetch thread of a group
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -165,7 +171,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
 
   if (warp >= 4 && warp < kFirstConvWarp) {
     // ========================= fetch =========================
-    const int ftid = tid - 128;
+    const int fgrp = (tid - 128) / kFetchG;  // K-blocks g with g % kGroups == fgrp
+    const int ftid = (tid - 128) % kFetchG;
     const int q = ftid & 7;
     const uint32_t ktab_s = smem_u32(ktab), koff_s = smem_u32(koff);
     uint32_t g = 0;  // global K-block counter (stage = g % kStages)
@@ -177,7 +184,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       int jb[kFetchChunks], ib[kFetchChunks], roff[kFetchChunks];
 #pragma unroll
       for (int i = 0; i < kFetchChunks; ++i) {
-        const int k = mt * kBM + i * (kFetch / 8) + (ftid >> 3);
+        const int k = mt * kBM + i * (kFetchG / 8) + (ftid >> 3);
         const int p = k < cnt ? __ldg(a.idx + s * HWout + k) : -1;
         const int jo = p / a.Wout, io = p - jo * a.Wout;
         jb[i] = p >= 0 ? jo * a.stride - a.pad : INT_MIN / 2;
@@ -188,6 +195,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       const uint8_t* bimg = a.wimg + static_cast<long long>(nt) * a.KB * 2 * C::kBBytes;
 #pragma unroll 1
       for (int kb = 0; kb < a.KB; ++kb, ++g) {
+        if (static_cast<int>(g % kGroups) != fgrp) continue;
         const int stage = g % C::kStages;
         const uint32_t phase = (g / C::kStages) & 1;
         const uint32_t tab = lds_u32(ktab_s + (kb * 8 + q) * 4);
@@ -205,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         const uint32_t base = smem_u32(sA);
 #pragma unroll
         for (int i = 0; i < kFetchChunks; ++i) {
-          const int r = i * (kFetch / 8) + (ftid >> 3);
+          const int r = i * (kFetchG / 8) + (ftid >> 3);
           const bool ok = tap_ok && static_cast<unsigned>(jb[i] + dj) < static_cast<unsigned>(a.Hin) &&
                           static_cast<unsigned>(ib[i] + di) < static_cast<unsigned>(a.Win);
           cp_async16(base + r * 128 + ((q ^ (r & 7)) << 4), ok ? src + (roff[i] + toff) : src, ok ? 16u : 0u);
@@ -216,12 +224,14 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     }
   } else if (warp >= kFirstConvWarp && warp < kMmaWarp) {
     // ========================= convert =========================
-    const int ctid = tid - kFirstConvWarp * 32;
+    const int cgrp = (tid - kFirstConvWarp * 32) / kConvG;
+    const int ctid = (tid - kFirstConvWarp * 32) % kConvG;
     const int q = ctid & 7;
     uint32_t g = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
 #pragma unroll 1
       for (int kb = 0; kb < a.KB; ++kb, ++g) {
+        if (static_cast<int>(g % kGroups) != cgrp) continue;
         const int stage = g % C::kStages;
         const uint32_t phase = (g / C::kStages) & 1;
         mbar_wait(&raw[stage], phase);
@@ -233,7 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         uint32_t offs[kConvChunks];
 #pragma unroll
         for (int i = 0; i < kConvChunks; ++i) {
-          const int r = i * (kConv / 8) + (ctid >> 3);
+          const int r = i * (kConvG / 8) + (ctid >> 3);
           offs[i] = smem_u32(sA) + r * 128 + ((q ^ (r & 7)) << 4);
           asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
                        : "=f"(x[i][0]), "=f"(x[i][1]), "=f"(x[i][2]), "=f"(x[i][3])
