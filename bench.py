@@ -62,6 +62,8 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU-baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--sweep-steps", type=int, default=6,
+                    help="timed steps per point of the change-rate sweep (0 disables the sweep)")
     return ap.parse_args()
 
 
@@ -181,6 +183,13 @@ class ClockSampler:
         reasons = sorted({name for _, r in self.rows for bit, name in self.REASONS.items() if r & bit})
         return {"sm_mhz": statistics.median(c for c, _ in self.rows), "sm_max_mhz": self.max_mhz,
                 "reasons": reasons, "samples": len(self.rows), "source": "nvml, ~1 ms polling in the timed region"}
+
+
+# change-rate sweep points (objects, object size) -> L1-output change of
+# ~0.1 / 0.4 / 1.2 / 3 / 6 / 15 / 28 % at 640x480 (gen_synthetic, v=4), plus
+# "random": every frame i.i.d. uniform noise, so ~100% of pixels change on
+# every layer (the change-based path's worst case, compared with the dense path)
+SWEEP = [(1, 8), (2, 16), (3, 32), (6, 40), (10, 48), (24, 64), (60, 96), "random"]
 
 
 # ---------------------------------------------------------------------------
@@ -421,6 +430,69 @@ def main():
         dense_fps = S * world * a.dense_steps / (dms / 1000.0)
         del dnets
 
+    # ---- change-rate sweep: frames/s vs changed-pixel % (the metric's x-axis) ---
+    sweep = []
+    if a.sweep_steps > 0:
+        from concurrent.futures import ThreadPoolExecutor
+        R = 6
+        sorder = list(range(1, R)) + list(range(R - 2, 1, -1))
+        sw_counts = torch.empty((G, n_slots, Sg), dtype=torch.int32, pin_memory=True)
+        for pt in SWEEP:
+            if pt == "random":
+                gen = torch.Generator(device=f"cuda:{local}").manual_seed(4242 + rank)
+                sdev = torch.rand((R, S, 3, H, W), generator=gen, device=f"cuda:{local}")
+            else:
+                ob, sz = pt
+                sh = torch.empty((R, S, 3, H, W), dtype=torch.float32, pin_memory=True)
+                shn = sh.numpy()
+
+                def _gen(s_, ob=ob, sz=sz, shn=shn):
+                    shn[:, s_] = cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, R, ob, sz, a.velocity, a.velocity,
+                                                                       a.noise, shard.seed(s_)))
+                with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as pool:
+                    list(pool.map(_gen, range(S)))
+                sdev = sh.to(f"cuda:{local}")
+            snets = [cbi.convert_to_cb(spec, taus, n_streams=Sg, ctx=ctxs[g]) for g in range(G)]
+            for g in range(G):
+                snets[g].enqueue_device(sdev[0, g * Sg].data_ptr())
+            for k in range(3):
+                for g in range(G):
+                    snets[g].enqueue_device(sdev[sorder[k % len(sorder)], g * Sg].data_ptr())
+            for c in ctxs:
+                c.synchronize()
+            barrier()
+
+            def sweep_step(k, snets=snets, sdev=sdev):
+                for g in range(G):
+                    snets[g].enqueue_device(sdev[sorder[(3 + k) % len(sorder)], g * Sg].data_ptr())
+
+            sms = max_over_ranks(timed_region(sweep_step, a.sweep_steps))
+            for g in range(G):
+                snets[g].copy_counts_async(sw_counts[g].data_ptr())
+            for c in ctxs:
+                c.synchronize()
+            sc = np.concatenate([sw_counts[g].numpy() for g in range(G)], axis=1)
+            fps = S * world * a.sweep_steps / (sms / 1000.0)
+            sweep.append({"synthetic": ("uniform noise every frame" if pt == "random"
+                                        else f"{pt[0]} objects x {pt[1]} px"),
+                          "l1_changed_pct": 100.0 * float(sc[node_slot[0]].mean()) / l1_px,
+                          "per_layer_changed_pct": {n.name: round(100.0 * float(sc[node_slot[i]].mean())
+                                                                  / (n.out_shape[1] * n.out_shape[2]), 3)
+                                                    for i, n in enumerate(nodes)},
+                          "frames_per_s": fps,
+                          "speedup_vs_dense": (fps / dense_fps) if dense_fps else None})
+            del snets, sdev
+        torch.cuda.empty_cache()
+    crossover = None
+    if dense_fps and sweep:
+        pts = sorted((p["l1_changed_pct"], p["frames_per_s"] / dense_fps) for p in sweep)
+        for (x0, r0), (x1, r1) in zip(pts, pts[1:]):
+            if r0 >= 1.0 > r1:  # linear in log(change) between the bracketing points
+                import math
+                f = (r0 - 1.0) / (r0 - r1)
+                crossover = math.exp(math.log(max(x0, 1e-6)) + f * (math.log(x1) - math.log(max(x0, 1e-6))))
+                break
+
     # ---- e2e: host frames through the C ABI, H2D + D2H in the timed region -------
     e2e = None
     if not a.no_e2e:
@@ -466,6 +538,7 @@ def main():
                "config": config_dict(a, world),
                "change": {"l1_changed_frac": l1_frac, "per_layer_changed_frac": per_layer},
                "dense_path_fps": dense_fps, "speedup_vs_dense": (value / dense_fps) if dense_fps else None,
+               "sweep": sweep, "crossover_l1_changed_pct": crossover,
                "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * a.steps,
                "clocks": clocks.summary()}
         print(json.dumps(out))

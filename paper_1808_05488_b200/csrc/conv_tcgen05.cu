@@ -81,7 +81,12 @@ template <int NPAD>
 struct Cfg {
   static constexpr int kBBytes = NPAD * kBK * 4;
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
-  static constexpr int kStages = NPAD >= 256 ? 2 : NPAD >= 128 ? 3 : NPAD >= 64 ? 4 : 5;
+  // A multiple of kGroups, so a stage is always filled and converted by the same
+  // group: with an odd count, a convert group could reach a stage one lap ahead
+  // of the other group's fetch and take that stage's previous `raw` phase
+  // (mbarrier parity aliases modulo 2) as complete.
+  static constexpr int kStages = NPAD >= 128 ? 2 : 4;
+  static_assert(kStages % kGroups == 0, "stages must be a multiple of the producer groups");
   static constexpr uint32_t kTmemCols = (2 * NPAD <= 32) ? 32 : (2 * NPAD <= 64) ? 64 : (2 * NPAD <= 128) ? 128
                                         : (2 * NPAD <= 256) ? 256 : 512;
 };
