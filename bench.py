@@ -409,7 +409,8 @@ def main():
                  "launch_streams": S, "peak_source": peaks["source"],
                  "step_roofline_frac": (sum(max(k["bytes_per_launch"] / hbm, k["flops_per_launch"] / tf32)
                                             for k in kernels) / (tot / 1000.0)),
-                 "top_kernels": kernels[:6]})
+                 "top_kernels": kernels[:6],
+                 "all_kernels_us": {k["kernel"]: round(1000 * k["ms_per_launch"], 1) for k in kernels}})
 
     # ---- dense path (same kernels, every frame a full update) -------------------
     dense_fps = None

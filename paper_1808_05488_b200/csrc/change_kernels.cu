@@ -124,6 +124,93 @@ __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs 
 }
 
 // ---------------------------------------------------------------------------
+// detect on the network-input frame against a CHW (planar, unpadded) state:
+// the layout of the first layer's state when that layer runs the CUDA-core
+// path (conv_exact.cu reads its taps from the planes). Every byte moved is
+// algorithmic: 4*C B of frame + 4*C B of state per pixel, state written only
+// where a pixel of the 4-pixel group changed. One thread = 4 consecutive
+// pixels (HW % 4 == 0), C <= 4 kept in registers.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) detect_frame_chw_kernel(DetectFrameArgs a) {
+  const int s = blockIdx.y;
+  const uint8_t e = epoch8(*a.frame);
+  const bool boot = a.boot[s] != 0;
+  const long long HW = static_cast<long long>(a.H) * a.W;
+  const float* x = *a.x_slot + static_cast<long long>(s) * a.C * HW;
+  float* st = a.state + static_cast<long long>(s) * a.C * HW;
+  uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  const bool write_all = boot || !a.closed_loop;
+  const float tau = *a.tau;
+  const long long n4 = HW >> 2;
+  for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long p0 = q << 2;
+    float4 xv[4], sv[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (c < a.C) {
+        xv[c] = ldg_nc_f4(x + c * HW + p0);
+        if (!boot) sv[c] = *reinterpret_cast<const float4*>(st + c * HW + p0);
+      }
+    }
+    uint32_t ch = 0;  // bit j: pixel p0+j changed
+    if (!boot) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < a.C) {
+          ch |= static_cast<uint32_t>(fabsf(xv[c].x - sv[c].x) > tau) << 0;
+          ch |= static_cast<uint32_t>(fabsf(xv[c].y - sv[c].y) > tau) << 1;
+          ch |= static_cast<uint32_t>(fabsf(xv[c].z - sv[c].z) > tau) << 2;
+          ch |= static_cast<uint32_t>(fabsf(xv[c].w - sv[c].w) > tau) << 3;
+        }
+      }
+    }
+    if (write_all || ch) {
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < a.C) {
+          float4 v = xv[c];
+          if (!write_all) {  // keep unchanged pixels' state (same bits written back)
+            if (!(ch & 1u)) v.x = sv[c].x;
+            if (!(ch & 2u)) v.y = sv[c].y;
+            if (!(ch & 4u)) v.z = sv[c].z;
+            if (!(ch & 8u)) v.w = sv[c].w;
+          }
+          *reinterpret_cast<float4*>(st + c * HW + p0) = v;
+        }
+      }
+    }
+    if (ch) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if ((ch >> j) & 1u) m[p0 + j] = e;
+    }
+  }
+}
+
+// scalar fallback (any C, any HW): CHW state, one thread per pixel
+__global__ void __launch_bounds__(kThreads) detect_frame_chw_scalar_kernel(DetectFrameArgs a) {
+  const int s = blockIdx.y;
+  const uint8_t e = epoch8(*a.frame);
+  const bool boot = a.boot[s] != 0;
+  const long long HW = static_cast<long long>(a.H) * a.W;
+  const float* x = *a.x_slot + static_cast<long long>(s) * a.C * HW;
+  float* st = a.state + static_cast<long long>(s) * a.C * HW;
+  uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  const bool write_all = boot || !a.closed_loop;
+  const float tau = *a.tau;
+  for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < HW;
+       p += static_cast<long long>(gridDim.x) * blockDim.x) {
+    bool changed = false;
+    if (!boot)
+      for (int c = 0; c < a.C; ++c) changed |= fabsf(__ldg(x + c * HW + p) - st[c * HW + p]) > tau;
+    if (changed || write_all)
+      for (int c = 0; c < a.C; ++c) st[c * HW + p] = __ldg(x + c * HW + p);
+    if (changed) m[p] = e;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // detect on NHWC inputs. A group of g lanes handles one pixel (g float4 per
 // step); the group's verdict is reduced with a warp ballot.
 // ---------------------------------------------------------------------------
@@ -503,7 +590,15 @@ int group_log2(int Cs) {
 
 void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
   const long long HW = static_cast<long long>(a.H) * a.W;
-  if (a.Cs == 4 && HW % 4 == 0) {
+  if (a.state_chw) {
+    if (a.C <= 4 && HW % 4 == 0) {
+      dim3 grid(blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
+      detect_frame_chw_kernel<<<grid, kThreads, 0, st>>>(a);
+    } else {
+      dim3 grid(blocks_for(HW, kThreads, a.S, sm_count()), a.S);
+      detect_frame_chw_scalar_kernel<<<grid, kThreads, 0, st>>>(a);
+    }
+  } else if (a.Cs == 4 && HW % 4 == 0) {
     dim3 grid(blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
     detect_frame_kernel<true><<<grid, kThreads, 0, st>>>(a);
   } else {

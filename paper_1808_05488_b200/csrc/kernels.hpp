@@ -28,6 +28,7 @@ struct DetectFrameArgs {
   int C, Cs, H, W, S;
   const float* tau;    // device scalar (set_thresholds needs no re-capture)
   int closed_loop;
+  int state_chw;       // state is [S][C][H][W] (unpadded planes) instead of NHWC
 };
 void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st);
 
@@ -116,6 +117,29 @@ struct ConvGemmArgs {
 void launch_conv_gemm(const ConvGemmArgs& a, cudaStream_t st);
 int conv_gemm_smem_bytes(int npad, int KB, int S);
 int conv_gemm_stages(int npad);
+
+// Bit-exact CUDA-core update for narrow layers (Cout <= 16): the reference's
+// sequential non-FMA fp32 sum in im2col row order (conv_exact.cu).
+struct ConvExactArgs {
+  const float* src;        // column source; element (c, j, i) at c*cstride + (j*Win + i)*pstride
+  long long src_sstride;   // per-stream stride of src (elements)
+  long long cstride;
+  int pstride;
+  float* out;              // [S][Hout][Wout][Co4]
+  const int32_t* idx;      // [S][Hout*Wout]
+  const int32_t* count;    // [S]
+  const float* w;          // [Cout][Cin*kh*kw] (reference weights layout, tensor.hpp:47)
+  const float* bias;       // [Cout]
+  int Cin, Cout, Co4, kh, kw, stride, pad;
+  int Hin, Win, Hout, Wout;
+  int relu;
+  int S;
+  int sm_count;
+};
+void launch_conv_exact(const ConvExactArgs& a, cudaStream_t st);
+int conv_exact_group(int cout);
+bool conv_exact_supported(int kw);
+size_t conv_exact_smem_bytes(int cout, int K);
 
 // Device frame-counter advance + per-stream boot flags for this frame.
 struct BeginFrameArgs {

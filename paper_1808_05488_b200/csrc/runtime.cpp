@@ -4,6 +4,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <numeric>
@@ -359,6 +360,13 @@ void build_weight_image(const NodeRT& n, std::vector<uint8_t>& img, std::vector<
   for (int o = 0; o < c.out_channels; ++o) bias[o] = c.bias[o];
 }
 
+// Layers with at most this many output channels take the bit-exact CUDA-core
+// path (conv_exact.cu); CBG_EXACT_MAX_COUT overrides it (0 = tcgen05 everywhere).
+int exact_max_cout() {
+  const char* e = std::getenv("CBG_EXACT_MAX_COUT");
+  return e ? std::atoi(e) : 16;
+}
+
 void dc_tiling(int Hin, int Win, int Hout, int Wout, int kh, int stride, int S, int* rows, int* tiles,
                int* smem) {
   if (Wout > 65536 || Win > 65536) throw Error(CBG_ERR_UNSUPPORTED, "map width > 65536 not supported");
@@ -438,20 +446,29 @@ void Net::build() {
       r.n_tiles = (Co4 + r.npad - 1) / r.npad;
       const int K = c.kernel_h * c.kernel_w * r.Csi;
       r.KB = (K + 31) / 32;
-      if (r.KB > 512) throw Error(CBG_ERR_UNSUPPORTED, "Cin*kh*kw too large for the GEMM kernel (K > 16384)");
-      if (r.Csi >= 32768) throw Error(CBG_ERR_UNSUPPORTED, "too many input channels");
-      std::vector<uint8_t> img;
-      std::vector<uint32_t> ktab;
+      const int Kref = c.in_channels * c.kernel_h * c.kernel_w;
+      r.exact = c.out_channels <= exact_max_cout() && conv_exact_supported(c.kernel_w) && conv_exact_smem_bytes(c.out_channels, Kref) <= 192 * 1024;
       std::vector<float> bias;
-      build_weight_image(r, img, ktab, bias);
-      r.wimg.alloc(img.size());
-      CK(cudaMemcpy(r.wimg.p, img.data(), img.size(), cudaMemcpyHostToDevice));
-      r.ktab.alloc(ktab.size() * 4);
-      CK(cudaMemcpy(r.ktab.p, ktab.data(), ktab.size() * 4, cudaMemcpyHostToDevice));
+      if (r.exact) {
+        r.wraw.alloc(c.weights.size() * sizeof(float));
+        CK(cudaMemcpy(r.wraw.p, c.weights.data(), c.weights.size() * sizeof(float), cudaMemcpyHostToDevice));
+        bias.assign(c.bias.begin(), c.bias.end());
+      } else {
+        if (r.KB > 512) throw Error(CBG_ERR_UNSUPPORTED, "Cin*kh*kw too large for the GEMM kernel (K > 16384)");
+        if (r.Csi >= 32768) throw Error(CBG_ERR_UNSUPPORTED, "too many input channels");
+        std::vector<uint8_t> img;
+        std::vector<uint32_t> ktab;
+        build_weight_image(r, img, ktab, bias);
+        r.wimg.alloc(img.size());
+        CK(cudaMemcpy(r.wimg.p, img.data(), img.size(), cudaMemcpyHostToDevice));
+        r.ktab.alloc(ktab.size() * 4);
+        CK(cudaMemcpy(r.ktab.p, ktab.data(), ktab.size() * 4, cudaMemcpyHostToDevice));
+      }
       r.bias.alloc(bias.size() * 4);
       CK(cudaMemcpy(r.bias.p, bias.data(), bias.size() * 4, cudaMemcpyHostToDevice));
       if (d.policy == CBG_POLICY_DETECT) {
-        r.state.alloc(static_cast<size_t>(S_) * HWi * r.Csi * sizeof(float));
+        r.state_chw = r.exact && d.inputs[0] < 0;
+        r.state.alloc(static_cast<size_t>(S_) * HWi * (r.state_chw ? d.Ci : r.Csi) * sizeof(float));
         r.inmap.alloc(static_cast<size_t>(S_) * HWi);
       }
       if (!reuse) {
@@ -543,7 +560,7 @@ void Net::enqueue_frame(unsigned flags) {
         if (!prod) {
           DetectFrameArgs a{frame_slot_.as<const float*>(), r.state.as<float>(), r.inmap.as<uint8_t>(), frame, boot,
                             d.Ci, r.Csi, d.Hi, d.Wi, S_, taus_.as<float>() + i,
-                            topo_.mode == CBG_MODE_CLOSEDLOOP};
+                            topo_.mode == CBG_MODE_CLOSEDLOOP, r.state_chw};
           timed(d.name + ".detect", [&] { launch_detect_frame(a, st); });
         } else {
           const bool ext = prod->d.kind == kExternal;  // standalone layer: arbitrary x, dense detect
@@ -597,6 +614,32 @@ void Net::enqueue_frame(unsigned flags) {
         dc.kh = c.kernel_h, dc.kw = c.kernel_w, dc.stride = c.stride, dc.pad = c.padding;
         dc.rows_per_tile = r.dc_wc_rows, dc.n_tiles = r.dc_wc_tiles, dc.S = S_, dc.smem_bytes = r.dc_wc_smem;
         timed(d.name + ".worstcase", [&] { launch_dilate_compact(dc, st); });
+      }
+      if (r.exact) {
+        ConvExactArgs x{};
+        x.src = column_src;
+        if (r.state_chw) {
+          x.src_sstride = static_cast<long long>(d.Hi) * d.Wi * d.Ci;
+          x.cstride = static_cast<long long>(d.Hi) * d.Wi;
+          x.pstride = 1;
+        } else {
+          x.src_sstride = static_cast<long long>(d.Hi) * d.Wi * r.Csi;
+          x.cstride = 1;
+          x.pstride = r.Csi;
+        }
+        x.out = r.out.as<float>();
+        x.idx = r.idx;
+        x.count = counts + r.count_slot * S_;
+        x.w = r.wraw.as<float>();
+        x.bias = r.bias.as<float>();
+        x.Cin = c.in_channels, x.Cout = c.out_channels, x.Co4 = r.Cs;
+        x.kh = c.kernel_h, x.kw = c.kernel_w, x.stride = c.stride, x.pad = c.padding;
+        x.Hin = d.Hi, x.Win = d.Wi, x.Hout = d.H, x.Wout = d.W;
+        x.relu = d.relu;
+        x.S = S_;
+        x.sm_count = ctx_->sm_count;
+        timed(d.name + ".gemm", [&] { launch_conv_exact(x, st); });
+        continue;
       }
       ConvGemmArgs g{};
       g.src = column_src;
@@ -881,6 +924,12 @@ void Net::read_state(int node, int stream, float* out_chw) {
   const NodeRT& r = nodes_[node];
   if (!r.state.bytes) throw_invalid("read_state: node has no input state (not a detect-policy conv)");
   const size_t HW = static_cast<size_t>(r.d.Hi) * r.d.Wi;
+  if (r.state_chw) {
+    CK(cudaMemcpyAsync(out_chw, r.state.as<float>() + static_cast<size_t>(stream) * HW * r.d.Ci,
+                       static_cast<size_t>(r.d.Ci) * HW * sizeof(float), cudaMemcpyDeviceToHost, ctx_->stream));
+    CK(cudaStreamSynchronize(ctx_->stream));
+    return;
+  }
   DevBuf tmp;
   tmp.alloc(static_cast<size_t>(r.d.Ci) * HW * sizeof(float));
   launch_nhwc_to_chw(r.state.as<float>() + static_cast<size_t>(stream) * HW * r.Csi, tmp.as<float>(), r.d.Ci, r.Csi,

@@ -92,7 +92,9 @@ struct NodeRT {
   int Cs = 0, Csi = 0;           // padded channel strides (out / in)
   // conv
   int npad = 0, n_tiles = 0, KB = 0;
-  DevBuf wimg, ktab, bias;
+  bool exact = false;            // CUDA-core bit-exact path (conv_exact.cu) instead of tcgen05
+  bool state_chw = false;        // first-layer exact conv: input state as CHW planes (= the frame layout)
+  DevBuf wimg, ktab, bias, wraw; // wraw: [Cout][Cin*kh*kw] fp32 for the exact path
   DevBuf state, inmap;           // Detect policy
   // every node
   DevBuf out;                    // [S][H][W][Cs]

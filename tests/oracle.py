@@ -176,8 +176,8 @@ class RefNet(_NetBase):
         self.lib.ref_net_read_output(self.h, node, p(y))
         return y
 
-    def state(self, node):
-        y = np.empty(self.in_shape(node), np.float32)
+    def state(self, node, shape=None):
+        y = np.empty(shape if shape is not None else self.in_shape(node), np.float32)
         self.lib.ref_net_read_state(self.h, node, p(y))
         return y
 

@@ -134,3 +134,23 @@ def test_identical_second_frame_changes_nothing(gpu):
     assert out.shape == (8, 136, 218) and np.all(np.isfinite(out))
     net.forward_frame(frame)
     assert np.all(net.counts() == 0)
+
+
+def test_narrow_layers_bit_exact(gpu):
+    """Layers with Cout <= 16 run the CUDA-core path (conv_exact.cu) in the
+    reference's own summation order: the first layer's retained output, the
+    pool after it and the next layer's change maps are bit-identical to the
+    reference, frame by frame (SURVEY.md §8c asks for <= 1e-5 there)."""
+    H, W = 96, 128
+    spec = cbi.make_seg_spec(2, H, W)
+    taus = [0.05] * 5
+    net = cbi.convert_to_cb(spec, taus)
+    ref = oracle.RefNet(spec, taus)
+    for t, f in enumerate(seq(H, W, n=6, seed=21, noise=0.002)):
+        net.forward_frame(f)
+        ref.forward(f)
+        assert np.array_equal(net.node_output(0), ref.output(0)), f"frame {t}: L1 output not bit-exact"
+        assert np.array_equal(net.node_output(1), ref.output(1)), f"frame {t}: L2b output not bit-exact"
+        gm, _ = net.node_changes(2)
+        assert np.array_equal(gm, ref.stats(2)["map"]), f"frame {t}: L3 map differs"
+        assert np.array_equal(net.node_state(2), ref.state(2, net.nodes()[2].in_shape)), f"frame {t}: L3 state differs"
