@@ -192,6 +192,57 @@ CBG_DEV void umma_tf32x3_kblock(uint32_t d_tmem, uint64_t a_hi, uint64_t a_lo, u
       "l"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// Same K=32 block with A (hi and lo) in tensor memory ("ts" form): A_hi at
+// TMEM columns [a_hi, a_hi+32), A_lo at [a_lo, a_lo+32), lane = row; each
+// k-step of 8 tf32 advances A by 8 columns and B by 32 B (2 in 16-B units).
+// The tensor core then reads only B from shared memory.
+CBG_DEV void umma_tf32x3_kblock_ts(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo, uint64_t b_hi, uint64_t b_lo,
+                                   uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], bh, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bl, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bh, %5, 1;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], bh, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bl, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bh, %5, 1;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], bh, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bl, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bh, %5, 1;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [al], bh, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bl, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [ah], bh, %5, 1;\n\t}" ::"r"(d_tmem),
+      "r"(a_hi), "r"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 32 bit, 32 consecutive columns per thread (this warp's lane quarter).
+CBG_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
+      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
+      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
+      : "memory");
+}
+// 32 lanes x 32 bit, 16 consecutive columns per thread.
+CBG_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(
+          taddr),
+      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
+      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
+      : "memory");
+}
+CBG_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
 CBG_DEV void umma_commit_elect(uint64_t* bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\t"

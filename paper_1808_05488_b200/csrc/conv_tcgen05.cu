@@ -15,23 +15,28 @@
 // tcgen05.mma kind::tf32 with fp32 accumulation in TMEM — near-fp32 accuracy,
 // the same precision on the sparse and the dense (full-update) path.
 //
-// Warp roles (416 threads, 1 CTA/SM, persistent over (stream, m-tile, n-tile)):
+// Warp roles (672 threads, 1 CTA/SM, persistent over (stream, m-tile, n-tile)):
 //   warps 0-3   epilogue: tcgen05.ld TMEM -> +bias -> ReLU -> scatter (lane = row)
-//   warps 4-7   fetch: gather the A tile (changed pixels' receptive fields) with
+//   warps 4-11  fetch: gather the A tile (changed pixels' receptive fields) with
 //               16-B cp.async copies (zero-fill for padding taps) straight into
-//               the UMMA SW128 K-major stage, completion signalled with
+//               the stage (rows of 128 B, 16-B chunks XOR-swizzled by row so the
+//               convert warps' row reads are conflict-free), completion signalled with
 //               cp.async.mbarrier.arrive.noinc so they never wait on data;
 //               fetch thread 0 also streams the pre-swizzled B (weight) image of
 //               the K-block with a bulk copy on the TMA engine
-//   warps 8-15  convert: split the landed fp32 chunks in place into tf32 hi / lo,
-//               fence.proxy.async, arrive for the MMA. Fetch and convert are
-//               separate warps because fence.proxy.async lowers to
-//               MEMBAR.ALL.CTA, which also waits for the thread's own in-flight
-//               global loads / cp.async (measured: long-scoreboard stalls at
-//               FENCE.VIEW.ASYNC.S when one warp did both).
-//   warp 16     TMEM allocator + single-thread tcgen05.mma issuer
-// Pipelines: smem stages full/empty (producers <-> MMA), two TMEM accumulators
-// full/empty (MMA <-> epilogue) so tile t's epilogue overlaps tile t+1's MMAs.
+//   warps 12-19 convert: thread = row of the tile; read the landed fp32 row from
+//               shared memory, split it into tf32 hi / lo and store both into
+//               TENSOR MEMORY (tcgen05.st), arrive for the MMA. The MMAs take
+//               A from TMEM ("ts" form), so per K-block the tensor core reads
+//               only B from shared memory: the stage traffic was 208 KB per
+//               K-block (N=256) / 136 KB (N=64) with A in smem (raw write + read,
+//               hi/lo write, 3 A reads), above the MMA time at 128 B/clk; it is
+//               128 KB / 56 KB now.
+//   warp 20     TMEM allocator + single-thread tcgen05.mma issuer
+// Pipelines: stages full/empty (producers <-> MMA; a stage = raw A rows and the
+// B hi/lo image in smem + A hi/lo columns in TMEM), TMEM accumulators
+// full/empty (MMA <-> epilogue): two for N <= 128 so tile t's epilogue overlaps
+// tile t+1's MMAs, one for N = 256 (TMEM holds 512 columns).
 #include <climits>
 #include <cstdio>
 
@@ -71,24 +76,26 @@ constexpr int kGroups = 2;
 constexpr int kFetchG = kFetch / kGroups;        // fetch threads per group
 constexpr int kConvG = kConv / kGroups;          // convert threads per group
 constexpr int kFetchChunks = 128 * 8 / kFetchG;  // 16-B A chunks per fetch thread per K-block
-constexpr int kConvChunks = 128 * 8 / kConvG;    // per convert thread
 constexpr int kBM = 128;                 // UMMA M
 constexpr int kBK = 32;                  // fp32 elements per K-block (= one 128-B swizzle row)
-constexpr int kABytes = kBM * kBK * 4;   // one of A_hi / A_lo: 16 KB
+constexpr int kABytes = kBM * kBK * 4;   // raw fp32 A rows of one K-block: 16 KB
+constexpr int kACols = 2 * kBK;          // TMEM columns of one stage's A_hi | A_lo
 constexpr int kMaxS = 1024;
 
 template <int NPAD>
 struct Cfg {
   static constexpr int kBBytes = NPAD * kBK * 4;
-  static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
+  static constexpr int kStageBytes = kABytes + 2 * kBBytes;
   // A multiple of kGroups, so a stage is always filled and converted by the same
   // group: with an odd count, a convert group could reach a stage one lap ahead
   // of the other group's fetch and take that stage's previous `raw` phase
   // (mbarrier parity aliases modulo 2) as complete.
-  static constexpr int kStages = NPAD >= 128 ? 2 : 4;
+  static constexpr int kStages = NPAD >= 256 ? 2 : NPAD >= 128 ? 4 : 6;
   static_assert(kStages % kGroups == 0, "stages must be a multiple of the producer groups");
-  static constexpr uint32_t kTmemCols = (2 * NPAD <= 32) ? 32 : (2 * NPAD <= 64) ? 64 : (2 * NPAD <= 128) ? 128
-                                        : (2 * NPAD <= 256) ? 256 : 512;
+  static constexpr int kNAcc = NPAD >= 256 ? 1 : 2;  // TMEM accumulator buffers
+  static constexpr uint32_t kTmemCols = 512;
+  static constexpr uint32_t kAColBase = kNAcc * NPAD;  // first A stage column
+  static_assert(kNAcc * NPAD + kStages * kACols <= 512, "TMEM budget");
 };
 
 __host__ __device__ constexpr int tail_bytes(int stages, int KB, int S) {
@@ -212,7 +219,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         uint8_t* sA = smem + stage * C::kStageBytes;
         if (ftid == 0) {
           mbar_arrive_expect_tx(&full[stage], 2 * C::kBBytes);
-          bulk_g2s(sA + 2 * kABytes, bimg + static_cast<long long>(kb) * 2 * C::kBBytes, 2 * C::kBBytes,
+          bulk_g2s(sA + kABytes, bimg + static_cast<long long>(kb) * 2 * C::kBBytes, 2 * C::kBBytes,
                    &full[stage]);
         }
         const uint32_t base = smem_u32(sA);
@@ -231,7 +238,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     // ========================= convert =========================
     const int cgrp = (tid - kFirstConvWarp * 32) / kConvG;
     const int ctid = (tid - kFirstConvWarp * 32) % kConvG;
-    const int q = ctid & 7;
     uint32_t g = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
 #pragma unroll 1
@@ -242,38 +248,36 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         mbar_wait(&raw[stage], phase);
         if (ctid == 0) TRACE(1, g);
         uint8_t* sA = smem + stage * C::kStageBytes;
-        // all of this thread's loads first, then split + stores (the asm
-        // memory clobbers keep program order, so interleaving would serialize)
-        float x[kConvChunks][4];
-        uint32_t offs[kConvChunks];
+        // thread = row r of the tile (= its TMEM lane: warp % 4 picks the lane
+        // quarter a warp may access); the 8 swizzled 16-B chunks of the row
+        const int r = 32 * (warp & 3) + lane;
+        const uint32_t row = smem_u32(sA) + r * 128;
+        const uint32_t ta = tmem_base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + C::kAColBase +
+                            stage * kACols;
 #pragma unroll
-        for (int i = 0; i < kConvChunks; ++i) {
-          const int r = i * (kConvG / 8) + (ctid >> 3);
-          offs[i] = smem_u32(sA) + r * 128 + ((q ^ (r & 7)) << 4);
-          asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                       : "=f"(x[i][0]), "=f"(x[i][1]), "=f"(x[i][2]), "=f"(x[i][3])
-                       : "r"(offs[i])
-                       : "memory");
-        }
+        for (int half = 0; half < 2; ++half) {  // 16 columns at a time (register pressure)
+          uint32_t h[16], l[16];
 #pragma unroll
-        for (int i = 0; i < kConvChunks; ++i) {
-          // hi = x truncated to tf32 (exactly representable), lo = x - hi
-          // (exact in fp32); the tensor core reads lo to tf32 precision, so
-          // hi + lo carries ~21 significant bits of x.
-          uint32_t h[4], l[4];
+          for (int qq = 0; qq < 4; ++qq) {
+            const int q = 4 * half + qq;
+            float x[4];
+            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                         : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
+                         : "r"(row + ((q ^ (r & 7)) << 4)));
+            // hi = x truncated to tf32 (exactly representable), lo = x - hi
+            // (exact in fp32); the tensor core reads lo to tf32 precision, so
+            // hi + lo carries ~21 significant bits of x.
 #pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            h[j] = __float_as_uint(x[i][j]) & 0xFFFFE000u;
-            l[j] = __float_as_uint(x[i][j] - __uint_as_float(h[j]));
+            for (int j = 0; j < 4; ++j) {
+              h[4 * qq + j] = __float_as_uint(x[j]) & 0xFFFFE000u;
+              l[4 * qq + j] = __float_as_uint(x[j] - __uint_as_float(h[4 * qq + j]));
+            }
           }
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(offs[i]), "r"(h[0]), "r"(h[1]), "r"(h[2]),
-                       "r"(h[3])
-                       : "memory");
-          asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(offs[i] + kABytes), "r"(l[0]), "r"(l[1]),
-                       "r"(l[2]), "r"(l[3])
-                       : "memory");
+          tmem_st16(ta + 16 * half, h);
+          tmem_st16(ta + kBK + 16 * half, l);
         }
-        fence_proxy_async_smem();
+        tmem_st_wait();
+        tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[stage]);
         if (ctid == 0) TRACE(5, g);
@@ -284,7 +288,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     // The whole warp runs the loop (warp-uniform control flow and operands);
     // elect.sync inside the asm picks the issuing lane.
     constexpr uint32_t idesc = umma_idesc_tf32(kBM, NPAD);
-    const uint64_t desc0 = umma_desc_sw128(smem_u32(smem));  // stage 0, A_hi; others by offset
+    const uint64_t desc0 = umma_desc_sw128(smem_u32(smem));  // stage 0 base; B by offset
     const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -299,12 +303,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         mbar_wait(&full[stage], phase);
         TRACE(2, gm);
         tc_fence_after();
-        // descriptor start addresses advance in 16-B units
-        const uint64_t a_hi = desc0 + static_cast<uint64_t>((stage * C::kStageBytes) >> 4);
-        const uint64_t a_lo = a_hi + (kABytes >> 4);
-        const uint64_t b_hi = a_hi + ((2 * kABytes) >> 4);
+        // B descriptors: start addresses advance in 16-B units; A in TMEM
+        const uint64_t b_hi = desc0 + static_cast<uint64_t>((stage * C::kStageBytes + kABytes) >> 4);
         const uint64_t b_lo = b_hi + (C::kBBytes >> 4);
-        umma_tf32x3_kblock(d, a_hi, a_lo, b_hi, b_lo, idesc, kb != 0);
+        const uint32_t a_hi = tbase + C::kAColBase + stage * kACols;
+        umma_tf32x3_kblock_ts(d, a_hi, a_hi + kBK, b_hi, b_lo, idesc, kb != 0);
         umma_commit_elect(&empty[stage]);  // smem slot free once these MMAs retire
         TRACE(3, gm);
         ++gm;
@@ -314,8 +317,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         }
       }
       umma_commit_elect(&tfull[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == C::kNAcc) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
     if (lane == 0) CTA_MARK(2);
   } else if (warp < 4) {
@@ -359,8 +364,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[acc]);
-      acc ^= 1;
-      if (acc == 0) acc_phase ^= 1;
+      if (++acc == C::kNAcc) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
     }
   }
 
@@ -411,7 +418,7 @@ int conv_gemm_stages(int npad) {
 
 int conv_gemm_smem_bytes(int npad, int KB, int S) {
   const int stages = conv_gemm_stages(npad);
-  const int stage_bytes = 2 * kABytes + 2 * npad * kBK * 4;
+  const int stage_bytes = kABytes + 2 * npad * kBK * 4;
   return 1024 + stages * stage_bytes + tail_bytes(stages, KB, S);
 }
 
