@@ -377,7 +377,11 @@ def main():
         if tj.get("streams") == S and tj.get("height") == H and tj.get("width") == W:
             traffic = tj.get("dram_bytes_per_launch", {})
     hbm = peaks["hbm_gbs"] * 1e9
-    tf32 = peaks["bf16_tflops"] * 1e12 / 2  # tf32 dense = half the measured bf16 rate
+    # the tcgen05 GEMMs run kind::f16 (3xFP16 split, default) or kind::tf32
+    # (CBG_GEMM_PREC=tf32); the tensor peak is that kind's dense rate: the
+    # measured bf16 (= fp16) rate, or half of it for tf32
+    f16_gemm = os.environ.get("CBG_GEMM_PREC", "f16") != "tf32"
+    tf32 = peaks["bf16_tflops"] * 1e12 / (1 if f16_gemm else 2)
     kernels = []
     for label, (tot_ms, nl) in rep["kernels"].items():
         bb, ff = work.get(label, [0.0, 0.0])
@@ -396,10 +400,11 @@ def main():
         achieved = dom["flops_per_launch"] / (dom["ms_per_launch"] / 1000.0) / 1e12
         roof = {"bound": "tensor", "achieved": achieved, "peak": tf32 / 1e12, "unit": "TFLOP/s",
                 "frac": achieved / (tf32 / 1e12),
-                # 3xTF32 issues 3 tf32 MMAs per useful MAC: the tensor pipe's
-                # share is 3x the useful fraction (attainable useful frac <= 1/3)
+                # the split-fp32 product issues 3 MMAs per useful MAC: the tensor
+                # pipe's share is 3x the useful fraction (attainable useful frac <= 1/3)
                 "tensor_issue_frac": 3 * achieved / (tf32 / 1e12),
-                "peak_note": "tf32 dense = measured bf16 / 2; useful fp32-accurate flops (2*Cout*Cin*k^2 per changed px)"}
+                "peak_note": ("fp16 dense = measured bf16 rate" if f16_gemm else "tf32 dense = measured bf16 / 2")
+                + "; useful fp32-accurate flops (2*Cout*Cin*k^2 per changed px), 3 MMAs per useful MAC"}
     else:
         achieved = dom["bytes_per_launch"] / (dom["ms_per_launch"] / 1000.0) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -534,7 +539,11 @@ def main():
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
                "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
-               "vs_baseline": None, "dtype": "f32", "gemm_precision": "3xTF32 tcgen05 (fp32-accurate)",
+               "vs_baseline": None, "dtype": "f32",
+               "gemm_precision": ("3xFP16 tcgen05 kind::f16, fp32 operands split hi+lo with power-of-two scaling, "
+                                  "fp32 accumulate (fp32-accurate); Cout<=16 layers bit-exact on CUDA cores"
+                                  if os.environ.get("CBG_GEMM_PREC", "f16") != "tf32" else
+                                  "3xTF32 tcgen05 (fp32-accurate); Cout<=16 layers bit-exact on CUDA cores"),
                "data": "synthetic (gen_synthetic, seeded; random-init He-uniform weights)",
                "config": config_dict(a, world),
                "change": {"l1_changed_frac": l1_frac, "per_layer_changed_frac": per_layer},

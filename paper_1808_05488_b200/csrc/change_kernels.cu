@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs 
   uint8_t* m = a.map + static_cast<long long>(s) * HW;
   const bool write_all = boot || !a.closed_loop;
   const float tau = *a.tau;
+  float vmax = 0.0f;
   if constexpr (kVec4) {
     // C <= 4 (Cs == 4), HW % 4 == 0: one thread = 4 consecutive pixels; the C
     // planes are read as float4, the 4 NHWC state vectors as 4 float4.
@@ -84,8 +85,10 @@ __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs 
           for (int c = 0; c < 4; ++c)
             if (c < a.C) changed |= fabsf(px[c] - sp[c]) > tau;
         }
-        if (changed || write_all)
+        if (changed || write_all) {
           *reinterpret_cast<float4*>(st + (p0 + j) * 4) = make_float4(px[0], px[1], px[2], px[3]);
+          vmax = fmaxf(vmax, fmaxf(fmaxf(fabsf(px[0]), fabsf(px[1])), fmaxf(fabsf(px[2]), fabsf(px[3]))));
+        }
         if (changed) mark |= static_cast<uint32_t>(e) << (8 * j);
       }
       if (mark) {  // only changed pixels get the epoch tag; others keep stale tags
@@ -94,6 +97,7 @@ __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs 
           if ((mark >> (8 * j)) & 0xffu) m[p0 + j] = e;
       }
     }
+    warp_amax(a.amax ? a.amax + s : nullptr, vmax);
     return;
   }
   for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < HW;
@@ -116,11 +120,15 @@ __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs 
       for (int c0 = 0; c0 < a.Cs; c0 += 4) {
         float v[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) v[j] = (c0 + j < a.C) ? __ldg(x + (c0 + j) * HW + p) : 0.0f;
+        for (int j = 0; j < 4; ++j) {
+          v[j] = (c0 + j < a.C) ? __ldg(x + (c0 + j) * HW + p) : 0.0f;
+          vmax = fmaxf(vmax, fabsf(v[j]));
+        }
         *reinterpret_cast<float4*>(sp + c0) = make_float4(v[0], v[1], v[2], v[3]);
       }
     }
   }
+  warp_amax(a.amax ? a.amax + s : nullptr, vmax);
 }
 
 // ---------------------------------------------------------------------------
@@ -142,6 +150,7 @@ __global__ void __launch_bounds__(kThreads) detect_frame_chw_kernel(DetectFrameA
   const bool write_all = boot || !a.closed_loop;
   const float tau = *a.tau;
   const long long n4 = HW >> 2;
+  float vmax = 0.0f;
   for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long p0 = q << 2;
@@ -177,6 +186,7 @@ __global__ void __launch_bounds__(kThreads) detect_frame_chw_kernel(DetectFrameA
             if (!(ch & 8u)) v.w = sv[c].w;
           }
           *reinterpret_cast<float4*>(st + c * HW + p0) = v;
+          vmax = fmaxf(vmax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
         }
       }
     }
@@ -186,6 +196,7 @@ __global__ void __launch_bounds__(kThreads) detect_frame_chw_kernel(DetectFrameA
         if ((ch >> j) & 1u) m[p0 + j] = e;
     }
   }
+  warp_amax(a.amax ? a.amax + s : nullptr, vmax);
 }
 
 // scalar fallback (any C, any HW): CHW state, one thread per pixel
@@ -199,15 +210,21 @@ __global__ void __launch_bounds__(kThreads) detect_frame_chw_scalar_kernel(Detec
   uint8_t* m = a.map + static_cast<long long>(s) * HW;
   const bool write_all = boot || !a.closed_loop;
   const float tau = *a.tau;
+  float vmax = 0.0f;
   for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < HW;
        p += static_cast<long long>(gridDim.x) * blockDim.x) {
     bool changed = false;
     if (!boot)
       for (int c = 0; c < a.C; ++c) changed |= fabsf(__ldg(x + c * HW + p) - st[c * HW + p]) > tau;
     if (changed || write_all)
-      for (int c = 0; c < a.C; ++c) st[c * HW + p] = __ldg(x + c * HW + p);
+      for (int c = 0; c < a.C; ++c) {
+        const float v = __ldg(x + c * HW + p);
+        st[c * HW + p] = v;
+        vmax = fmaxf(vmax, fabsf(v));
+      }
     if (changed) m[p] = e;
   }
+  warp_amax(a.amax ? a.amax + s : nullptr, vmax);
 }
 
 // ---------------------------------------------------------------------------
@@ -527,6 +544,7 @@ __global__ void __launch_bounds__(kThreads) join_kernel(JoinArgs a) {
   const long long n = a.count[s];
   const int32_t* list = a.idx + static_cast<long long>(s) * a.HW;
   const long long total = n * a.Cs_out;
+  float vmax = 0.0f;
   for (long long w = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; w < total;
        w += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long k = w / a.Cs_out;
@@ -547,7 +565,9 @@ __global__ void __launch_bounds__(kThreads) join_kernel(JoinArgs a) {
       }
     }
     a.out[(static_cast<long long>(s) * a.HW + p) * a.Cs_out + c] = v;
+    vmax = fmaxf(vmax, fabsf(v));
   }
+  warp_amax(a.amax_out ? a.amax_out + s : nullptr, vmax);
 }
 
 __global__ void begin_frame_kernel(BeginFrameArgs a) {

@@ -16,6 +16,15 @@ namespace cbg {
 // clears every map once per 255 frames (runtime.cpp, Net::forward).
 CBG_DEV uint8_t epoch8(uint32_t frame) { return static_cast<uint8_t>((frame - 1u) % 255u + 1u); }
 
+// ---- running magnitude bounds (fp16 GEMM operand scales) -----------------------
+// Warp max of v >= 0, one atomicMax per warp (non-negative floats order as ints).
+// Every lane of the warp must call it.
+CBG_DEV void warp_amax(float* dst, float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  if ((threadIdx.x & 31) == 0 && dst != nullptr && v > 0.0f) atomicMax(reinterpret_cast<int*>(dst), __float_as_int(v));
+}
+
 // ---- global acquire / release --------------------------------------------------
 CBG_DEV uint64_t ld_acquire_u64(const uint64_t* p) {
   uint64_t v;
@@ -221,6 +230,32 @@ CBG_DEV void umma_tf32x3_kblock_ts(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo
       "r"(a_hi), "r"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// K=32 block of the 3-term fp16 product with A in TMEM: fp16 pairs packed per
+// 32-bit column, so a K=16 MMA spans 8 columns; B (K-major SW64, 64-B rows)
+// advances 32 B (2 in 16-B units) per k-step.
+CBG_DEV void umma_f16x3_kblock_ts(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo, uint64_t b_hi, uint64_t b_lo,
+                                  uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh, bl;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %6, 0;\n\t"
+      "mov.b32 ah, %1;\n\tmov.b32 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, 1;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [al], bh, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bl, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, 1;\n\t}" ::"r"(d_tmem),
+      "r"(a_hi), "r"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// 32 lanes x 32 bit, 8 consecutive columns per thread.
+CBG_DEV void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
 // 32 lanes x 32 bit, 32 consecutive columns per thread (this warp's lane quarter).
 CBG_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
   asm volatile(
@@ -296,6 +331,15 @@ __host__ __device__ constexpr uint32_t umma_idesc_tf32(int M, int N) {
   return (1u << 4)                                   // c_format = F32
          | (2u << 7)                                 // a_format = TF32
          | (2u << 10)                                // b_format = TF32
+         | (static_cast<uint32_t>(N >> 3) << 17)     // n_dim
+         | (static_cast<uint32_t>(M >> 4) << 24);    // m_dim
+}
+
+// Instruction descriptor for kind::f16 with fp16 A and B, fp32 accumulate, K-major.
+__host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N) {
+  return (1u << 4)                                   // c_format = F32
+         | (0u << 7)                                 // a_format = F16
+         | (0u << 10)                                // b_format = F16
          | (static_cast<uint32_t>(N >> 3) << 17)     // n_dim
          | (static_cast<uint32_t>(M >> 4) << 24);    // m_dim
 }

@@ -97,6 +97,7 @@ __global__ void __launch_bounds__(kThreads) conv_exact_kernel(ConvExactArgs a) {
   const int ps = PS ? PS : a.pstride;
   const long long rstride = static_cast<long long>(a.Win) * ps;
   for (int wb = blockIdx.x; wb < total; wb += gridDim.x) {
+    float vmax = 0.0f;
     int lo = 0, hi = a.S;  // stream s with s_prefix[s] <= wb < s_prefix[s+1]
     while (hi - lo > 1) {
       const int mid = (lo + hi) >> 1;
@@ -228,11 +229,13 @@ __global__ void __launch_bounds__(kThreads) conv_exact_kernel(ConvExactArgs a) {
             float y = __fadd_rn(acc[u][4 * q + e], o + e < a.Cout ? __ldg(a.bias + o + e) : 0.0f);
             if (a.relu) y = (y < 0.0f) ? 0.0f : y;  // std::max(v, 0.f)
             v[e] = o + e < a.Cout ? y : 0.0f;
+            vmax = fmaxf(vmax, fabsf(v[e]));
           }
           *reinterpret_cast<float4*>(orow + 4 * q) = make_float4(v[0], v[1], v[2], v[3]);
         }
       }
     }
+    warp_amax(a.amax_out ? a.amax_out + s : nullptr, vmax);
   }
 }
 

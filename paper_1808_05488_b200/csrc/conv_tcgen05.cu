@@ -40,6 +40,8 @@
 #include <climits>
 #include <cstdio>
 
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -79,18 +81,33 @@ constexpr int kFetchChunks = 128 * 8 / kFetchG;  // 16-B A chunks per fetch thre
 constexpr int kBM = 128;                 // UMMA M
 constexpr int kBK = 32;                  // fp32 elements per K-block (= one 128-B swizzle row)
 constexpr int kABytes = kBM * kBK * 4;   // raw fp32 A rows of one K-block: 16 KB
-constexpr int kACols = 2 * kBK;          // TMEM columns of one stage's A_hi | A_lo
 constexpr int kMaxS = 1024;
 
-template <int NPAD>
+// Operand precision of the split-fp32 product (both fp32-accurate):
+//   kPrecTF32: x = hi + lo in tf32 (hi = x truncated to 10 mantissa bits),
+//              kind::tf32, K = 8 per MMA, B rows of 128 B (32 fp32) per K-block.
+//   kPrecF16:  x*2^-e = hi + lo in fp16 (round-to-nearest, 11 + 11 bits), with
+//              e a per-stream power-of-two scale from a running bound of the
+//              operand magnitude (so |x*2^-e| < 2^15: no overflow), weights
+//              scaled by 2^-ew on the host; kind::f16 at twice the tf32 rate,
+//              K = 16 per MMA, B rows of 64 B (32 fp16) per K-block (SW64);
+//              the epilogue multiplies by 2^(e+ew) (exact).
+constexpr int kPrecTF32 = 0;
+constexpr int kPrecF16 = 1;
+
+template <int NPAD, int PREC>
 struct Cfg {
-  static constexpr int kBBytes = NPAD * kBK * 4;
+  static constexpr int kBRow = PREC == kPrecF16 ? 64 : 128;  // B bytes per row per K-block
+  static constexpr int kBBytes = NPAD * kBRow;
   static constexpr int kStageBytes = kABytes + 2 * kBBytes;
+  static constexpr int kACols = PREC == kPrecF16 ? kBK : 2 * kBK;  // TMEM columns of A_hi | A_lo
+  static constexpr int kALo = kACols / 2;                          // A_lo column offset
   // A multiple of kGroups, so a stage is always filled and converted by the same
   // group: with an odd count, a convert group could reach a stage one lap ahead
   // of the other group's fetch and take that stage's previous `raw` phase
   // (mbarrier parity aliases modulo 2) as complete.
-  static constexpr int kStages = NPAD >= 256 ? 2 : NPAD >= 128 ? 4 : 6;
+  static constexpr int kStages = PREC == kPrecF16 ? (NPAD >= 256 ? 4 : NPAD >= 128 ? 6 : 8)
+                                                  : (NPAD >= 256 ? 2 : NPAD >= 128 ? 4 : 6);
   static_assert(kStages % kGroups == 0, "stages must be a multiple of the producer groups");
   static constexpr int kNAcc = NPAD >= 256 ? 1 : 2;  // TMEM accumulator buffers
   static constexpr uint32_t kTmemCols = 512;
@@ -98,13 +115,23 @@ struct Cfg {
   static_assert(kNAcc * NPAD + kStages * kACols <= 512, "TMEM budget");
 };
 
+// Exponent e with bound * 2^-e < 2^15 (fp16 operands stay finite), clamped so
+// 2^-e and 2^e are normal floats.
+CBG_DEV int f16_scale_exp(float bound) {
+  const uint32_t E = (__float_as_uint(bound) >> 23) & 0xFFu;
+  if (!(bound > 0.0f) || E == 0xFFu) return 0;
+  int e = static_cast<int>(E) - 127 - 14;
+  return e < -126 ? -126 : e > 126 ? 126 : e;
+}
+CBG_DEV float exp2i(int e) { return __uint_as_float(static_cast<uint32_t>(e + 127) << 23); }
+
 __host__ __device__ constexpr int tail_bytes(int stages, int KB, int S) {
   return 8 * (3 * stages + 4) + 16 + kBM * 8 + KB * 8 * 8 + (S + 1) * 4;
 }
 
-template <int NPAD>
+template <int NPAD, int PREC>
 __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) {
-  using C = Cfg<NPAD>;
+  using C = Cfg<NPAD, PREC>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tail = smem + C::kStages * C::kStageBytes;
@@ -240,6 +267,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     const int ctid = (tid - kFirstConvWarp * 32) % kConvG;
     uint32_t g = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      float xs = 1.0f;  // fp16 operand scale 2^-e of this tile's stream
+      if constexpr (PREC == kPrecF16) {
+        int s, mt, nt;
+        decode(w, s, mt, nt);
+        xs = exp2i(-f16_scale_exp(__ldg(a.amax_in + s)));
+      }
 #pragma unroll 1
       for (int kb = 0; kb < a.KB; ++kb, ++g) {
         if (static_cast<int>(g % kGroups) != cgrp) continue;
@@ -253,28 +286,56 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         const int r = 32 * (warp & 3) + lane;
         const uint32_t row = smem_u32(sA) + r * 128;
         const uint32_t ta = tmem_base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + C::kAColBase +
-                            stage * kACols;
+                            stage * C::kACols;
+        if constexpr (PREC == kPrecF16) {
 #pragma unroll
-        for (int half = 0; half < 2; ++half) {  // 16 columns at a time (register pressure)
-          uint32_t h[16], l[16];
+          for (int half = 0; half < 2; ++half) {  // 16 elements -> 8 packed columns each of hi and lo
+            uint32_t h[8], l[8];
 #pragma unroll
-          for (int qq = 0; qq < 4; ++qq) {
-            const int q = 4 * half + qq;
-            float x[4];
-            asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
-                         : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
-                         : "r"(row + ((q ^ (r & 7)) << 4)));
-            // hi = x truncated to tf32 (exactly representable), lo = x - hi
-            // (exact in fp32); the tensor core reads lo to tf32 precision, so
-            // hi + lo carries ~21 significant bits of x.
+            for (int qq = 0; qq < 4; ++qq) {
+              const int q = 4 * half + qq;
+              float x[4];
+              asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                           : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
+                           : "r"(row + ((q ^ (r & 7)) << 4)));
+              // x*2^-e exact; hi = fp16 round-to-nearest, lo = fp16(x - hi)
+              // (x - hi exact in fp32): hi + lo carries 22 significant bits
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
-              h[4 * qq + j] = __float_as_uint(x[j]) & 0xFFFFE000u;
-              l[4 * qq + j] = __float_as_uint(x[j] - __uint_as_float(h[4 * qq + j]));
+              for (int j = 0; j < 2; ++j) {
+                const float x0 = x[2 * j] * xs, x1 = x[2 * j + 1] * xs;
+                const __half2 hh = __floats2half2_rn(x0, x1);
+                const float2 hf = __half22float2(hh);
+                const __half2 ll = __floats2half2_rn(x0 - hf.x, x1 - hf.y);
+                h[2 * qq + j] = *reinterpret_cast<const uint32_t*>(&hh);
+                l[2 * qq + j] = *reinterpret_cast<const uint32_t*>(&ll);
+              }
             }
+            tmem_st8(ta + 8 * half, h);
+            tmem_st8(ta + C::kALo + 8 * half, l);
           }
-          tmem_st16(ta + 16 * half, h);
-          tmem_st16(ta + kBK + 16 * half, l);
+        } else {
+#pragma unroll
+          for (int half = 0; half < 2; ++half) {  // 16 columns at a time (register pressure)
+            uint32_t h[16], l[16];
+#pragma unroll
+            for (int qq = 0; qq < 4; ++qq) {
+              const int q = 4 * half + qq;
+              float x[4];
+              asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];"
+                           : "=f"(x[0]), "=f"(x[1]), "=f"(x[2]), "=f"(x[3])
+                           : "r"(row + ((q ^ (r & 7)) << 4)));
+              // hi = x truncated to tf32 (exactly representable), lo = x - hi
+              // (exact in fp32); the tensor core reads lo to tf32 precision, so
+              // hi + lo carries ~21 significant bits of x.
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                h[4 * qq + j] = __float_as_uint(x[j]) & 0xFFFFE000u;
+                l[4 * qq + j] = __float_as_uint(x[j] - __uint_as_float(h[4 * qq + j]));
+              }
+            }
+            tmem_st16(ta + 16 * half, h);
+            tmem_st16(ta + C::kALo + 16 * half, l);
+          }
         }
         tmem_st_wait();
         tc_fence_before();
@@ -287,8 +348,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     // ========================= MMA issuer =========================
     // The whole warp runs the loop (warp-uniform control flow and operands);
     // elect.sync inside the asm picks the issuing lane.
-    constexpr uint32_t idesc = umma_idesc_tf32(kBM, NPAD);
-    const uint64_t desc0 = umma_desc_sw128(smem_u32(smem));  // stage 0 base; B by offset
+    constexpr uint32_t idesc = PREC == kPrecF16 ? umma_idesc_f16(kBM, NPAD) : umma_idesc_tf32(kBM, NPAD);
+    // stage 0 base; B by offset (K-major, 128-B rows for tf32, 64-B rows for fp16)
+    const uint64_t desc0 = PREC == kPrecF16 ? umma_desc_sw64(smem_u32(smem)) : umma_desc_sw128(smem_u32(smem));
     const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -306,8 +368,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         // B descriptors: start addresses advance in 16-B units; A in TMEM
         const uint64_t b_hi = desc0 + static_cast<uint64_t>((stage * C::kStageBytes + kABytes) >> 4);
         const uint64_t b_lo = b_hi + (C::kBBytes >> 4);
-        const uint32_t a_hi = tbase + C::kAColBase + stage * kACols;
-        umma_tf32x3_kblock_ts(d, a_hi, a_hi + kBK, b_hi, b_lo, idesc, kb != 0);
+        const uint32_t a_hi = tbase + C::kAColBase + stage * C::kACols;
+        if constexpr (PREC == kPrecF16)
+          umma_f16x3_kblock_ts(d, a_hi, a_hi + C::kALo, b_hi, b_lo, idesc, kb != 0);
+        else
+          umma_tf32x3_kblock_ts(d, a_hi, a_hi + C::kALo, b_hi, b_lo, idesc, kb != 0);
         umma_commit_elect(&empty[stage]);  // smem slot free once these MMAs retire
         TRACE(3, gm);
         ++gm;
@@ -336,6 +401,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       const int p = valid ? a.idx[s * HWout + k] : 0;
       float* orow = a.out + (s * HWout + p) * a.Co4;
       const int nbase = nt * NPAD;
+      float ys = 1.0f;  // undo the fp16 operand scales: 2^(e + ew), two exact steps
+      if constexpr (PREC == kPrecF16) ys = exp2i(f16_scale_exp(__ldg(a.amax_in + s)));
+      const float ws = PREC == kPrecF16 ? exp2i(a.w_exp) : 1.0f;
+      float vmax = 0.0f;  // |written value| bound for the consumers' scales
       mbar_wait(&tfull[acc], acc_phase);
       tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + acc * NPAD;
@@ -352,9 +421,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
               float o[4];
 #pragma unroll
               for (int u = 0; u < 4; ++u) {
-                float y = __uint_as_float(r[4 * j + u]) + __ldg(a.bias + n + u);
+                float y = __uint_as_float(r[4 * j + u]);
+                if constexpr (PREC == kPrecF16) y = (y * ys) * ws;
+                y = y + __ldg(a.bias + n + u);
                 if (a.relu) y = (y < 0.0f) ? 0.0f : y;  // std::max(v, 0.f)
                 o[u] = y;
+                vmax = fmaxf(vmax, fabsf(y));
               }
               *reinterpret_cast<float4*>(orow + n) = make_float4(o[0], o[1], o[2], o[3]);
             }
@@ -362,8 +434,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         }
       }
       tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
+      if (lane == 0) {
+        mbar_arrive(&tempty[acc]);
+        if (a.amax_out) atomicMax(reinterpret_cast<int*>(a.amax_out + s), __float_as_int(vmax));
+      }
       if (++acc == C::kNAcc) {
         acc = 0;
         acc_phase ^= 1;
@@ -380,15 +456,37 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   }
 }
 
-template <int NPAD>
+template <int NPAD, int PREC>
 void launch_impl(const ConvGemmArgs& a, cudaStream_t st) {
-  const int smem = conv_gemm_smem_bytes(NPAD, a.KB, a.S);
+  const int smem = conv_gemm_smem_bytes(NPAD, a.KB, a.S, PREC);
   static bool configured = false;
   if (!configured) {
-    cudaFuncSetAttribute(conv_gemm_kernel<NPAD>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+    cudaFuncSetAttribute(conv_gemm_kernel<NPAD, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     configured = true;
   }
-  conv_gemm_kernel<NPAD><<<a.grid, kThreads, smem, st>>>(a);
+  conv_gemm_kernel<NPAD, PREC><<<a.grid, kThreads, smem, st>>>(a);
+}
+
+template <int PREC>
+void launch_prec(const ConvGemmArgs& a, cudaStream_t st) {
+  switch (a.npad) {
+    case 16: launch_impl<16, PREC>(a, st); break;
+    case 32: launch_impl<32, PREC>(a, st); break;
+    case 64: launch_impl<64, PREC>(a, st); break;
+    case 128: launch_impl<128, PREC>(a, st); break;
+    default: launch_impl<256, PREC>(a, st); break;
+  }
+}
+
+template <int PREC>
+int stages_prec(int npad) {
+  switch (npad) {
+    case 16: return Cfg<16, PREC>::kStages;
+    case 32: return Cfg<32, PREC>::kStages;
+    case 64: return Cfg<64, PREC>::kStages;
+    case 128: return Cfg<128, PREC>::kStages;
+    default: return Cfg<256, PREC>::kStages;
+  }
 }
 
 }  // namespace
@@ -406,30 +504,19 @@ int conv_gemm_read_trace(unsigned long long* host, int n) {
 #endif
 }
 
-int conv_gemm_stages(int npad) {
-  switch (npad) {
-    case 16: return Cfg<16>::kStages;
-    case 32: return Cfg<32>::kStages;
-    case 64: return Cfg<64>::kStages;
-    case 128: return Cfg<128>::kStages;
-    default: return Cfg<256>::kStages;
-  }
+int conv_gemm_stages(int npad, int prec) {
+  return prec == kPrecF16 ? stages_prec<kPrecF16>(npad) : stages_prec<kPrecTF32>(npad);
 }
 
-int conv_gemm_smem_bytes(int npad, int KB, int S) {
-  const int stages = conv_gemm_stages(npad);
-  const int stage_bytes = kABytes + 2 * npad * kBK * 4;
+int conv_gemm_smem_bytes(int npad, int KB, int S, int prec) {
+  const int stages = conv_gemm_stages(npad, prec);
+  const int stage_bytes = kABytes + 2 * npad * (prec == kPrecF16 ? 64 : 128);
   return 1024 + stages * stage_bytes + tail_bytes(stages, KB, S);
 }
 
 void launch_conv_gemm(const ConvGemmArgs& a, cudaStream_t st) {
-  switch (a.npad) {
-    case 16: launch_impl<16>(a, st); break;
-    case 32: launch_impl<32>(a, st); break;
-    case 64: launch_impl<64>(a, st); break;
-    case 128: launch_impl<128>(a, st); break;
-    default: launch_impl<256>(a, st); break;
-  }
+  if (a.prec == kPrecF16) launch_prec<kPrecF16>(a, st);
+  else launch_prec<kPrecTF32>(a, st);
 }
 
 }  // namespace cbg

@@ -29,6 +29,7 @@ struct DetectFrameArgs {
   const float* tau;    // device scalar (set_thresholds needs no re-capture)
   int closed_loop;
   int state_chw;       // state is [S][C][H][W] (unpadded planes) instead of NHWC
+  float* amax;         // [S] running max |value written to the state| (atomicMax)
 };
 void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st);
 
@@ -92,6 +93,7 @@ struct JoinArgs {
   const int32_t* idx;
   const int32_t* count;
   int HW, S;
+  float* amax_out;       // [S] running max |written value|
 };
 void launch_join(const JoinArgs& a, cudaStream_t st);
 
@@ -113,10 +115,14 @@ struct ConvGemmArgs {
   int relu;
   int S;
   int grid;                // persistent CTAs (<= SM count)
+  int prec;                // 0: 3xTF32, 1: 3xFP16 with power-of-two scaling (conv_tcgen05.cu)
+  int w_exp;               // fp16: weights were scaled by 2^-w_exp on the host
+  const float* amax_in;    // [S] bound of |source values| (fp16 operand scale)
+  float* amax_out;         // [S] running max |written output| (atomicMax), nullable
 };
 void launch_conv_gemm(const ConvGemmArgs& a, cudaStream_t st);
-int conv_gemm_smem_bytes(int npad, int KB, int S);
-int conv_gemm_stages(int npad);
+int conv_gemm_smem_bytes(int npad, int KB, int S, int prec);
+int conv_gemm_stages(int npad, int prec);
 
 // Bit-exact CUDA-core update for narrow layers (Cout <= 16): the reference's
 // sequential non-FMA fp32 sum in im2col row order (conv_exact.cu).
@@ -135,6 +141,7 @@ struct ConvExactArgs {
   int relu;
   int S;
   int sm_count;
+  float* amax_out;         // [S] running max |written value|
 };
 void launch_conv_exact(const ConvExactArgs& a, cudaStream_t st);
 int conv_exact_group(int cout);

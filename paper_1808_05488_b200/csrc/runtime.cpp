@@ -313,13 +313,52 @@ uint32_t tf32_round(float x) {  // round-to-nearest-away into the top 19 bits (c
 
 // Pre-swizzled UMMA SW128 K-major images of the (kj, ki, c)-ordered weight
 // matrix, split into tf32 hi / lo: [n_tile][kb][hi|lo][npad rows][128 B].
+// IEEE binary16 round-to-nearest-even of a float (normal, subnormal, overflow to inf).
+uint16_t f16_rn(float f) {
+  uint32_t x;
+  std::memcpy(&x, &f, 4);
+  const uint32_t sign = (x >> 16) & 0x8000u;
+  const uint32_t ax = x & 0x7fffffffu;
+  if (ax >= 0x7f800000u) return static_cast<uint16_t>(sign | 0x7c00u | (ax > 0x7f800000u ? 0x200u : 0u));
+  if (ax >= 0x477ff000u) return static_cast<uint16_t>(sign | 0x7c00u);  // rounds to >= 65520: inf
+  if (ax < 0x38800000u) {  // below 2^-14: fp16 subnormal (or zero), quantum 2^-24
+    const float q = std::ldexp(std::fabs(f), 24);
+    const float r = std::nearbyint(q);  // round-half-even under the default rounding mode
+    return static_cast<uint16_t>(sign | static_cast<uint32_t>(r));
+  }
+  uint32_t m = ax + 0xfffu + ((ax >> 13) & 1u);  // round the 13 dropped bits to nearest even
+  return static_cast<uint16_t>(sign | ((m - 0x38000000u) >> 13));
+}
+float f16_to_f32(uint16_t h) {
+  const uint32_t sign = (h & 0x8000u) << 16, e = (h >> 10) & 0x1fu, m = h & 0x3ffu;
+  float v;
+  if (e == 0) v = std::ldexp(static_cast<float>(m), -24);
+  else if (e == 31) v = m ? NAN : INFINITY;
+  else v = std::ldexp(static_cast<float>(m | 0x400u), static_cast<int>(e) - 25);
+  return sign ? -v : v;
+}
+
+// Exponent ew with max|w| * 2^-ew < 2^15 (mirrors f16_scale_exp in conv_tcgen05.cu).
+int weight_exp(const std::vector<float>& w) {
+  float m = 0.0f;
+  for (float v : w) m = std::max(m, std::fabs(v));
+  if (!(m > 0.0f) || !std::isfinite(m)) return 0;
+  uint32_t u;
+  std::memcpy(&u, &m, 4);
+  const int e = static_cast<int>((u >> 23) & 0xffu) - 127 - 14;
+  return std::min(126, std::max(-126, e));
+}
+
 void build_weight_image(const NodeRT& n, std::vector<uint8_t>& img, std::vector<uint32_t>& ktab,
                         std::vector<float>& bias) {
   const ConvDesc& c = n.d.conv;
   const int taps = c.kernel_h * c.kernel_w;
   const int Kreal = taps * n.Csi;
-  const int Bbytes = n.npad * 128;
+  const bool f16 = n.prec == 1;
+  const int Brow = f16 ? 64 : 128;
+  const int Bbytes = n.npad * Brow;
   img.assign(static_cast<size_t>(n.n_tiles) * n.KB * 2 * Bbytes, 0);
+  const float wscale = std::ldexp(1.0f, -n.w_exp);
   auto wval = [&](int o, int k) -> float {
     if (o >= c.out_channels || k >= Kreal) return 0.0f;
     const int t = k / n.Csi, ch = k % n.Csi;
@@ -330,18 +369,32 @@ void build_weight_image(const NodeRT& n, std::vector<uint8_t>& img, std::vector<
   for (int nt = 0; nt < n.n_tiles; ++nt)
     for (int kb = 0; kb < n.KB; ++kb) {
       uint8_t* base = img.data() + (static_cast<size_t>(nt) * n.KB + kb) * 2 * Bbytes;
-      for (int r = 0; r < n.npad; ++r)
-        for (int q = 0; q < 8; ++q)
-          for (int j = 0; j < 4; ++j) {
-            const float w = wval(nt * n.npad + r, kb * 32 + q * 4 + j);
-            const uint32_t hi = tf32_round(w);
-            float hf;
-            std::memcpy(&hf, &hi, 4);
-            const uint32_t lo = tf32_round(w - hf);
-            const size_t off = static_cast<size_t>(r) * 128 + ((q ^ (r & 7)) << 4) + j * 4;
-            std::memcpy(base + off, &hi, 4);
-            std::memcpy(base + Bbytes + off, &lo, 4);
-          }
+      for (int r = 0; r < n.npad; ++r) {
+        if (f16) {
+          // K-major SWIZZLE_64B: 64-B rows, 16-B chunk q at (q ^ ((r >> 1) & 3))
+          for (int q = 0; q < 4; ++q)
+            for (int j = 0; j < 8; ++j) {
+              const float w = wval(nt * n.npad + r, kb * 32 + q * 8 + j) * wscale;  // exact (power of 2)
+              const uint16_t hi = f16_rn(w);
+              const uint16_t lo = f16_rn(w - f16_to_f32(hi));
+              const size_t off = static_cast<size_t>(r) * 64 + ((q ^ ((r >> 1) & 3)) << 4) + j * 2;
+              std::memcpy(base + off, &hi, 2);
+              std::memcpy(base + Bbytes + off, &lo, 2);
+            }
+        } else {
+          for (int q = 0; q < 8; ++q)
+            for (int j = 0; j < 4; ++j) {
+              const float w = wval(nt * n.npad + r, kb * 32 + q * 4 + j);
+              const uint32_t hi = tf32_round(w);
+              float hf;
+              std::memcpy(&hf, &hi, 4);
+              const uint32_t lo = tf32_round(w - hf);
+              const size_t off = static_cast<size_t>(r) * 128 + ((q ^ (r & 7)) << 4) + j * 4;
+              std::memcpy(base + off, &hi, 4);
+              std::memcpy(base + Bbytes + off, &lo, 4);
+            }
+        }
+      }
     }
   ktab.assign(static_cast<size_t>(n.KB) * 8, 0);
   for (int kb = 0; kb < n.KB; ++kb)
@@ -358,6 +411,13 @@ void build_weight_image(const NodeRT& n, std::vector<uint8_t>& img, std::vector<
     }
   bias.assign(static_cast<size_t>(n.n_tiles) * n.npad, 0.0f);
   for (int o = 0; o < c.out_channels; ++o) bias[o] = c.bias[o];
+}
+
+// tcgen05 operand split: 3xFP16 with power-of-two scaling (default) or 3xTF32
+// (CBG_GEMM_PREC=tf32); both fp32-accurate, DESIGN.md §3.3.
+int gemm_prec() {
+  const char* e = std::getenv("CBG_GEMM_PREC");
+  return (e && std::strcmp(e, "tf32") == 0) ? 0 : 1;
 }
 
 // Layers with at most this many output channels take the bit-exact CUDA-core
@@ -403,6 +463,8 @@ std::unique_ptr<Net> Net::clone() const {
     if (a.state.bytes) CK(cudaMemcpy(b.state.p, a.state.p, a.state.bytes, cudaMemcpyDeviceToDevice));
   }
   CK(cudaMemcpy(c->boot_req_.p, boot_req_.p, S_, cudaMemcpyDeviceToDevice));
+  CK(cudaMemcpy(c->amax_.p, amax_.p, amax_.bytes, cudaMemcpyDeviceToDevice));
+  c->ext_amax_ = ext_amax_;
   c->host_taus_ = host_taus_;
   CK(cudaMemcpy(c->taus_.p, taus_.p, taus_.bytes, cudaMemcpyDeviceToDevice));
   CK(cudaMemcpy(c->rescan_req_.p, rescan_req_.p, rescan_req_.bytes, cudaMemcpyDeviceToDevice));
@@ -456,6 +518,8 @@ void Net::build() {
       } else {
         if (r.KB > 512) throw Error(CBG_ERR_UNSUPPORTED, "Cin*kh*kw too large for the GEMM kernel (K > 16384)");
         if (r.Csi >= 32768) throw Error(CBG_ERR_UNSUPPORTED, "too many input channels");
+        r.prec = gemm_prec();
+        r.w_exp = r.prec == 1 ? weight_exp(c.weights) : 0;
         std::vector<uint8_t> img;
         std::vector<uint32_t> ktab;
         build_weight_image(r, img, ktab, bias);
@@ -511,6 +575,13 @@ void Net::build() {
   for (int i = 0; i < n; ++i) host_taus_[i] = nodes_[i].d.tau;
   CK(cudaMemcpy(taus_.p, host_taus_.data(), n * sizeof(float), cudaMemcpyHostToDevice));
   counts_.alloc(static_cast<size_t>(std::max(1, n_slots_)) * S_ * sizeof(int32_t));
+  amax_.alloc(static_cast<size_t>(n + 1) * S_ * sizeof(float));
+  ext_amax_.assign(S_, 0.0f);
+}
+
+int Net::amax_origin(int node) const {
+  while (node >= 0 && nodes_[node].d.kind == CBG_LAYER_POOL) node = nodes_[node].d.inputs[0];
+  return node;  // -1 = network input
 }
 
 void Net::clear_maps() {
@@ -560,7 +631,7 @@ void Net::enqueue_frame(unsigned flags) {
         if (!prod) {
           DetectFrameArgs a{frame_slot_.as<const float*>(), r.state.as<float>(), r.inmap.as<uint8_t>(), frame, boot,
                             d.Ci, r.Csi, d.Hi, d.Wi, S_, taus_.as<float>() + i,
-                            topo_.mode == CBG_MODE_CLOSEDLOOP, r.state_chw};
+                            topo_.mode == CBG_MODE_CLOSEDLOOP, r.state_chw, amax_entry(-1)};
           timed(d.name + ".detect", [&] { launch_detect_frame(a, st); });
         } else {
           const bool ext = prod->d.kind == kExternal;  // standalone layer: arbitrary x, dense detect
@@ -638,6 +709,7 @@ void Net::enqueue_frame(unsigned flags) {
         x.relu = d.relu;
         x.S = S_;
         x.sm_count = ctx_->sm_count;
+        x.amax_out = amax_entry(i);
         timed(d.name + ".gemm", [&] { launch_conv_exact(x, st); });
         continue;
       }
@@ -655,6 +727,10 @@ void Net::enqueue_frame(unsigned flags) {
       g.relu = d.relu;
       g.S = S_;
       g.grid = ctx_->sm_count;
+      g.prec = r.prec;
+      g.w_exp = r.w_exp;
+      g.amax_in = amax_entry(amax_origin(src));  // state / producer output values come from here
+      g.amax_out = amax_entry(i);
       timed(d.name + ".gemm", [&] { launch_conv_gemm(g, st); });
     } else if (d.kind == CBG_LAYER_POOL) {
       DilateCompactArgs dc{};
@@ -702,6 +778,7 @@ void Net::enqueue_frame(unsigned flags) {
       ja.count = counts + r.count_slot * S_;
       ja.HW = d.H * d.W;
       ja.S = S_;
+      ja.amax_out = amax_entry(i);
       timed(d.name + ".join", [&] { launch_join(ja, st); });
     }
   }
@@ -824,6 +901,14 @@ void Net::set_external(const float* x_chw, const uint8_t* map, const int32_t* ro
   const NodeDesc& d = e.d;
   cudaStream_t st = ctx_->stream;
   const size_t HW = static_cast<size_t>(d.H) * d.W;
+  // running bound of the uploaded values (the consumer's state holds earlier uploads too)
+  {
+    float m = ext_amax_[0];
+    const size_t n_el = static_cast<size_t>(d.C) * HW;
+    for (size_t k = 0; k < n_el; ++k) m = std::max(m, std::fabs(x_chw[k]));
+    ext_amax_[0] = m;
+    CK(cudaMemcpyAsync(amax_entry(0), &ext_amax_[0], sizeof(float), cudaMemcpyHostToDevice, st));
+  }
   // the frame of the external node is a CHW staging copy
   CK(cudaMemcpyAsync(frame_.p, x_chw, static_cast<size_t>(d.C) * HW * sizeof(float), cudaMemcpyHostToDevice, st));
   launch_chw_to_nhwc(frame_.as<float>(), e.out.as<float>(), d.C, e.Cs, static_cast<int>(HW), st);
@@ -864,6 +949,9 @@ void Net::reset(int stream) {
     }
   }
   CK(cudaMemsetAsync(boot_req_.as<uint8_t>() + s0, 1, s1 - s0, st));
+  for (int e = 0; e <= static_cast<int>(nodes_.size()); ++e)
+    CK(cudaMemsetAsync(amax_.as<float>() + static_cast<size_t>(e) * S_ + s0, 0, (s1 - s0) * sizeof(float), st));
+  for (int k = s0; k < s1; ++k) ext_amax_[k] = 0.0f;
 }
 
 void Net::set_thresholds(const std::vector<float>& taus) {

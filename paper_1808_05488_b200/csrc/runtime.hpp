@@ -92,6 +92,8 @@ struct NodeRT {
   int Cs = 0, Csi = 0;           // padded channel strides (out / in)
   // conv
   int npad = 0, n_tiles = 0, KB = 0;
+  int prec = 1;                  // tcgen05 operand split: 0 = 3xTF32, 1 = 3xFP16 (scaled)
+  int w_exp = 0;                 // fp16: weights scaled by 2^-w_exp in the image
   bool exact = false;            // CUDA-core bit-exact path (conv_exact.cu) instead of tcgen05
   bool state_chw = false;        // first-layer exact conv: input state as CHW planes (= the frame layout)
   DevBuf wimg, ktab, bias, wraw; // wraw: [Cout][Cin*kh*kw] fp32 for the exact path
@@ -158,6 +160,12 @@ class Net {
   std::vector<NodeRT> nodes_;
   DevBuf frame_, frame_slot_, frame_ctr_, boot_req_, boot_now_, dense_flag_, rescan_req_, rescan_now_,
       taus_, counts_;
+  // running max |value| per stream: entry 0 = network input (state of the first
+  // layer), entry i+1 = node i's output; the fp16 GEMM scales come from these
+  DevBuf amax_;
+  float* amax_entry(int node) const { return amax_.as<float>() + static_cast<size_t>(node + 1) * S_; }
+  int amax_origin(int node) const;  // node whose entry bounds node's output values (pools pass through)
+  std::vector<float> ext_amax_;      // host running max of standalone-layer uploads
   int n_slots_ = 0;
   uint32_t host_frame_ = 0;
   unsigned last_flags_ = 0;
