@@ -220,3 +220,31 @@ def test_pool_layers_bit_exact(gpu):
             assert np.array_equal(g.prev_output, r.prev_output)
     with pytest.raises(cbi.ConfigError):
         cbi.CBPoolLayer(2, 2, 1, 4, 4, 2, 2).forward(np.zeros((1, 4, 4), np.float32))
+
+
+@pytest.mark.parametrize("prec", ["f16", "tf32"])
+@pytest.mark.parametrize("scale", [1.0, 3.0e4, 2.0e-5])
+def test_tensor_precisions_and_operand_scaling(gpu, monkeypatch, prec, scale):
+    """Both tcgen05 operand splits (3xFP16 with power-of-two scaling, the
+    default, and 3xTF32) are fp32-accurate over magnitudes far outside fp16's
+    range: inputs scaled by 3e4 (fp16 would overflow unscaled) and 2e-5 (the
+    lo parts would be subnormal unscaled). Error is measured relative to the
+    output's magnitude."""
+    monkeypatch.setenv("CBG_GEMM_PREC", prec)
+    rng = np.random.default_rng(77)
+    spec = rand_spec(rng, 24, kernels=(3,), stride=1, pad=1)
+    spec.out_channels = 48
+    a = 1.0 / np.sqrt(24 * 9)
+    spec.weights = rng.uniform(-a, a, spec.weight_count()).astype(np.float32)
+    spec.bias = (scale * rng.uniform(-0.1, 0.1, 48)).astype(np.float32)
+    g, r = pair(spec, 0.0, h=40, w=36)
+    x = (scale * rng.uniform(-1, 1, (24, 40, 36))).astype(np.float32)
+    for t in range(3):
+        g.forward(x, force_full_update=(t == 0))
+        r.forward(x, force=(t == 0))
+        want = r.prev_output
+        rel = np.max(np.abs(g.prev_output.astype(np.float64) - want)) / np.max(np.abs(want))
+        print(f"{prec} scale {scale}: relative error {rel:.3g}")
+        assert rel <= 5e-6, f"{prec} scale {scale}: relative error {rel}"
+        x = x.copy()
+        x[:, rng.integers(0, 40, 50), rng.integers(0, 36, 50)] *= -1.5
