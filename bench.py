@@ -80,6 +80,7 @@ def config_dict(a, world):
             "total_streams": a.streams * world, "stream_groups": a.groups, "frame_ring": a.ring,
             "objects": a.objects, "object_size": a.object_size,
             "velocity": a.velocity, "noise_std": a.noise, "tau": a.tau,
+            "frames": "gen_synthetic quantized to 8-bit PNM payloads; fp32 arms see load_pnm's byte/255.0f",
             "parallelism": f"streams sharded over {world} GPU(s), no collective",
             "l2": "inputs larger than L2 (frame ring + per-stream state >> 126 MB)"}
 
@@ -94,7 +95,7 @@ def run_ref_bench(a, threads, frames, budget, streams=None):
     cmd = [REF_BENCH, "--height", str(a.height), "--width", str(a.width), "--streams", str(streams),
            "--threads", str(threads), "--frames", str(frames), "--objects", str(a.objects),
            "--object-size", str(a.object_size), "--velocity", str(a.velocity), "--noise", str(a.noise),
-           "--tau", str(a.tau), "--time-budget", str(budget)]
+           "--tau", str(a.tau), "--time-budget", str(budget), "--pnm8"]
     out = subprocess.run(cmd, capture_output=True, text=True, check=True).stdout
     return json.loads(out.strip().splitlines()[-1])
 
@@ -256,12 +257,18 @@ def main():
     L = max(3, a.ring)
     # frame ring [L][S][C][H][W], pinned on the host and resident in HBM; played
     # ping-pong (1..L-1, L-2..2, ...) so motion stays continuous for any step count
+    # The frames are what a PNM sequence delivers (cbi run -> load_pnm): 8-bit
+    # payloads ([H][W][C] bytes) of gen_synthetic frames; the fp32 arm sees
+    # load_pnm's byte / 255.0f of the same bytes, so every arm runs one workload.
     host = torch.empty((L, S, 3, H, W), dtype=torch.float32, pin_memory=True)
-    hnp = host.numpy()
+    host8 = torch.empty((L, S, H, W, 3), dtype=torch.uint8, pin_memory=True)
+    hnp, h8np = host.numpy(), host8.numpy()
     shard = weak_shard(S, rank, world)  # streams rank*S .. rank*S+S-1, seed 1000 + global id
     for s in range(S):
-        hnp[:, s] = cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, L, a.objects, a.object_size, a.velocity,
-                                                          a.velocity, a.noise, shard.seed(s)))
+        raw = cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, L, a.objects, a.object_size, a.velocity,
+                                                    a.velocity, a.noise, shard.seed(s)))
+        h8np[:, s] = cbi.to_pnm8(raw)
+        hnp[:, s] = cbi.from_pnm8(h8np[:, s])
     dev = host.to(f"cuda:{local}")
     torch.cuda.synchronize()
     order = list(range(1, L)) + list(range(L - 2, 1, -1))
@@ -270,6 +277,7 @@ def main():
         return order[k % len(order)]
 
     frame_bytes = S * 3 * H * W * 4
+    frame8_bytes = S * 3 * H * W
 
     def barrier():
         if world > 1:
@@ -453,8 +461,8 @@ def main():
                 shn = sh.numpy()
 
                 def _gen(s_, ob=ob, sz=sz, shn=shn):
-                    shn[:, s_] = cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, R, ob, sz, a.velocity, a.velocity,
-                                                                       a.noise, shard.seed(s_)))
+                    shn[:, s_] = cbi.from_pnm8(cbi.to_pnm8(cbi.gen_synthetic(cbi.SyntheticConfig(
+                        H, W, 3, R, ob, sz, a.velocity, a.velocity, a.noise, shard.seed(s_)))))
                 with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as pool:
                     list(pool.map(_gen, range(S)))
                 sdev = sh.to(f"cuda:{local}")
@@ -500,30 +508,44 @@ def main():
                 break
 
     # ---- e2e: host frames through the C ABI, H2D + D2H in the timed region -------
-    e2e = None
+    # headline: 8-bit PNM payloads (cbg_net_forward_u8, load_pnm's conversion on
+    # the device); also the fp32 Tensor3 API (cbg_net_forward) with host frames
+    e2e = e2e_f32 = None
     if not a.no_e2e:
-        enets = [cbi.convert_to_cb(spec, taus, n_streams=Sg, ctx=ctxs[g]) for g in range(G)]
-        out_bytes = enets[0].output_bytes(-1)
-        out_host = [torch.empty(out_bytes // 4, dtype=torch.float32, pin_memory=True) for _ in range(G)]
-        for g in range(G):
-            enets[g].enqueue(hnp[0, g * Sg:(g + 1) * Sg])
-        for k in range(a.warmup):
-            for g in range(G):
-                enets[g].enqueue(hnp[frame_at(k), g * Sg:(g + 1) * Sg])
-        for c in ctxs:
-            c.synchronize()
-        barrier()
+        def run_e2e(u8):
+            enets = [cbi.convert_to_cb(spec, taus, n_streams=Sg, ctx=ctxs[g]) for g in range(G)]
+            out_bytes = enets[0].output_bytes(-1)
+            out_host = [torch.empty(out_bytes // 4, dtype=torch.float32, pin_memory=True) for _ in range(G)]
 
-        def e2e_step(k):
+            def put(g, k):
+                if u8:
+                    enets[g].enqueue_u8(h8np[k, g * Sg:(g + 1) * Sg])
+                else:
+                    enets[g].enqueue(hnp[k, g * Sg:(g + 1) * Sg])
             for g in range(G):
-                enets[g].enqueue(hnp[frame_at(base_k + k), g * Sg:(g + 1) * Sg])
-                enets[g].copy_output_async(out_host[g].data_ptr())
+                put(g, 0)
+            for k in range(a.warmup):
+                for g in range(G):
+                    put(g, frame_at(k))
+            for c in ctxs:
+                c.synchronize()
+            barrier()
 
-        ems = max_over_ranks(timed_region(e2e_step, a.steps))
-        e2e = {"value": S * world * a.steps / (ems / 1000.0), "unit": "frames/s",
-               "h2d_bytes_per_step": frame_bytes, "d2h_bytes_per_step": out_bytes * G,
-               "ms_per_step": ems / a.steps}
-        del enets
+            def e2e_step(k):
+                for g in range(G):
+                    put(g, frame_at(base_k + k))
+                    enets[g].copy_output_async(out_host[g].data_ptr())
+
+            ems = max_over_ranks(timed_region(e2e_step, a.steps))
+            del enets
+            return {"value": S * world * a.steps / (ems / 1000.0), "unit": "frames/s",
+                    "h2d_bytes_per_step": frame8_bytes if u8 else frame_bytes, "d2h_bytes_per_step": out_bytes * G,
+                    "ms_per_step": ems / a.steps}
+        e2e = run_e2e(True)
+        e2e["api"] = ("cbg_net_forward_u8: pinned host 8-bit PNM payloads [S][H][W][3], load_pnm conversion "
+                      "(byte/255.0f) fused into the first layer's detect; D2H of the last node's output")
+        e2e_f32 = run_e2e(False)
+        e2e_f32["api"] = "cbg_net_forward: pinned host fp32 CHW frames (Tensor3); D2H of the last node's output"
 
     # ---- CPU baseline (rank 0, N=1) ---------------------------------------------
     cpu = None
@@ -549,7 +571,8 @@ def main():
                "change": {"l1_changed_frac": l1_frac, "per_layer_changed_frac": per_layer},
                "dense_path_fps": dense_fps, "speedup_vs_dense": (value / dense_fps) if dense_fps else None,
                "sweep": sweep, "crossover_l1_changed_pct": crossover,
-               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches * a.steps,
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_f32": e2e_f32,
+               "gpu_launches": launches * a.steps,
                "clocks": clocks.summary()}
         print(json.dumps(out))
     if world > 1:

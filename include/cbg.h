@@ -168,6 +168,12 @@ int cbg_net_node_info(cbg_net net, int node, cbg_node_info* info);
  * n_streams frames, CHW each. Host pointers are copied in on the ctx stream
  * (pinned memory makes it asynchronous). Flags: CBG_FWD_*. */
 int cbg_net_forward(cbg_net net, const float* frames, unsigned flags);
+/* Same frame step with 8-bit frames in the byte order of a binary PNM payload
+ * (P5 gray / P6 RGB: [n_streams][H][W][C] interleaved, maxval 255), converted
+ * on the device exactly as load_pnm does (io.cpp:349-399: planar fp32 =
+ * byte / 255.0f, IEEE division). A quarter of the fp32 ingest bytes. The
+ * network input must have C <= 4 channels. Flags: CBG_FWD_*. */
+int cbg_net_forward_u8(cbg_net net, const uint8_t* frames_hwc, unsigned flags);
 /* reset() (network.cpp:274-290); stream = -1 resets all streams. */
 int cbg_net_reset(cbg_net net, int stream);
 /* set_thresholds() / thresholds() (network.cpp:256-272). */

@@ -15,6 +15,7 @@
 // Output: one JSON object on stdout.
 #include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <chrono>
 #include <cstdio>
 #include <cstdlib>
@@ -106,6 +107,9 @@ int main(int argc, char** argv) {
   const double tau = arg_dbl(argc, argv, "--tau", 0.05);
   const double budget_s = arg_dbl(argc, argv, "--time-budget", 20.0);
   const bool dense = has_flag(argc, argv, "--dense");
+  // --pnm8: frames as a PNM sequence would deliver them (bench.py's workload):
+  // byte = floor(clamp(v, 0, 1) * 255 + 0.5), then load_pnm's byte / 255.0f
+  const bool pnm8 = has_flag(argc, argv, "--pnm8");
 
   NetworkSpec spec = seg_spec(h, w);
   DenseNetwork net = build_network(spec);
@@ -124,6 +128,12 @@ int main(int argc, char** argv) {
     cfg.noise_std = static_cast<float>(noise);
     cfg.seed = 1000u + static_cast<unsigned>(s);
     seqs[s] = gen_synthetic(cfg);
+    if (pnm8)
+      for (Tensor3& f : seqs[s])
+        for (float& v : f.data) {
+          const float q = std::floor(std::min(std::max(v, 0.0f), 1.0f) * 255.0f + 0.5f);
+          v = static_cast<float>(static_cast<unsigned char>(q)) / 255.0f;
+        }
   }
 
   std::vector<CBNetwork> nets(streams, proto);

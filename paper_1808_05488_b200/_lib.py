@@ -100,6 +100,7 @@ SIGNATURES = {
     "cbg_net_stream_count": (C.c_int, [_vp, _P(C.c_int)]),
     "cbg_net_node_info": (C.c_int, [_vp, C.c_int, _P(NodeInfoC)]),
     "cbg_net_forward": (C.c_int, [_vp, _vp, C.c_uint]),
+    "cbg_net_forward_u8": (C.c_int, [_vp, _vp, C.c_uint]),
     "cbg_net_reset": (C.c_int, [_vp, C.c_int]),
     "cbg_net_set_thresholds": (C.c_int, [_vp, _vp, C.c_int]),
     "cbg_net_thresholds": (C.c_int, [_vp, _vp, C.c_int]),

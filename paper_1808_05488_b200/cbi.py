@@ -171,6 +171,21 @@ def gen_synthetic(cfg: SyntheticConfig, with_corners: bool = False):
     return (frames, corners) if with_corners else frames
 
 
+def to_pnm8(frames: np.ndarray) -> np.ndarray:
+    """8-bit PNM payload ([..., H, W, C] uint8) of planar fp32 frames ([..., C, H, W]):
+    byte = floor(clamp(v, 0, 1) * 255 + 0.5) in fp32 (what a camera / PNM writer
+    would store; the reference has no writer, only load_pnm)."""
+    f = np.clip(np.asarray(frames, np.float32), np.float32(0), np.float32(1))
+    q = np.floor(f * np.float32(255.0) + np.float32(0.5)).astype(np.uint8)
+    return np.ascontiguousarray(np.moveaxis(q, -3, -1))
+
+
+def from_pnm8(payload: np.ndarray) -> np.ndarray:
+    """load_pnm's conversion (io.cpp:389-397): [..., H, W, C] bytes -> [..., C, H, W] fp32 = byte / 255.0f."""
+    return np.ascontiguousarray(np.moveaxis(np.asarray(payload, np.uint8).astype(np.float32) / np.float32(255.0),
+                                            -1, -3))
+
+
 def fill_random_weights(spec: NetworkSpec, seed: int) -> None:
     """fill_random_weights, io.cpp:554-566 (in place)."""
     convs = [d for d in spec.layers if d.kind == LayerKind.Conv]
@@ -572,6 +587,26 @@ class CBNetwork:
         """Forward with frames already in device memory (e.g. a torch CUDA tensor's data_ptr())."""
         check(lib.cbg_net_forward(self.handle, C.c_void_p(device_ptr), flags | _lib.FWD_INPUT_ON_DEVICE))
         self._frame_no += 1
+
+    def enqueue_u8(self, frames_hwc: np.ndarray, flags: int = 0):
+        """Asynchronous forward of 8-bit frames in PNM payload order ([S, H, W, C] uint8),
+        converted on the device as load_pnm does (io.cpp:349-399: byte / 255.0f)."""
+        fa = np.ascontiguousarray(frames_hwc, dtype=np.uint8)
+        _, c, h, w = (self.n_streams,) + tuple(self._nodes[0].in_shape)
+        if fa.size != self.n_streams * h * w * c:
+            raise InvalidInputError("forward_u8: frame resolution mismatch")
+        check(lib.cbg_net_forward_u8(self.handle, fa.ctypes.data_as(C.c_void_p), flags))
+        self._frame_no += 1
+
+    def enqueue_device_u8(self, device_ptr: int, flags: int = 0):
+        """8-bit frames ([S, H, W, C] uint8) already in device memory."""
+        check(lib.cbg_net_forward_u8(self.handle, C.c_void_p(device_ptr), flags | _lib.FWD_INPUT_ON_DEVICE))
+        self._frame_no += 1
+
+    def forward_frame_u8(self, frame_hwc, stream: int = 0) -> np.ndarray:
+        """forward_frame on an 8-bit PNM-payload frame per stream ([S, H, W, C] or [H, W, C])."""
+        self.enqueue_u8(frame_hwc)
+        return self.output(stream)
 
     def forward_frame(self, frame, cfg: StatsConfig = None, frame_stats: Optional[FrameStats] = None,
                       stream: int = 0) -> np.ndarray:

@@ -194,6 +194,12 @@ int cbg_net_forward(cbg_net net, const float* frames, unsigned flags) {
     net->net->forward(frames, flags);
   });
 }
+int cbg_net_forward_u8(cbg_net net, const uint8_t* frames_hwc, unsigned flags) {
+  return guard([&] {
+    need(net, "cbg_net_forward_u8");
+    net->net->forward_u8(frames_hwc, flags);
+  });
+}
 int cbg_net_reset(cbg_net net, int stream) {
   return guard([&] {
     need(net, "cbg_net_reset");

@@ -228,6 +228,132 @@ __global__ void __launch_bounds__(kThreads) detect_frame_chw_scalar_kernel(Detec
 }
 
 // ---------------------------------------------------------------------------
+// detect on 8-bit frames in PNM payload order ([H][W][C] interleaved bytes),
+// converted as load_pnm does (io.cpp:389-397): x = float(byte) / 255.0f with
+// IEEE division. One thread = 4 consecutive pixels = C 32-bit words of the
+// frame; the state is CHW planes (state_chw) or NHWC (Cs == 4). C <= 4.
+// ---------------------------------------------------------------------------
+template <bool kChw>
+__global__ void __launch_bounds__(kThreads) detect_frame_u8_kernel(DetectFrameArgs a) {
+  const int s = blockIdx.y;
+  const uint8_t e = epoch8(*a.frame);
+  const bool boot = a.boot[s] != 0;
+  const long long HW = static_cast<long long>(a.H) * a.W;
+  const uint8_t* x8 = *a.x8_slot + static_cast<long long>(s) * a.C * HW;
+  float* st = a.state + static_cast<long long>(s) * (kChw ? a.C : a.Cs) * HW;
+  uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  const bool write_all = boot || !a.closed_loop;
+  const float tau = *a.tau;
+  const long long n4 = HW >> 2;
+  float vmax = 0.0f;
+  for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
+       q += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long p0 = q << 2;
+    // 4 pixels x C bytes = C words, 4-byte aligned (byte offset 4*C*q)
+    uint32_t wd[4];
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(x8 + p0 * a.C);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) wd[i] = i < a.C ? __ldg(src + i) : 0u;
+    float px[4][4];  // [pixel][channel]
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        if (c < a.C) {
+          const int b = j * a.C + c;  // byte index within the 4-pixel group
+          const uint32_t v = (wd[b >> 2] >> (8 * (b & 3))) & 0xffu;
+          px[j][c] = __fdiv_rn(static_cast<float>(v), 255.0f);
+        } else {
+          px[j][c] = 0.0f;
+        }
+      }
+    uint32_t ch = 0;
+    float sv[4][4];
+    if (!boot) {
+      if constexpr (kChw) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < a.C) {
+            const float4 v = *reinterpret_cast<const float4*>(st + c * HW + p0);
+            sv[0][c] = v.x, sv[1][c] = v.y, sv[2][c] = v.z, sv[3][c] = v.w;
+          }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float4 v = *reinterpret_cast<const float4*>(st + (p0 + j) * 4);
+          sv[j][0] = v.x, sv[j][1] = v.y, sv[j][2] = v.z, sv[j][3] = v.w;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+          if (c < a.C && fabsf(px[j][c] - sv[j][c]) > tau) ch |= 1u << j;
+    }
+    if (write_all || ch) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if (write_all || ((ch >> j) & 1u))
+#pragma unroll
+          for (int c = 0; c < 4; ++c) vmax = fmaxf(vmax, px[j][c]);
+      if constexpr (kChw) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < a.C) {
+            float v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = (write_all || ((ch >> j) & 1u)) ? px[j][c] : sv[j][c];
+            *reinterpret_cast<float4*>(st + c * HW + p0) = make_float4(v[0], v[1], v[2], v[3]);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          if (write_all || ((ch >> j) & 1u))
+            *reinterpret_cast<float4*>(st + (p0 + j) * 4) = make_float4(px[j][0], px[j][1], px[j][2], px[j][3]);
+      }
+    }
+    if (ch) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if ((ch >> j) & 1u) m[p0 + j] = e;
+    }
+  }
+  warp_amax(a.amax ? a.amax + s : nullptr, vmax);
+}
+
+// scalar fallback for 8-bit frames (HW % 4 != 0)
+__global__ void __launch_bounds__(kThreads) detect_frame_u8_scalar_kernel(DetectFrameArgs a) {
+  const int s = blockIdx.y;
+  const uint8_t e = epoch8(*a.frame);
+  const bool boot = a.boot[s] != 0;
+  const long long HW = static_cast<long long>(a.H) * a.W;
+  const uint8_t* x8 = *a.x8_slot + static_cast<long long>(s) * a.C * HW;
+  const bool chw = a.state_chw != 0;
+  float* st = a.state + static_cast<long long>(s) * (chw ? a.C : a.Cs) * HW;
+  uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  const bool write_all = boot || !a.closed_loop;
+  const float tau = *a.tau;
+  float vmax = 0.0f;
+  for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < HW;
+       p += static_cast<long long>(gridDim.x) * blockDim.x) {
+    auto sidx = [&](int c) { return chw ? c * HW + p : p * a.Cs + c; };
+    bool changed = false;
+    if (!boot)
+      for (int c = 0; c < a.C; ++c)
+        changed |= fabsf(__fdiv_rn(static_cast<float>(x8[p * a.C + c]), 255.0f) - st[sidx(c)]) > tau;
+    if (changed || write_all)
+      for (int c = 0; c < a.C; ++c) {
+        const float v = __fdiv_rn(static_cast<float>(x8[p * a.C + c]), 255.0f);
+        st[sidx(c)] = v;
+        vmax = fmaxf(vmax, v);
+      }
+    if (changed) m[p] = e;
+  }
+  warp_amax(a.amax ? a.amax + s : nullptr, vmax);
+}
+
+// ---------------------------------------------------------------------------
 // detect on NHWC inputs. A group of g lanes handles one pixel (g float4 per
 // step); the group's verdict is reduced with a warp ballot.
 // ---------------------------------------------------------------------------
@@ -610,6 +736,17 @@ int group_log2(int Cs) {
 
 void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
   const long long HW = static_cast<long long>(a.H) * a.W;
+  if (a.x8_slot) {
+    if (HW % 4 == 0 && (a.state_chw || a.Cs == 4)) {
+      dim3 grid(blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
+      if (a.state_chw) detect_frame_u8_kernel<true><<<grid, kThreads, 0, st>>>(a);
+      else detect_frame_u8_kernel<false><<<grid, kThreads, 0, st>>>(a);
+    } else {
+      dim3 grid(blocks_for(HW, kThreads, a.S, sm_count()), a.S);
+      detect_frame_u8_scalar_kernel<<<grid, kThreads, 0, st>>>(a);
+    }
+    return;
+  }
   if (a.state_chw) {
     if (a.C <= 4 && HW % 4 == 0) {
       dim3 grid(blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);

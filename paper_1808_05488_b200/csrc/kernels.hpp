@@ -30,6 +30,7 @@ struct DetectFrameArgs {
   int closed_loop;
   int state_chw;       // state is [S][C][H][W] (unpadded planes) instead of NHWC
   float* amax;         // [S] running max |value written to the state| (atomicMax)
+  const uint8_t* const* x8_slot;  // non-null: 8-bit frames [S][H][W][C] (PNM payload order), x = byte/255
 };
 void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st);
 

@@ -281,6 +281,9 @@ void DevBuf::alloc(size_t n) {
   if (n == 0) return;
   CK(cudaMalloc(&p, n));
   CK(cudaMemset(p, 0, n));
+  // the memset runs on the legacy stream, which does not order against the
+  // non-blocking ctx streams: finish it before any ctx-stream write can land
+  CK(cudaStreamSynchronize(nullptr));
 }
 
 Ctx::Ctx(int dev) : device(dev) {
@@ -607,7 +610,7 @@ int Net::launch_count(unsigned flags) const {
   return k;
 }
 
-void Net::enqueue_frame(unsigned flags) {
+void Net::enqueue_frame(unsigned flags, bool u8) {
   cudaStream_t st = ctx_->stream;
   int32_t* counts = counts_.as<int32_t>();
   const uint32_t* frame = frame_ctr_.as<uint32_t>();
@@ -631,7 +634,8 @@ void Net::enqueue_frame(unsigned flags) {
         if (!prod) {
           DetectFrameArgs a{frame_slot_.as<const float*>(), r.state.as<float>(), r.inmap.as<uint8_t>(), frame, boot,
                             d.Ci, r.Csi, d.Hi, d.Wi, S_, taus_.as<float>() + i,
-                            topo_.mode == CBG_MODE_CLOSEDLOOP, r.state_chw, amax_entry(-1)};
+                            topo_.mode == CBG_MODE_CLOSEDLOOP, r.state_chw, amax_entry(-1),
+                            u8 ? frame8_slot_.as<const uint8_t*>() : nullptr};
           timed(d.name + ".detect", [&] { launch_detect_frame(a, st); });
         } else {
           const bool ext = prod->d.kind == kExternal;  // standalone layer: arbitrary x, dense detect
@@ -802,14 +806,47 @@ void Net::forward(const float* frames, unsigned flags) {
     if (!(flags & CBG_FWD_INPUT_ON_DEVICE))
       CK(cudaMemcpyAsync(frame_.p, frames, frame_.bytes, cudaMemcpyHostToDevice, st));
   }
+  run_frame(flags, flags & CBG_FWD_RECORD_WORST_CASE);
+}
+
+void Net::forward_u8(const uint8_t* frames, unsigned flags) {
+  cudaStream_t st = ctx_->stream;
+  CK(cudaSetDevice(ctx_->device));
+  if (!nodes_.empty() && nodes_[0].d.kind == kExternal) throw_invalid("forward_u8: standalone layers take fp32 input");
+  if (frames == nullptr) throw_invalid("forward_u8: null frame");
+  if (topo_.C > 4) throw Error(CBG_ERR_UNSUPPORTED, "8-bit ingest supports at most 4 input channels (PNM: 1 or 3)");
+  bool first_detect = false;
+  for (const NodeRT& r : nodes_)
+    if (r.d.kind == CBG_LAYER_CONV && r.d.inputs[0] < 0 && r.d.policy == CBG_POLICY_DETECT) first_detect = true;
+  if (!first_detect) throw Error(CBG_ERR_UNSUPPORTED, "8-bit ingest needs a detect-policy first layer");
+  if (!frame8_.bytes) {
+    frame8_.alloc(static_cast<size_t>(S_) * topo_.H * topo_.W * topo_.C);
+    frame8_slot_.alloc(sizeof(void*));
+  }
+  const uint8_t* want = (flags & CBG_FWD_INPUT_ON_DEVICE) ? frames : frame8_.as<uint8_t>();
+  if (want != slot8_value_) {
+    const uint8_t* v = want;
+    CK(cudaMemcpyAsync(frame8_slot_.p, &v, sizeof(v), cudaMemcpyHostToDevice, st));
+    slot8_value_ = want;
+  }
+  if (!(flags & CBG_FWD_INPUT_ON_DEVICE))
+    CK(cudaMemcpyAsync(frame8_.p, frames, frame8_.bytes, cudaMemcpyHostToDevice, st));
+  run_frame(flags, (flags & CBG_FWD_RECORD_WORST_CASE) | (1u << 31));
+}
+
+// One frame step: bookkeeping, then the captured graph for this flag set
+// (graph_key bit 31 = 8-bit ingest).
+void Net::run_frame(unsigned flags, unsigned graph_key) {
+  cudaStream_t st = ctx_->stream;
   if (flags & CBG_FWD_FORCE_FULL) CK(cudaMemsetAsync(boot_req_.p, 1, S_, st));
   ++host_frame_;
   if (host_frame_ > 1 && (host_frame_ - 1) % 255 == 0) clear_maps();  // epoch8 wraps
   const unsigned gflags = flags & CBG_FWD_RECORD_WORST_CASE;
+  const bool u8 = (graph_key >> 31) != 0;
   last_flags_ = flags;
   last_launches_ = launch_count(gflags);
   if (timing_) {
-    enqueue_frame(gflags);
+    enqueue_frame(gflags, u8);
     CK(cudaStreamSynchronize(st));
     size_t k = 0;
     for (auto& p : pending_) {
@@ -826,12 +863,12 @@ void Net::forward(const float* frames, unsigned flags) {
     CK(cudaGetLastError());
     return;
   }
-  auto it = graphs_.find(gflags);
+  auto it = graphs_.find(graph_key);
   if (it == graphs_.end()) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     try {
-      enqueue_frame(gflags);
+      enqueue_frame(gflags, u8);
     } catch (...) {
       cudaStreamEndCapture(st, &g);
       throw;
@@ -840,7 +877,7 @@ void Net::forward(const float* frames, unsigned flags) {
     cudaGraphExec_t ge;
     CK(cudaGraphInstantiate(&ge, g, 0));
     cudaGraphDestroy(g);
-    it = graphs_.emplace(gflags, ge).first;
+    it = graphs_.emplace(graph_key, ge).first;
   }
   CK(cudaGraphLaunch(it->second, st));
   CK(cudaGetLastError());

@@ -124,6 +124,7 @@ class Net {
   const std::vector<NodeRT>& nodes() const { return nodes_; }
 
   void forward(const float* frames, unsigned flags);
+  void forward_u8(const uint8_t* frames_hwc, unsigned flags);  // PNM-payload frames (load_pnm semantics)
   // standalone layers: external producer contents (node 0 must be kExternal)
   void set_external(const float* x_chw, const uint8_t* map, const int32_t* rowcol, int64_t n, bool full = false);
   void reset(int stream);
@@ -150,7 +151,7 @@ class Net {
 
  private:
   void build();
-  void enqueue_frame(unsigned flags);  // kernels of one frame (graph body)
+  void enqueue_frame(unsigned flags, bool u8 = false);  // kernels of one frame (graph body)
   int launch_count(unsigned flags) const;
   void clear_maps();
 
@@ -163,6 +164,9 @@ class Net {
   // running max |value| per stream: entry 0 = network input (state of the first
   // layer), entry i+1 = node i's output; the fp16 GEMM scales come from these
   DevBuf amax_;
+  DevBuf frame8_, frame8_slot_;        // 8-bit ingest: staging + device pointer slot
+  const uint8_t* slot8_value_ = nullptr;
+  void run_frame(unsigned flags, unsigned graph_key);
   float* amax_entry(int node) const { return amax_.as<float>() + static_cast<size_t>(node + 1) * S_; }
   int amax_origin(int node) const;  // node whose entry bounds node's output values (pools pass through)
   std::vector<float> ext_amax_;      // host running max of standalone-layer uploads

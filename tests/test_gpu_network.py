@@ -154,3 +154,29 @@ def test_narrow_layers_bit_exact(gpu):
         gm, _ = net.node_changes(2)
         assert np.array_equal(gm, ref.stats(2)["map"]), f"frame {t}: L3 map differs"
         assert np.array_equal(net.node_state(2), ref.state(2, net.nodes()[2].in_shape)), f"frame {t}: L3 state differs"
+
+
+def test_pnm8_ingest_matches_fp32_and_reference(gpu):
+    """8-bit frames in PNM payload order (cbg_net_forward_u8) are converted on
+    the device exactly as load_pnm does (byte / 255.0f): the run is bit-identical
+    to the fp32 API fed with from_pnm8(frames), and matches the reference on them."""
+    S, H, W = 2, 64, 80
+    spec = cbi.make_seg_spec(4, H, W)
+    taus = [0.05] * 5
+    raw = np.stack([seq(H, W, n=5, seed=300 + s, noise=0.01) for s in range(S)], axis=1)
+    pnm = cbi.to_pnm8(raw)                      # [T, S, H, W, C] uint8
+    f32 = cbi.from_pnm8(pnm)                    # [T, S, C, H, W] = byte / 255
+    assert np.array_equal(f32[..., :4, :4], (pnm.astype(np.float32) / np.float32(255)).transpose(0, 1, 4, 2, 3)[..., :4, :4])
+    a = cbi.convert_to_cb(spec, taus, n_streams=S)
+    b = cbi.convert_to_cb(spec, taus, n_streams=S)
+    refs = [oracle.RefNet(spec, taus) for _ in range(S)]
+    for t in range(len(pnm)):
+        a.enqueue_u8(pnm[t])
+        b.enqueue(f32[t])
+        assert np.array_equal(a.counts(), b.counts())
+        for s in range(S):
+            assert np.array_equal(a.output(s), b.output(s))
+            assert np.array_equal(a.node_state(0, s), b.node_state(0, s))
+            want = refs[s].forward(f32[t, s])
+            assert np.array_equal(a.node_output(0, s), refs[s].output(0))  # first layer bit-exact
+            assert oracle.max_rel_err(a.output(s), want) <= TOL_NET
