@@ -50,6 +50,10 @@ namespace cbg {
 #ifdef CBG_TRACE
 __device__ unsigned long long g_trace[6][4096];  // [event][g] clock64 of CTA 0
 __device__ unsigned long long g_cta[4][160];     // per CTA: start, setup done, last MMA issued, epilogue done (ns)
+__device__ unsigned long long g_epi[3][64];      // CTA 0 warp 0 per tile: saw tfull, released TMEM, stores done (clock64)
+__device__ unsigned long long g_chunk[4][64];    // CTA 0 warp 0, chunks of tiles 0-7: start, TMEM landed, staged, stored
+#define CHUNK_MARK(ev, c) do { if (blockIdx.x == 0 && warp == 0 && lane == 0 && (c) < 64) g_chunk[ev][c] = clock64(); } while (0)
+#define EPI_MARK(ev, t) do { if (blockIdx.x == 0 && warp == 0 && lane == 0 && (t) < 64) g_epi[ev][t] = clock64(); } while (0)
 CBG_DEV unsigned long long gtimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -60,6 +64,8 @@ CBG_DEV unsigned long long gtimer() {
 #else
 #define TRACE(ev, g) do { } while (0)
 #define CTA_MARK(ev) do { } while (0)
+#define EPI_MARK(ev, t) do { } while (0)
+#define CHUNK_MARK(ev, c) do { } while (0)
 #endif
 
 namespace {
@@ -125,8 +131,8 @@ CBG_DEV int f16_scale_exp(float bound) {
 }
 CBG_DEV float exp2i(int e) { return __uint_as_float(static_cast<uint32_t>(e + 127) << 23); }
 
-__host__ __device__ constexpr int tail_bytes(int stages, int KB, int S) {
-  return 8 * (3 * stages + 4) + 16 + kBM * 8 + KB * 8 * 8 + (S + 1) * 4;
+__host__ __device__ constexpr int tail_bytes(int stages, int KB, int S, int nbias) {
+  return 8 * (3 * stages + 4) + 16 + kBM * 8 + KB * 8 * 8 + (S + 1) * 4 + 16 + 4 * 32 * 36 * 4 + 4 * nbias;
 }
 
 template <int NPAD, int PREC>
@@ -145,6 +151,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   uint32_t* ktab = reinterpret_cast<uint32_t*>(rowinfo + kBM);
   int* koff = reinterpret_cast<int*>(ktab + a.KB * 8);  // tap offset (dj*Win + di)*Cs + c0 per chunk
   int* tprefix = koff + a.KB * 8;
+  float* epi_buf = reinterpret_cast<float*>(
+      (reinterpret_cast<uintptr_t>(tprefix + a.S + 1) + 15) & ~uintptr_t(15));  // [4 warps][32][CH + 4]
+  float* s_bias = epi_buf + 4 * 32 * 36;                                       // [n_tiles * NPAD]
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -166,6 +175,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     fence_mbar_init();
   }
   if (warp == kMmaWarp) tmem_alloc(tmem_holder, C::kTmemCols);
+  for (int i = tid; i < a.n_tiles * NPAD; i += kThreads) s_bias[i] = a.bias[i];  // zero-padded to n_tiles*NPAD
   for (int i = tid; i < a.KB * 8; i += kThreads) {
     const uint32_t t = a.ktab[i];
     ktab[i] = t;
@@ -390,56 +400,90 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     if (lane == 0) CTA_MARK(2);
   } else if (warp < 4) {
     // ========================= epilogue =========================
+    // Per chunk of CH accumulator columns: tcgen05.ld (lane = row) -> scale,
+    // bias, ReLU -> the warp's smem transpose buffer -> global stores in which
+    // CH/4 consecutive lanes write one pixel's CH contiguous outputs (full
+    // 32-B sectors; lane = row would scatter 32 rows per store instruction).
+    constexpr int CH = NPAD >= 32 ? 32 : 16;
+    constexpr int LPR = CH / 4;     // lanes per pixel row in the store phase
+    constexpr int RPI = 32 / LPR;   // pixel rows per store instruction
+    float* tbuf = epi_buf + warp * 32 * (CH + 4);
     int acc = 0;
     uint32_t acc_phase = 0;
+    int tile_no = 0;
+    (void)tile_no;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int s, mt, nt;
       decode(w, s, mt, nt);
       const int cnt = a.count[s];
       const int k = mt * kBM + warp * 32 + lane;
       const bool valid = k < cnt;
-      const int p = valid ? a.idx[s * HWout + k] : 0;
-      float* orow = a.out + (s * HWout + p) * a.Co4;
+      const int p = valid ? a.idx[s * HWout + k] : -1;
+      float* obase = a.out + s * HWout * a.Co4;
       const int nbase = nt * NPAD;
       float ys = 1.0f;  // undo the fp16 operand scales: 2^(e + ew), two exact steps
       if constexpr (PREC == kPrecF16) ys = exp2i(f16_scale_exp(__ldg(a.amax_in + s)));
       const float ws = PREC == kPrecF16 ? exp2i(a.w_exp) : 1.0f;
       float vmax = 0.0f;  // |written value| bound for the consumers' scales
       mbar_wait(&tfull[acc], acc_phase);
+      EPI_MARK(0, tile_no);
       tc_fence_after();
       const uint32_t tb = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + acc * NPAD;
 #pragma unroll 1
-      for (int n0 = 0; n0 < NPAD; n0 += 16) {
-        uint32_t r[16];
-        tmem_ld16(tb + n0, r);
+      for (int n0 = 0; n0 < NPAD; n0 += CH) {
+        const int cidx = tile_no * (NPAD / CH) + n0 / CH;
+        (void)cidx;
+        CHUNK_MARK(0, cidx);
+        uint32_t r[CH];
+        if constexpr (CH == 32) tmem_ld32(tb + n0, r);
+        else tmem_ld16(tb + n0, r);
         tmem_ld_wait();
-        if (valid) {
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int n = nbase + n0 + 4 * j;
-            if (n < a.Co4) {
-              float o[4];
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                float y = __uint_as_float(r[4 * j + u]);
-                if constexpr (PREC == kPrecF16) y = (y * ys) * ws;
-                y = y + __ldg(a.bias + n + u);
-                if (a.relu) y = (y < 0.0f) ? 0.0f : y;  // std::max(v, 0.f)
-                o[u] = y;
-                vmax = fmaxf(vmax, fabsf(y));
-              }
-              *reinterpret_cast<float4*>(orow + n) = make_float4(o[0], o[1], o[2], o[3]);
-            }
-          }
+        CHUNK_MARK(1, cidx);
+        if (n0 + CH >= NPAD) {  // last TMEM read of the tile: hand the accumulator back
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+          EPI_MARK(1, tile_no);
         }
+        const float4* bias4 = reinterpret_cast<const float4*>(s_bias + nbase + n0);
+#pragma unroll
+        for (int j = 0; j < CH / 4; ++j) {
+          const float4 b = bias4[j];  // broadcast
+          float o[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float y = __uint_as_float(r[4 * j + u]);
+            if constexpr (PREC == kPrecF16) y = (y * ys) * ws;
+            y = y + (&b.x)[u];
+            if (a.relu) y = (y < 0.0f) ? 0.0f : y;  // std::max(v, 0.f)
+            o[u] = y;
+            vmax = fmaxf(vmax, valid ? fabsf(y) : 0.0f);
+          }
+          *reinterpret_cast<float4*>(tbuf + lane * (CH + 4) + 4 * j) = make_float4(o[0], o[1], o[2], o[3]);
+        }
+        __syncwarp();
+        CHUNK_MARK(2, cidx);
+        const int c4 = lane % LPR;
+        const int n = nbase + n0 + 4 * c4;
+        float4 v[32 / RPI];
+        int pr[32 / RPI];
+#pragma unroll
+        for (int i = 0; i < 32 / RPI; ++i) {
+          const int rr = i * RPI + lane / LPR;
+          pr[i] = __shfl_sync(0xffffffffu, p, rr);
+          v[i] = *reinterpret_cast<const float4*>(tbuf + rr * (CH + 4) + 4 * c4);
+        }
+#pragma unroll
+        for (int i = 0; i < 32 / RPI; ++i)
+          if (pr[i] >= 0 && n < a.Co4) *reinterpret_cast<float4*>(obase + static_cast<long long>(pr[i]) * a.Co4 + n) = v[i];
+        __syncwarp();
+        CHUNK_MARK(3, cidx);
       }
-      tc_fence_before();
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) vmax = fmaxf(vmax, __shfl_xor_sync(0xffffffffu, vmax, o));
-      if (lane == 0) {
-        mbar_arrive(&tempty[acc]);
-        if (a.amax_out) atomicMax(reinterpret_cast<int*>(a.amax_out + s), __float_as_int(vmax));
-      }
+      if (lane == 0 && a.amax_out) atomicMax(reinterpret_cast<int*>(a.amax_out + s), __float_as_int(vmax));
+      EPI_MARK(2, tile_no);
+      ++tile_no;
       if (++acc == C::kNAcc) {
         acc = 0;
         acc_phase ^= 1;
@@ -458,7 +502,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
 
 template <int NPAD, int PREC>
 void launch_impl(const ConvGemmArgs& a, cudaStream_t st) {
-  const int smem = conv_gemm_smem_bytes(NPAD, a.KB, a.S, PREC);
+  const int smem = conv_gemm_smem_bytes(NPAD, a.KB, a.S, PREC, a.n_tiles);
   static bool configured = false;
   if (!configured) {
     cudaFuncSetAttribute(conv_gemm_kernel<NPAD, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
@@ -496,6 +540,15 @@ int conv_gemm_read_trace(unsigned long long* host, int n) {
   if (n >= 6 * 4096 + 4 * 160) {
     if (cudaMemcpyFromSymbol(host + 6 * 4096, g_cta, sizeof(unsigned long long) * 4 * 160) != cudaSuccess) return -1;
   }
+  if (n >= 6 * 4096 + 4 * 160 + 3 * 64) {
+    if (cudaMemcpyFromSymbol(host + 6 * 4096 + 4 * 160, g_epi, sizeof(unsigned long long) * 3 * 64) != cudaSuccess)
+      return -1;
+  }
+  if (n >= 6 * 4096 + 4 * 160 + 7 * 64) {
+    if (cudaMemcpyFromSymbol(host + 6 * 4096 + 4 * 160 + 3 * 64, g_chunk, sizeof(unsigned long long) * 4 * 64) !=
+        cudaSuccess)
+      return -1;
+  }
   return cudaMemcpyFromSymbol(host, g_trace, sizeof(unsigned long long) * 6 * 4096) == cudaSuccess ? 6 * 4096 : -1;
 #else
   (void)host;
@@ -508,10 +561,10 @@ int conv_gemm_stages(int npad, int prec) {
   return prec == kPrecF16 ? stages_prec<kPrecF16>(npad) : stages_prec<kPrecTF32>(npad);
 }
 
-int conv_gemm_smem_bytes(int npad, int KB, int S, int prec) {
+int conv_gemm_smem_bytes(int npad, int KB, int S, int prec, int n_tiles) {
   const int stages = conv_gemm_stages(npad, prec);
   const int stage_bytes = kABytes + 2 * npad * (prec == kPrecF16 ? 64 : 128);
-  return 1024 + stages * stage_bytes + tail_bytes(stages, KB, S);
+  return 1024 + stages * stage_bytes + tail_bytes(stages, KB, S, n_tiles * npad);
 }
 
 void launch_conv_gemm(const ConvGemmArgs& a, cudaStream_t st) {

@@ -122,7 +122,7 @@ struct ConvGemmArgs {
   float* amax_out;         // [S] running max |written output| (atomicMax), nullable
 };
 void launch_conv_gemm(const ConvGemmArgs& a, cudaStream_t st);
-int conv_gemm_smem_bytes(int npad, int KB, int S, int prec);
+int conv_gemm_smem_bytes(int npad, int KB, int S, int prec, int n_tiles);
 int conv_gemm_stages(int npad, int prec);
 
 // Bit-exact CUDA-core update for narrow layers (Cout <= 16): the reference's

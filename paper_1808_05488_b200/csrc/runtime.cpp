@@ -522,6 +522,10 @@ void Net::build() {
         if (r.KB > 512) throw Error(CBG_ERR_UNSUPPORTED, "Cin*kh*kw too large for the GEMM kernel (K > 16384)");
         if (r.Csi >= 32768) throw Error(CBG_ERR_UNSUPPORTED, "too many input channels");
         r.prec = gemm_prec();
+        constexpr int kSmemMax = 232448;  // 227 KB opt-in per CTA
+        if (conv_gemm_smem_bytes(r.npad, r.KB, S_, r.prec, r.n_tiles) > kSmemMax) r.prec = 0;  // fewer stages (tf32)
+        if (conv_gemm_smem_bytes(r.npad, r.KB, S_, r.prec, r.n_tiles) > kSmemMax)
+          throw Error(CBG_ERR_UNSUPPORTED, "conv layer too large for the GEMM kernel's shared memory (K or streams)");
         r.w_exp = r.prec == 1 ? weight_exp(c.weights) : 0;
         std::vector<uint8_t> img;
         std::vector<uint32_t> ktab;
