@@ -43,7 +43,7 @@ REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--streams", type=int, default=64, help="camera streams per GPU")
@@ -311,7 +311,9 @@ def main():
             ev.record(e)
             ext.wait_event(ev)
         t1.record(ext)
-        t1.synchronize()
+        # wait with the GIL released (the NVML clock poller runs meanwhile)
+        while not t1.query():
+            time.sleep(0.0002)
         torch.cuda.synchronize()
         return t0.elapsed_time(t1)
 
