@@ -233,6 +233,85 @@ def make_seg_spec(seed: int, height: int, width: int) -> NetworkSpec:
     return spec
 
 
+def make_openpose_spec(seed: int, height: int = 368, width: int = 368, width_div: int = 1,
+                       stages: int = 2) -> NetworkSpec:
+    """OpenPose-style pose net (BASELINE configs[2]) as a reference layer manifest
+    (conv / pool / concat with ``from=`` producers, network.hpp:25-44, io.hpp:14-22):
+    the VGG-19 front end (conv1_1 .. conv4_2) + conv4_3/4_4 "CPM" layers -> features
+    F, stage 1 = two branches (PAF: 38 maps, heatmaps: 19 maps) of 3x3 convs and 1x1
+    heads, stage t >= 2 = concat(PAF_{t-1}, heat_{t-1}, F) -> two branches of 7x7
+    convs. ReLU after every conv except the heads. Channel widths are divided by
+    ``width_div`` (heads keep 38 / 19) so the CPU reference can check it quickly."""
+    def ch(c):
+        return max(4, c // width_div)
+
+    L = []
+    def conv(name, cin, cout, k, relu=True, frm=None):
+        d = _conv(name, cin, cout, k, k // 2, relu)
+        if frm:
+            d.from_ = list(frm)
+        L.append(d)
+        return cout
+
+    c = conv("conv1_1", 3, ch(64), 3)
+    c = conv("conv1_2", c, ch(64), 3)
+    L.append(_pool("pool1"))
+    c = conv("conv2_1", c, ch(128), 3)
+    c = conv("conv2_2", c, ch(128), 3)
+    L.append(_pool("pool2"))
+    c = conv("conv3_1", c, ch(256), 3)
+    for i in (2, 3, 4):
+        c = conv(f"conv3_{i}", c, ch(256), 3)
+    L.append(_pool("pool3"))
+    c = conv("conv4_1", c, ch(512), 3)
+    c = conv("conv4_2", c, ch(512), 3)
+    c = conv("conv4_3_CPM", c, ch(256), 3)
+    feat = conv("conv4_4_CPM", c, ch(128), 3)
+    prev = None
+    for t in range(1, stages + 1):
+        heads = []
+        for br, n_out in ((1, 38), (2, 19)):
+            src = ["conv4_4_CPM"] if t == 1 else [f"concat_stage{t}"]
+            if t > 1 and br == 1:
+                L.append(LayerDesc(LayerKind.Concat, f"concat_stage{t}", list(prev) + ["conv4_4_CPM"]))
+            cin = feat if t == 1 else 38 + 19 + feat
+            k, n_mid = (3, 3) if t == 1 else (7, 5)
+            x = conv(f"Mconv1_stage{t}_L{br}", cin, ch(128), k, frm=src)
+            for i in range(2, n_mid + 1):
+                x = conv(f"Mconv{i}_stage{t}_L{br}", x, ch(128), k)
+            x = conv(f"Mconv{n_mid + 1}_stage{t}_L{br}", x, ch(512) if t == 1 else ch(128), 1)
+            conv(f"Mconv{n_mid + 2}_stage{t}_L{br}", x, n_out, 1, relu=False)
+            heads.append(f"Mconv{n_mid + 2}_stage{t}_L{br}")
+        prev = heads
+    spec = NetworkSpec(3, height, width, L)
+    fill_random_weights(spec, seed)
+    return spec
+
+
+def make_yolo_spec(seed: int, height: int = 1080, width: int = 1920, width_div: int = 1) -> NetworkSpec:
+    """YOLO-style detector (BASELINE configs[3]): the tiny-YOLOv2 layer stack
+    (3x3 convs 16..1024 with 2x2 / stride-2 max-pools, then a 1x1 head of 5
+    anchors x (5 + 20 classes) = 125 maps). The reference has ReLU only
+    (network.hpp:10), so ReLU stands in for the leaky ReLU; widths are divided by
+    ``width_div`` (head kept) for the CPU-checked tests."""
+    def ch(c):
+        return max(4, c // width_div)
+
+    L = []
+    c = 3
+    for i, cout in enumerate((16, 32, 64, 128, 256)):
+        L.append(_conv(f"conv{i + 1}", c, ch(cout), 3, 1, True))
+        L.append(_pool(f"pool{i + 1}"))
+        c = ch(cout)
+    L.append(_conv("conv6", c, ch(512), 3, 1, True))
+    L.append(_conv("conv7", ch(512), ch(1024), 3, 1, True))
+    L.append(_conv("conv8", ch(1024), ch(1024), 3, 1, True))
+    L.append(_conv("head", ch(1024), 125, 1, 0, False))
+    spec = NetworkSpec(3, height, width, L)
+    fill_random_weights(spec, seed)
+    return spec
+
+
 def make_small_spec(seed: int, in_channels: int, height: int, width: int) -> NetworkSpec:
     """make_small_spec, io.cpp:619-654."""
     spec = NetworkSpec(in_channels, height, width, [

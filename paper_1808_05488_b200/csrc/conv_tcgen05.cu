@@ -132,7 +132,7 @@ CBG_DEV int f16_scale_exp(float bound) {
 CBG_DEV float exp2i(int e) { return __uint_as_float(static_cast<uint32_t>(e + 127) << 23); }
 
 __host__ __device__ constexpr int tail_bytes(int stages, int KB, int S, int nbias) {
-  return 8 * (3 * stages + 4) + 16 + kBM * 8 + KB * 8 * 8 + (S + 1) * 4 + 16 + 4 * 32 * 36 * 4 + 4 * nbias;
+  return 8 * (3 * stages + 4) + 16 + kBM * 8 + (S + 1) * 4 + 16 + 4 * 32 * 36 * 4 + 4 * nbias + 0 * KB;
 }
 
 template <int NPAD, int PREC>
@@ -148,9 +148,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   uint64_t* tempty = tfull + 2;
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(tempty + 2);
   int2* rowinfo = reinterpret_cast<int2*>(tmem_holder + 4);
-  uint32_t* ktab = reinterpret_cast<uint32_t*>(rowinfo + kBM);
-  int* koff = reinterpret_cast<int*>(ktab + a.KB * 8);  // tap offset (dj*Win + di)*Cs + c0 per chunk
-  int* tprefix = koff + a.KB * 8;
+  int* tprefix = reinterpret_cast<int*>(rowinfo + kBM);
   float* epi_buf = reinterpret_cast<float*>(
       (reinterpret_cast<uintptr_t>(tprefix + a.S + 1) + 15) & ~uintptr_t(15));  // [4 warps][32][CH + 4]
   float* s_bias = epi_buf + 4 * 32 * 36;                                       // [n_tiles * NPAD]
@@ -176,12 +174,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   }
   if (warp == kMmaWarp) tmem_alloc(tmem_holder, C::kTmemCols);
   for (int i = tid; i < a.n_tiles * NPAD; i += kThreads) s_bias[i] = a.bias[i];  // zero-padded to n_tiles*NPAD
-  for (int i = tid; i < a.KB * 8; i += kThreads) {
-    const uint32_t t = a.ktab[i];
-    ktab[i] = t;
-    koff[i] = (static_cast<int>(t & 0xFF) * a.Win + static_cast<int>((t >> 8) & 0xFF)) * a.Cs +
-              static_cast<int>((t >> 16) & 0x7FFF);
-  }
   if (warp == 0) {
     int carry = 0;
     if (lane == 0) tprefix[0] = 0;
@@ -223,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     const int fgrp = (tid - 128) / kFetchG;  // K-blocks g with g % kGroups == fgrp
     const int ftid = (tid - 128) % kFetchG;
     const int q = ftid & 7;
-    const uint32_t ktab_s = smem_u32(ktab), koff_s = smem_u32(koff);
+    const uint2* ktab = reinterpret_cast<const uint2*>(a.ktab);  // (tap code, element offset) per 16-B chunk
     uint32_t g = 0;  // global K-block counter (stage = g % kStages)
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int s, mt, nt;
@@ -247,8 +239,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         if (static_cast<int>(g % kGroups) != fgrp) continue;
         const int stage = g % C::kStages;
         const uint32_t phase = (g / C::kStages) & 1;
-        const uint32_t tab = lds_u32(ktab_s + (kb * 8 + q) * 4);
-        const int toff = static_cast<int>(lds_u32(koff_s + (kb * 8 + q) * 4));
+        const uint2 tk = __ldg(ktab + kb * 8 + q);
+        const uint32_t tab = tk.x;
+        const int toff = static_cast<int>(tk.y);
         const int dj = tab & 0xFF, di = (tab >> 8) & 0xFF;
         const bool tap_ok = (tab >> 31) == 0;
         mbar_wait(&empty[stage], phase ^ 1);

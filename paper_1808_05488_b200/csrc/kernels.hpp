@@ -106,7 +106,7 @@ struct ConvGemmArgs {
   const int32_t* idx;      // [S][Hout*Wout]
   const int32_t* count;    // [S]
   const uint8_t* wimg;     // pre-swizzled tf32 hi/lo weight images [n_tiles][KB][2][NPAD][128B]
-  const uint32_t* ktab;    // [KB*8] (kj | ki<<8 | c0<<16 | invalid<<31) per 16-B chunk
+  const uint32_t* ktab;    // [KB*8][2] per 16-B chunk: (kj | ki<<8 | c0<<16 | invalid<<31, (kj*Win + ki)*Cs + c0)
   const float* bias;       // [n_tiles*NPAD]
   int Cs, Hin, Win, Hout, Wout, Co4;
   int stride, pad;

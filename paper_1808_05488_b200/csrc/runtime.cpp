@@ -2,6 +2,7 @@
 #include "runtime.hpp"
 
 #include <algorithm>
+#include <climits>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -399,16 +400,19 @@ void build_weight_image(const NodeRT& n, std::vector<uint8_t>& img, std::vector<
         }
       }
     }
-  ktab.assign(static_cast<size_t>(n.KB) * 8, 0);
+  ktab.assign(static_cast<size_t>(n.KB) * 8 * 2, 0);
   for (int kb = 0; kb < n.KB; ++kb)
     for (int q = 0; q < 8; ++q) {
       const int k0 = kb * 32 + q * 4;
       const int t = k0 / n.Csi, c0 = k0 % n.Csi;
       if (t >= taps) {
-        ktab[kb * 8 + q] = 0x80000000u;
+        ktab[(kb * 8 + q) * 2] = 0x80000000u;
       } else {
         const int kj = t / c.kernel_w, ki = t % c.kernel_w;
-        ktab[kb * 8 + q] = static_cast<uint32_t>(kj) | (static_cast<uint32_t>(ki) << 8) |
+        const long long off = (static_cast<long long>(kj) * n.d.Wi + ki) * n.Csi + c0;
+        if (off > INT32_MAX) throw Error(CBG_ERR_UNSUPPORTED, "input row too large for 32-bit tap offsets");
+        ktab[(kb * 8 + q) * 2 + 1] = static_cast<uint32_t>(off);
+        ktab[(kb * 8 + q) * 2] = static_cast<uint32_t>(kj) | (static_cast<uint32_t>(ki) << 8) |
                            (static_cast<uint32_t>(c0) << 16);
       }
     }

@@ -158,3 +158,53 @@ def test_pinned_seg7_full_resolution_against_reference(gpu):
         assert np.array_equal(gm, ref.stats(0)["map"])
         for i in range(len(net.nodes())):
             assert len(net.node_changes(i)[1]) == ref.stats(i)["changed_px"]
+
+
+def test_openpose_style_graph_cfg3(gpu):
+    """BASELINE configs[2]: OpenPose-style graph (VGG front end, two-branch
+    stages re-joined by Concat) at 368x368 on a moving-subject sequence, as a
+    reference manifest with from= producers. Width-reduced (channels / 8, the
+    38 / 19 heads kept) so the CPU reference checks it in seconds."""
+    H = W = 368
+    spec = cbi.make_openpose_spec(5, H, W, width_div=8, stages=2)
+    n_conv = sum(1 for d in spec.layers if d.kind == cbi.LayerKind.Conv)
+    taus = [0.02] * n_conv
+    net = cbi.convert_to_cb(spec, taus)
+    ref = oracle.RefNet(spec, taus)
+    frames = cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, 4, 1, 64, 5, 3, 0.0, 31))
+    names = [n.name for n in net.nodes()]
+    for t, f in enumerate(frames):
+        net.forward_frame(f)
+        ref.forward(f)
+        assert np.array_equal(net.node_output(0), ref.output(0)), f"frame {t}: conv1_1 not bit-exact"
+        agree = []
+        for i, nm in enumerate(names):
+            assert oracle.max_rel_err(net.node_output(i), ref.output(i)) <= 1e-4, (t, nm)
+            gm, _ = net.node_changes(i)
+            agree.append(float(np.mean(gm == ref.stats(i)["map"])))
+        assert min(agree) >= 0.999, (t, min(agree))
+    st = ref.stats(names.index("concat_stage2"))
+    assert st["changed_px"] > 0  # the join saw changes
+
+
+def test_yolo_style_detector_cfg4(gpu):
+    """BASELINE configs[3]: tiny-YOLO-style detector (3x3 conv + pool stack, 1x1
+    head of 125 maps) on a static-camera surveillance sequence with a few moving
+    objects and sensor noise; width- and resolution-reduced (270x480, channels /
+    8) for the CPU reference."""
+    H, W = 270, 480
+    spec = cbi.make_yolo_spec(9, H, W, width_div=8)
+    n_conv = sum(1 for d in spec.layers if d.kind == cbi.LayerKind.Conv)
+    taus = [0.03] * n_conv
+    net = cbi.convert_to_cb(spec, taus)
+    ref = oracle.RefNet(spec, taus)
+    frames = cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, 4, 3, 24, 4, 6, 0.002, 77))
+    for t, f in enumerate(frames):
+        got = net.forward_frame(f)
+        want = ref.forward(f)
+        assert np.array_equal(net.node_output(0), ref.output(0)), f"frame {t}: conv1 not bit-exact"
+        gm, gi = net.node_changes(0)
+        assert np.array_equal(gm, ref.stats(0)["map"])
+        assert oracle.max_rel_err(got, want) <= 1e-4, t
+        for i in range(len(net.nodes())):
+            assert float(np.mean(net.node_changes(i)[0] == ref.stats(i)["map"])) >= 0.999, (t, i)
