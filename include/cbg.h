@@ -59,7 +59,8 @@ enum { CBG_MODE_FEEDFORWARD = 0, CBG_MODE_CLOSEDLOOP = 1 };
 enum {
   CBG_FWD_FORCE_FULL = 1u << 0,        /* force_full_update: bootstrap-style full recompute */
   CBG_FWD_RECORD_WORST_CASE = 1u << 1, /* record_worst_case: also compute propagate_changes(up) */
-  CBG_FWD_INPUT_ON_DEVICE = 1u << 2    /* the frame pointer is a device pointer */
+  CBG_FWD_INPUT_ON_DEVICE = 1u << 2,   /* the frame pointer is a device pointer */
+  CBG_FWD_BROADCAST_INPUT = 1u << 3    /* one frame [C][H][W] is fed to every stream (fp32 API) */
 };
 
 /* ---- descriptions --------------------------------------------------------- */
@@ -179,6 +180,9 @@ int cbg_net_reset(cbg_net net, int stream);
 /* set_thresholds() / thresholds() (network.cpp:256-272). */
 int cbg_net_set_thresholds(cbg_net net, const float* taus, int n_taus);
 int cbg_net_thresholds(cbg_net net, float* taus, int n_taus);
+/* Thresholds of one stream only (the others keep theirs): a stream set can
+ * evaluate several threshold vectors at once (GPU calibration, below). */
+int cbg_net_set_stream_thresholds(cbg_net net, int stream, const float* taus, int n_taus);
 /* Dense path: every frame is a full update through the same kernels and
  * GEMM precision (the implementation's own dense-conv baseline). */
 int cbg_net_set_dense(cbg_net net, int dense);
@@ -230,6 +234,66 @@ int cbg_pool_forward(cbg_pool layer, const float* x, const uint8_t* up_map,
 int cbg_pool_read_output(cbg_pool layer, float* out_chw);
 int cbg_pool_read_changes(cbg_pool layer, uint8_t* map_out, int32_t* rowcol_out,
                           int64_t* count_out);
+
+/* ---- threshold calibration on the GPU (calibration.hpp:16-84) -------------- */
+/* An evaluation sequence (EvalSequence, calibration.hpp:19-22): host frames
+ * [n_frames][C][H][W] (network input) and one reference output per frame,
+ * [n_frames][ref_channels][Ho][Wo] (ref_channels = the net's output channels,
+ * or 1 = class labels for the pixel-accuracy metric). */
+typedef struct cbg_eval_sequence {
+  int n_frames;
+  const float* frames;
+  const float* references;
+  int ref_channels;
+} cbg_eval_sequence;
+
+enum { CBG_LOSS_MSE = 0, CBG_LOSS_PIXEL_ACCURACY_DELTA = 1 };  /* LossMetric, network.hpp:183 */
+enum { CBG_AGG_MEAN = 0, CBG_AGG_WORST = 1 };                   /* LossAggregation, calibration.hpp:26 */
+
+/* CalibConfig, calibration.hpp:28-36 (budget_overrides nullable). */
+typedef struct cbg_calib_config {
+  double initial_tau;
+  double growth_factor;
+  double per_layer_budget;
+  const double* budget_overrides;
+  int n_budget_overrides;
+  int metric;
+  int aggregation;
+  int max_steps;
+} cbg_calib_config;
+
+typedef struct cbg_calib_trace_point {  /* CalibTracePoint, calibration.hpp:38-42 */
+  int layer;
+  double tau;
+  double loss;
+} cbg_calib_trace_point;
+
+/* select_thresholds (calibration.cpp:95-141) with the replays on the GPU: for
+ * each conv layer, the base vector and all max_steps geometric candidates are
+ * replayed at once as the streams of one stream set per sequence, and the
+ * reference's sequential rule (keep the last candidate before the first budget
+ * violation) is applied to the losses. `proto` supplies topology, policies and
+ * mode (its thresholds and state are not used). taus_out / hit_cap_out: one per
+ * conv layer; trace_out (nullable) gets the reference's trace, trace_len its
+ * length (capped at trace_cap). */
+int cbg_select_thresholds(cbg_net proto, const cbg_eval_sequence* seqs, int n_seqs, const cbg_calib_config* cfg,
+                          float* taus_out, uint8_t* hit_cap_out, cbg_calib_trace_point* trace_out, int trace_cap,
+                          int* trace_len);
+
+typedef struct cbg_tradeoff_row {  /* TradeoffRow, calibration.hpp:56-61 */
+  double factor;
+  double loss;
+  int64_t total_eff_ops;
+  int64_t wall_ns;
+} cbg_tradeoff_row;
+
+/* sweep_threshold_factor (calibration.cpp:143-180): every factor's scaled
+ * vector replayed from reset as one stream per factor; loss = mean per-frame
+ * loss and ops = conv-op total over post-bootstrap frames. wall_ns = device
+ * time of the replay shared by all factors of a sequence, split evenly. */
+int cbg_sweep_threshold_factor(cbg_net proto, const float* base_tau, int n_tau, const double* factors,
+                               int n_factors, const cbg_eval_sequence* seqs, int n_seqs, int metric,
+                               cbg_tradeoff_row* rows_out);
 
 /* ---- instrumentation / async I/O (bench, profiling) ----------------------- */
 /* Kernel launches enqueued per cbg_net_forward (one frame of every stream). */

@@ -17,6 +17,7 @@
 //    CUDA-event timing of the bench instead).
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <memory>
 #include <stdexcept>
@@ -418,6 +419,12 @@ class CBNetwork {
     return {m, detail::to_indexes(rc, n)};
   }
 
+  // One stream's thresholds (the others keep theirs).
+  void set_stream_thresholds(int stream, const std::vector<float>& taus) {
+    check(cbg_net_set_stream_thresholds(h_.get(), stream, taus.data(), static_cast<int>(taus.size())));
+  }
+  cbg_net handle() const { return h_.get(); }
+
   CBNetwork clone() const {
     CBNetwork c;
     cbg_net h = nullptr;
@@ -482,6 +489,100 @@ inline CBNetwork convert_to_cb(const DenseNetwork& net, const std::vector<float>
   cb.info_.resize(static_cast<size_t>(n));
   for (int i = 0; i < n; ++i) check(cbg_net_node_info(h, i, &cb.info_[i]));
   return cb;
+}
+
+// ---- calibration (calibration.hpp:16-84), replays on the GPU --------------------
+enum class LossMetric { Mse, PixelAccuracyDelta };
+enum class LossAggregation { Mean, Worst };
+
+struct EvalSequence {
+  std::vector<Tensor3> frames;
+  std::vector<Tensor3> reference;
+};
+
+struct CalibConfig {
+  double initial_tau = 0.01;
+  double growth_factor = 1.1;
+  double per_layer_budget = 0.0;
+  std::vector<double> budget_overrides;
+  LossMetric metric = LossMetric::Mse;
+  LossAggregation aggregation = LossAggregation::Mean;
+  int max_steps = 64;
+};
+
+struct CalibTracePoint {
+  int layer = 0;
+  double tau = 0.0;
+  double loss = 0.0;
+};
+
+struct CalibResult {
+  std::vector<float> taus;
+  std::vector<bool> hit_cap;
+  std::vector<CalibTracePoint> trace;
+};
+
+struct TradeoffRow {
+  double factor = 0.0;
+  double loss = 0.0;
+  std::int64_t total_eff_ops = 0;
+  std::int64_t wall_ns = 0;
+};
+
+namespace detail {
+// Flattened host copies of the sequences for the C ABI.
+struct CSequences {
+  std::vector<std::vector<float>> f, r;
+  std::vector<cbg_eval_sequence> v;
+  explicit CSequences(const std::vector<EvalSequence>& seqs) {
+    for (const EvalSequence& q : seqs) {
+      if (q.frames.empty() || q.reference.size() != q.frames.size())
+        throw InvalidInputError("calibration sequence needs frames and per-frame references");
+      f.emplace_back();
+      r.emplace_back();
+      for (const Tensor3& t : q.frames) f.back().insert(f.back().end(), t.data.begin(), t.data.end());
+      for (const Tensor3& t : q.reference) r.back().insert(r.back().end(), t.data.begin(), t.data.end());
+      v.push_back({static_cast<int>(q.frames.size()), f.back().data(), r.back().data(), q.reference[0].channels});
+    }
+  }
+};
+}  // namespace detail
+
+// select_thresholds, calibration.cpp:95-141
+inline CalibResult select_thresholds(const CBNetwork& net, const std::vector<EvalSequence>& sequences,
+                                     const CalibConfig& cfg) {
+  detail::CSequences cs(sequences);
+  cbg_calib_config c{cfg.initial_tau, cfg.growth_factor, cfg.per_layer_budget,
+                     cfg.budget_overrides.empty() ? nullptr : cfg.budget_overrides.data(),
+                     static_cast<int>(cfg.budget_overrides.size()), static_cast<int>(cfg.metric),
+                     static_cast<int>(cfg.aggregation), cfg.max_steps};
+  const int n_conv = net.conv_layer_count();
+  std::vector<float> taus(static_cast<size_t>(n_conv));
+  std::vector<uint8_t> cap(static_cast<size_t>(n_conv));
+  std::vector<cbg_calib_trace_point> tr(static_cast<size_t>(std::max(1, n_conv * std::max(1, cfg.max_steps))));
+  int n = 0;
+  check(cbg_select_thresholds(net.handle(), cs.v.data(), static_cast<int>(cs.v.size()), &c, taus.data(), cap.data(),
+                              tr.data(), static_cast<int>(tr.size()), &n));
+  CalibResult res;
+  res.taus = taus;
+  for (uint8_t b : cap) res.hit_cap.push_back(b != 0);
+  for (int i = 0; i < n && i < static_cast<int>(tr.size()); ++i) res.trace.push_back({tr[i].layer, tr[i].tau, tr[i].loss});
+  return res;
+}
+
+// sweep_threshold_factor, calibration.cpp:143-180
+inline std::vector<TradeoffRow> sweep_threshold_factor(const CBNetwork& net, const std::vector<float>& base_tau,
+                                                       const std::vector<double>& factors,
+                                                       const std::vector<EvalSequence>& sequences,
+                                                       LossMetric metric = LossMetric::Mse) {
+  detail::CSequences cs(sequences);
+  std::vector<cbg_tradeoff_row> rows(factors.size());
+  check(cbg_sweep_threshold_factor(net.handle(), base_tau.data(), static_cast<int>(base_tau.size()), factors.data(),
+                                   static_cast<int>(factors.size()), cs.v.data(), static_cast<int>(cs.v.size()),
+                                   static_cast<int>(metric), rows.data()));
+  std::vector<TradeoffRow> out;
+  for (const cbg_tradeoff_row& r : rows) out.push_back({r.factor, r.loss, r.total_eff_ops, r.wall_ns});
+  return out;
 }
 
 }  // namespace cbg

@@ -14,6 +14,8 @@
 #include <vector>
 
 #include "cbg.h"
+#include <algorithm>
+
 #include "cbi/calibration.hpp"
 #include "cbi/change.hpp"
 #include "cbi/dense.hpp"
@@ -456,6 +458,60 @@ int ref_dense_forward_row(void* h, const float* frame, int row, float* y) {
     std::vector<Tensor3> all =
         r->dense->forward_all(to_tensor(frame, s.in_channels, s.in_height, s.in_width));
     put_tensor(all[row < 0 ? all.size() - 1 : row], y);
+  });
+}
+
+// ---- calibration (calibration.cpp:95-180) ---------------------------------------
+namespace {
+std::vector<EvalSequence> to_sequences(const RefNet& r, const cbg_eval_sequence* seqs, int n_seqs) {
+  const Shape3 in = r.cb.input_shape();
+  const auto& nodes = r.cb.nodes();
+  const Shape3 out = nodes.back().out_shape;
+  std::vector<EvalSequence> v(n_seqs);
+  for (int q = 0; q < n_seqs; ++q) {
+    const size_t fe = static_cast<size_t>(in.channels) * in.height * in.width;
+    const size_t re = static_cast<size_t>(seqs[q].ref_channels) * out.height * out.width;
+    for (int t = 0; t < seqs[q].n_frames; ++t) {
+      v[q].frames.push_back(to_tensor(seqs[q].frames + t * fe, in.channels, in.height, in.width));
+      v[q].reference.push_back(to_tensor(seqs[q].references + t * re, seqs[q].ref_channels, out.height, out.width));
+    }
+  }
+  return v;
+}
+}  // namespace
+
+int ref_select_thresholds(void* h, const cbg_eval_sequence* seqs, int n_seqs, const cbg_calib_config* c,
+                          float* taus_out, uint8_t* cap_out, cbg_calib_trace_point* trace_out, int trace_cap,
+                          int* trace_len) {
+  auto* r = static_cast<RefNet*>(h);
+  return guard([&] {
+    CalibConfig cfg;
+    cfg.initial_tau = c->initial_tau;
+    cfg.growth_factor = c->growth_factor;
+    cfg.per_layer_budget = c->per_layer_budget;
+    if (c->budget_overrides)
+      cfg.budget_overrides.assign(c->budget_overrides, c->budget_overrides + c->n_budget_overrides);
+    cfg.metric = static_cast<LossMetric>(c->metric);
+    cfg.aggregation = static_cast<LossAggregation>(c->aggregation);
+    cfg.max_steps = c->max_steps;
+    CalibResult res = select_thresholds(r->cb, to_sequences(*r, seqs, n_seqs), cfg);
+    std::copy(res.taus.begin(), res.taus.end(), taus_out);
+    for (size_t i = 0; i < res.hit_cap.size(); ++i) cap_out[i] = res.hit_cap[i] ? 1 : 0;
+    const int n = std::min<int>(static_cast<int>(res.trace.size()), trace_cap);
+    for (int i = 0; i < n; ++i) trace_out[i] = {res.trace[i].layer, res.trace[i].tau, res.trace[i].loss};
+    *trace_len = static_cast<int>(res.trace.size());
+  });
+}
+
+int ref_sweep_threshold_factor(void* h, const float* base_tau, int n_tau, const double* factors, int n_factors,
+                               const cbg_eval_sequence* seqs, int n_seqs, int metric, cbg_tradeoff_row* rows) {
+  auto* r = static_cast<RefNet*>(h);
+  return guard([&] {
+    auto curve = sweep_threshold_factor(r->cb, std::vector<float>(base_tau, base_tau + n_tau),
+                                        std::vector<double>(factors, factors + n_factors),
+                                        to_sequences(*r, seqs, n_seqs), static_cast<LossMetric>(metric));
+    for (size_t i = 0; i < curve.size(); ++i)
+      rows[i] = {curve[i].factor, curve[i].loss, curve[i].total_eff_ops, curve[i].wall_ns};
   });
 }
 

@@ -22,6 +22,7 @@ POLICY_DETECT, POLICY_PROPAGATE, POLICY_REUSE1X1 = range(3)
 MODE_FEEDFORWARD, MODE_CLOSEDLOOP = range(2)
 FWD_FORCE_FULL = 1
 FWD_RECORD_WORST_CASE = 2
+FWD_BROADCAST_INPUT = 8
 FWD_INPUT_ON_DEVICE = 4
 
 
@@ -79,6 +80,26 @@ class LayerStatsC(C.Structure):
     ]
 
 
+class EvalSequenceC(C.Structure):
+    _fields_ = [("n_frames", C.c_int), ("frames", C.c_void_p), ("references", C.c_void_p), ("ref_channels", C.c_int)]
+
+
+class CalibConfigC(C.Structure):
+    _fields_ = [
+        ("initial_tau", C.c_double), ("growth_factor", C.c_double), ("per_layer_budget", C.c_double),
+        ("budget_overrides", C.c_void_p), ("n_budget_overrides", C.c_int),
+        ("metric", C.c_int), ("aggregation", C.c_int), ("max_steps", C.c_int),
+    ]
+
+
+class CalibTracePointC(C.Structure):
+    _fields_ = [("layer", C.c_int), ("tau", C.c_double), ("loss", C.c_double)]
+
+
+class TradeoffRowC(C.Structure):
+    _fields_ = [("factor", C.c_double), ("loss", C.c_double), ("total_eff_ops", C.c_int64), ("wall_ns", C.c_int64)]
+
+
 # every symbol include/cbg.h declares: (name, restype, argtypes)
 _vp = C.c_void_p
 _P = C.POINTER
@@ -103,6 +124,11 @@ SIGNATURES = {
     "cbg_net_forward_u8": (C.c_int, [_vp, _vp, C.c_uint]),
     "cbg_net_reset": (C.c_int, [_vp, C.c_int]),
     "cbg_net_set_thresholds": (C.c_int, [_vp, _vp, C.c_int]),
+    "cbg_net_set_stream_thresholds": (C.c_int, [_vp, C.c_int, _vp, C.c_int]),
+    "cbg_select_thresholds": (C.c_int, [_vp, _P(EvalSequenceC), C.c_int, _P(CalibConfigC), _vp, _vp,
+                                        _P(CalibTracePointC), C.c_int, _P(C.c_int)]),
+    "cbg_sweep_threshold_factor": (C.c_int, [_vp, _vp, C.c_int, _vp, C.c_int, _P(EvalSequenceC), C.c_int, C.c_int,
+                                             _P(TradeoffRowC)]),
     "cbg_net_thresholds": (C.c_int, [_vp, _vp, C.c_int]),
     "cbg_net_set_dense": (C.c_int, [_vp, C.c_int]),
     "cbg_net_read_output": (C.c_int, [_vp, C.c_int, C.c_int, _vp]),

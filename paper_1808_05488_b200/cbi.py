@@ -171,6 +171,111 @@ def gen_synthetic(cfg: SyntheticConfig, with_corners: bool = False):
     return (frames, corners) if with_corners else frames
 
 
+# ---------------------------------------------------------------------------
+# threshold calibration on the GPU (calibration.hpp:16-84)
+# ---------------------------------------------------------------------------
+class LossMetric(enum.IntEnum):  # network.hpp:183
+    Mse = 0
+    PixelAccuracyDelta = 1
+
+
+class LossAggregation(enum.IntEnum):  # calibration.hpp:26
+    Mean = 0
+    Worst = 1
+
+
+@dataclass
+class EvalSequence:
+    """EvalSequence, calibration.hpp:19-22: frames [n, C, H, W] and one reference
+    output per frame ([n, Co, Ho, Wo], or [n, 1, Ho, Wo] class labels)."""
+
+    frames: np.ndarray
+    reference: np.ndarray
+
+
+@dataclass
+class CalibConfig:  # calibration.hpp:28-36
+    initial_tau: float = 0.01
+    growth_factor: float = 1.1
+    per_layer_budget: float = 0.0
+    budget_overrides: List[float] = field(default_factory=list)
+    metric: LossMetric = LossMetric.Mse
+    aggregation: LossAggregation = LossAggregation.Mean
+    max_steps: int = 64
+
+
+@dataclass
+class CalibTracePoint:  # calibration.hpp:38-42
+    layer: int
+    tau: float
+    loss: float
+
+
+@dataclass
+class CalibResult:  # calibration.hpp:44-48
+    taus: List[float]
+    hit_cap: List[bool]
+    trace: List[CalibTracePoint]
+
+
+@dataclass
+class TradeoffRow:  # calibration.hpp:56-61
+    factor: float
+    loss: float
+    total_eff_ops: int
+    wall_ns: int
+
+
+def _sequences_c(sequences, keep):
+    arr = (_lib.EvalSequenceC * max(1, len(sequences)))()
+    for i, q in enumerate(sequences):
+        f = np.ascontiguousarray(q.frames, dtype=np.float32)
+        r = np.ascontiguousarray(q.reference, dtype=np.float32)
+        if r.ndim != 4 or f.ndim != 4 or len(r) != len(f):
+            raise InvalidInputError("calibration sequence needs frames and per-frame references")
+        keep += [f, r]
+        arr[i] = _lib.EvalSequenceC(len(f), f.ctypes.data, r.ctypes.data, r.shape[1])
+    keep.append(arr)
+    return arr
+
+
+def select_thresholds(net: "CBNetwork", sequences: Sequence[EvalSequence], cfg: CalibConfig = None) -> CalibResult:
+    """select_thresholds (calibration.cpp:95-141) with every candidate's replay on
+    the GPU (one stream per candidate, cbg_select_thresholds). ``net`` supplies the
+    topology, policies and mode."""
+    cfg = cfg or CalibConfig()
+    keep: list = []
+    seqs = _sequences_c(list(sequences), keep)
+    ov = np.ascontiguousarray(cfg.budget_overrides, dtype=np.float64)
+    c = _lib.CalibConfigC(cfg.initial_tau, cfg.growth_factor, cfg.per_layer_budget,
+                          ov.ctypes.data if len(ov) else None, len(ov), int(cfg.metric), int(cfg.aggregation),
+                          cfg.max_steps)
+    n_conv = net.conv_layer_count()
+    taus = np.zeros(n_conv, np.float32)
+    cap = np.zeros(n_conv, np.uint8)
+    cap_trace = max(1, n_conv * max(1, cfg.max_steps))
+    trace = (_lib.CalibTracePointC * cap_trace)()
+    n = C.c_int(0)
+    check(lib.cbg_select_thresholds(net.handle, seqs, len(sequences), C.byref(c), fptr(taus),
+                                    cap.ctypes.data_as(C.c_void_p), trace, cap_trace, C.byref(n)))
+    return CalibResult([float(t) for t in taus], [bool(x) for x in cap],
+                       [CalibTracePoint(trace[i].layer, trace[i].tau, trace[i].loss) for i in range(min(n.value,
+                                                                                                       cap_trace))])
+
+
+def sweep_threshold_factor(net: "CBNetwork", base_tau: Sequence[float], factors: Sequence[float],
+                           sequences: Sequence[EvalSequence], metric: LossMetric = LossMetric.Mse) -> List[TradeoffRow]:
+    """sweep_threshold_factor (calibration.cpp:143-180), one stream per factor on the GPU."""
+    keep: list = []
+    seqs = _sequences_c(list(sequences), keep)
+    bt = np.ascontiguousarray(base_tau, dtype=np.float32)
+    fa = np.ascontiguousarray(factors, dtype=np.float64)
+    rows = (_lib.TradeoffRowC * max(1, len(fa)))()
+    check(lib.cbg_sweep_threshold_factor(net.handle, fptr(bt), len(bt), fa.ctypes.data_as(C.c_void_p), len(fa), seqs,
+                                         len(sequences), int(metric), rows))
+    return [TradeoffRow(rows[i].factor, rows[i].loss, rows[i].total_eff_ops, rows[i].wall_ns) for i in range(len(fa))]
+
+
 def to_pnm8(frames: np.ndarray) -> np.ndarray:
     """8-bit PNM payload ([..., H, W, C] uint8) of planar fp32 frames ([..., C, H, W]):
     byte = floor(clamp(v, 0, 1) * 255 + 0.5) in fp32 (what a camera / PNM writer
@@ -642,6 +747,11 @@ class CBNetwork:
     def set_thresholds(self, taus: Sequence[float]):
         t = np.ascontiguousarray(taus, dtype=np.float32)
         check(lib.cbg_net_set_thresholds(self.handle, fptr(t), len(t)))
+
+    def set_stream_thresholds(self, stream: int, taus: Sequence[float]):
+        """Thresholds of one stream of the set (the others keep theirs)."""
+        t = np.ascontiguousarray(taus, dtype=np.float32)
+        check(lib.cbg_net_set_stream_thresholds(self.handle, stream, fptr(t), len(t)))
 
     def reset(self, stream: int = -1):
         check(lib.cbg_net_reset(self.handle, stream))

@@ -200,6 +200,49 @@ int cbg_net_forward_u8(cbg_net net, const uint8_t* frames_hwc, unsigned flags) {
     net->net->forward_u8(frames_hwc, flags);
   });
 }
+int cbg_net_set_stream_thresholds(cbg_net net, int stream, const float* taus, int n_taus) {
+  return guard([&] {
+    need(net, "cbg_net_set_stream_thresholds");
+    if (n_taus > 0) need(taus, "cbg_net_set_stream_thresholds");
+    net->net->set_stream_thresholds(stream, std::vector<float>(taus, taus + std::max(0, n_taus)));
+  });
+}
+int cbg_select_thresholds(cbg_net proto, const cbg_eval_sequence* seqs, int n_seqs, const cbg_calib_config* cfg,
+                          float* taus_out, uint8_t* hit_cap_out, cbg_calib_trace_point* trace_out, int trace_cap,
+                          int* trace_len) {
+  return guard([&] {
+    need(proto, "cbg_select_thresholds");
+    need(cfg, "cbg_select_thresholds");
+    need(taus_out, "cbg_select_thresholds");
+    std::vector<float> taus;
+    std::vector<uint8_t> cap;
+    std::vector<cbg_calib_trace_point> trace;
+    cbg::select_thresholds(&proto->ctx->ctx, proto->net->topology(), seqs, n_seqs, *cfg, taus, cap, trace);
+    std::copy(taus.begin(), taus.end(), taus_out);
+    if (hit_cap_out) std::copy(cap.begin(), cap.end(), hit_cap_out);
+    const int n = std::min<int>(static_cast<int>(trace.size()), std::max(0, trace_cap));
+    if (trace_out) std::copy(trace.begin(), trace.begin() + n, trace_out);
+    if (trace_len) *trace_len = static_cast<int>(trace.size());
+  });
+}
+int cbg_sweep_threshold_factor(cbg_net proto, const float* base_tau, int n_tau, const double* factors,
+                               int n_factors, const cbg_eval_sequence* seqs, int n_seqs, int metric,
+                               cbg_tradeoff_row* rows_out) {
+  return guard([&] {
+    need(proto, "cbg_sweep_threshold_factor");
+    if (n_tau > 0) need(base_tau, "cbg_sweep_threshold_factor");
+    if (n_factors > 0) {
+      need(factors, "cbg_sweep_threshold_factor");
+      need(rows_out, "cbg_sweep_threshold_factor");
+    }
+    std::vector<cbg_tradeoff_row> rows;
+    cbg::sweep_threshold_factor(&proto->ctx->ctx, proto->net->topology(),
+                                std::vector<float>(base_tau, base_tau + std::max(0, n_tau)),
+                                std::vector<double>(factors, factors + std::max(0, n_factors)), seqs, n_seqs, metric,
+                                rows);
+    std::copy(rows.begin(), rows.end(), rows_out);
+  });
+}
 int cbg_net_reset(cbg_net net, int stream) {
   return guard([&] {
     need(net, "cbg_net_reset");

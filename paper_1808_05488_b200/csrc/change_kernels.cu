@@ -52,11 +52,11 @@ __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs 
   const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
-  const float* x = *a.x_slot + static_cast<long long>(s) * a.C * HW;
+  const float* x = *a.x_slot + static_cast<long long>(s) * a.x_sstride;
   float* st = a.state + static_cast<long long>(s) * HW * a.Cs;
   uint8_t* m = a.map + static_cast<long long>(s) * HW;
   const bool write_all = boot || !a.closed_loop;
-  const float tau = *a.tau;
+  const float tau = a.tau[s];
   float vmax = 0.0f;
   if constexpr (kVec4) {
     // C <= 4 (Cs == 4), HW % 4 == 0: one thread = 4 consecutive pixels; the C
@@ -144,11 +144,11 @@ __global__ void __launch_bounds__(kThreads) detect_frame_chw_kernel(DetectFrameA
   const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
-  const float* x = *a.x_slot + static_cast<long long>(s) * a.C * HW;
+  const float* x = *a.x_slot + static_cast<long long>(s) * a.x_sstride;
   float* st = a.state + static_cast<long long>(s) * a.C * HW;
   uint8_t* m = a.map + static_cast<long long>(s) * HW;
   const bool write_all = boot || !a.closed_loop;
-  const float tau = *a.tau;
+  const float tau = a.tau[s];
   const long long n4 = HW >> 2;
   float vmax = 0.0f;
   for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
@@ -205,11 +205,11 @@ __global__ void __launch_bounds__(kThreads) detect_frame_chw_scalar_kernel(Detec
   const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
-  const float* x = *a.x_slot + static_cast<long long>(s) * a.C * HW;
+  const float* x = *a.x_slot + static_cast<long long>(s) * a.x_sstride;
   float* st = a.state + static_cast<long long>(s) * a.C * HW;
   uint8_t* m = a.map + static_cast<long long>(s) * HW;
   const bool write_all = boot || !a.closed_loop;
-  const float tau = *a.tau;
+  const float tau = a.tau[s];
   float vmax = 0.0f;
   for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < HW;
        p += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(kThreads) detect_frame_u8_kernel(DetectFrameAr
   float* st = a.state + static_cast<long long>(s) * (kChw ? a.C : a.Cs) * HW;
   uint8_t* m = a.map + static_cast<long long>(s) * HW;
   const bool write_all = boot || !a.closed_loop;
-  const float tau = *a.tau;
+  const float tau = a.tau[s];
   const long long n4 = HW >> 2;
   float vmax = 0.0f;
   for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
@@ -333,7 +333,7 @@ __global__ void __launch_bounds__(kThreads) detect_frame_u8_scalar_kernel(Detect
   float* st = a.state + static_cast<long long>(s) * (chw ? a.C : a.Cs) * HW;
   uint8_t* m = a.map + static_cast<long long>(s) * HW;
   const bool write_all = boot || !a.closed_loop;
-  const float tau = *a.tau;
+  const float tau = a.tau[s];
   float vmax = 0.0f;
   for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < HW;
        p += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -378,7 +378,7 @@ __global__ void __launch_bounds__(kThreads) detect_list_kernel(DetectListArgs a,
   const int nv = a.Cs >> 2;                   // float4 per pixel
   const unsigned gmask = (g == 32 ? 0xffffffffu : ((1u << g) - 1u)) << ((lane >> glog) * g);
   const bool write_all = boot || !a.closed_loop;
-  const float tau = *a.tau;
+  const float tau = a.tau[s];
 
   for (long long base = (static_cast<long long>(blockIdx.x) * wpb + warp) * gpw; base < n;
        base += static_cast<long long>(gridDim.x) * wpb * gpw) {

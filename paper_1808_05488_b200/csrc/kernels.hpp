@@ -26,11 +26,12 @@ struct DetectFrameArgs {
   const uint32_t* frame;     // device frame counter
   const uint8_t* boot;       // [S] full-update flags for this frame
   int C, Cs, H, W, S;
-  const float* tau;    // device scalar (set_thresholds needs no re-capture)
+  const float* tau;    // device [S] per-stream thresholds of this node (set_thresholds needs no re-capture)
   int closed_loop;
   int state_chw;       // state is [S][C][H][W] (unpadded planes) instead of NHWC
   float* amax;         // [S] running max |value written to the state| (atomicMax)
   const uint8_t* const* x8_slot;  // non-null: 8-bit frames [S][H][W][C] (PNM payload order), x = byte/255
+  long long x_sstride;  // fp32 frames: elements between streams' frames (C*H*W, or 0 = one frame for all)
 };
 void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st);
 
@@ -47,7 +48,7 @@ struct DetectListArgs {
   const uint8_t* boot;
   const uint8_t* dense;      // device flag (nullable = 0): rescan every pixel
   int Cs, H, W, S;
-  const float* tau;
+  const float* tau;          // device [S]
   int closed_loop;
 };
 void launch_detect_list(const DetectListArgs& a, cudaStream_t st);

@@ -473,6 +473,7 @@ std::unique_ptr<Net> Net::clone() const {
   CK(cudaMemcpy(c->amax_.p, amax_.p, amax_.bytes, cudaMemcpyDeviceToDevice));
   c->ext_amax_ = ext_amax_;
   c->host_taus_ = host_taus_;
+  c->stream_taus_ = stream_taus_;
   CK(cudaMemcpy(c->taus_.p, taus_.p, taus_.bytes, cudaMemcpyDeviceToDevice));
   CK(cudaMemcpy(c->rescan_req_.p, rescan_req_.p, rescan_req_.bytes, cudaMemcpyDeviceToDevice));
   c->set_dense(dense_);
@@ -581,10 +582,14 @@ void Net::build() {
   dense_flag_.alloc(1);
   rescan_req_.alloc(std::max(1, n));
   rescan_now_.alloc(std::max(1, n));
-  taus_.alloc(std::max(1, n) * sizeof(float));
+  taus_.alloc(static_cast<size_t>(std::max(1, n)) * S_ * sizeof(float));
   host_taus_.assign(n, 0.0f);
-  for (int i = 0; i < n; ++i) host_taus_[i] = nodes_[i].d.tau;
-  CK(cudaMemcpy(taus_.p, host_taus_.data(), n * sizeof(float), cudaMemcpyHostToDevice));
+  stream_taus_.assign(static_cast<size_t>(n) * S_, 0.0f);
+  for (int i = 0; i < n; ++i) {
+    host_taus_[i] = nodes_[i].d.tau;
+    for (int k = 0; k < S_; ++k) stream_taus_[static_cast<size_t>(i) * S_ + k] = nodes_[i].d.tau;
+  }
+  if (n) CK(cudaMemcpy(taus_.p, stream_taus_.data(), stream_taus_.size() * sizeof(float), cudaMemcpyHostToDevice));
   counts_.alloc(static_cast<size_t>(std::max(1, n_slots_)) * S_ * sizeof(int32_t));
   amax_.alloc(static_cast<size_t>(n + 1) * S_ * sizeof(float));
   ext_amax_.assign(S_, 0.0f);
@@ -618,7 +623,7 @@ int Net::launch_count(unsigned flags) const {
   return k;
 }
 
-void Net::enqueue_frame(unsigned flags, bool u8) {
+void Net::enqueue_frame(unsigned flags, bool u8, bool bcast) {
   cudaStream_t st = ctx_->stream;
   int32_t* counts = counts_.as<int32_t>();
   const uint32_t* frame = frame_ctr_.as<uint32_t>();
@@ -641,15 +646,17 @@ void Net::enqueue_frame(unsigned flags, bool u8) {
       if (d.policy == CBG_POLICY_DETECT) {
         if (!prod) {
           DetectFrameArgs a{frame_slot_.as<const float*>(), r.state.as<float>(), r.inmap.as<uint8_t>(), frame, boot,
-                            d.Ci, r.Csi, d.Hi, d.Wi, S_, taus_.as<float>() + i,
+                            d.Ci, r.Csi, d.Hi, d.Wi, S_, taus_.as<float>() + static_cast<size_t>(i) * S_,
                             topo_.mode == CBG_MODE_CLOSEDLOOP, r.state_chw, amax_entry(-1),
-                            u8 ? frame8_slot_.as<const uint8_t*>() : nullptr};
+                            u8 ? frame8_slot_.as<const uint8_t*>() : nullptr,
+                            bcast ? 0LL : static_cast<long long>(d.Ci) * d.Hi * d.Wi};
           timed(d.name + ".detect", [&] { launch_detect_frame(a, st); });
         } else {
           const bool ext = prod->d.kind == kExternal;  // standalone layer: arbitrary x, dense detect
           DetectListArgs a{prod->out.as<float>(), r.state.as<float>(), r.inmap.as<uint8_t>(),
                            ext ? nullptr : prod->idx, counts + prod->count_slot * S_, frame, boot,
-                           rescan_now_.as<uint8_t>() + i, r.Csi, d.Hi, d.Wi, S_, taus_.as<float>() + i,
+                           rescan_now_.as<uint8_t>() + i, r.Csi, d.Hi, d.Wi, S_,
+                           taus_.as<float>() + static_cast<size_t>(i) * S_,
                            topo_.mode == CBG_MODE_CLOSEDLOOP};
           timed(d.name + ".detect", [&] { launch_detect_list(a, st); });
         }
@@ -812,9 +819,10 @@ void Net::forward(const float* frames, unsigned flags) {
       slot_value_ = want;
     }
     if (!(flags & CBG_FWD_INPUT_ON_DEVICE))
-      CK(cudaMemcpyAsync(frame_.p, frames, frame_.bytes, cudaMemcpyHostToDevice, st));
+      CK(cudaMemcpyAsync(frame_.p, frames, (flags & CBG_FWD_BROADCAST_INPUT) ? frame_.bytes / S_ : frame_.bytes,
+                         cudaMemcpyHostToDevice, st));
   }
-  run_frame(flags, flags & CBG_FWD_RECORD_WORST_CASE);
+  run_frame(flags, (flags & CBG_FWD_RECORD_WORST_CASE) | ((flags & CBG_FWD_BROADCAST_INPUT) ? (1u << 30) : 0u));
 }
 
 void Net::forward_u8(const uint8_t* frames, unsigned flags) {
@@ -851,10 +859,11 @@ void Net::run_frame(unsigned flags, unsigned graph_key) {
   if (host_frame_ > 1 && (host_frame_ - 1) % 255 == 0) clear_maps();  // epoch8 wraps
   const unsigned gflags = flags & CBG_FWD_RECORD_WORST_CASE;
   const bool u8 = (graph_key >> 31) != 0;
+  const bool bcast = ((graph_key >> 30) & 1u) != 0;
   last_flags_ = flags;
   last_launches_ = launch_count(gflags);
   if (timing_) {
-    enqueue_frame(gflags, u8);
+    enqueue_frame(gflags, u8, bcast);
     CK(cudaStreamSynchronize(st));
     size_t k = 0;
     for (auto& p : pending_) {
@@ -876,7 +885,7 @@ void Net::run_frame(unsigned flags, unsigned graph_key) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     try {
-      enqueue_frame(gflags, u8);
+      enqueue_frame(gflags, u8, bcast);
     } catch (...) {
       cudaStreamEndCapture(st, &g);
       throw;
@@ -999,6 +1008,17 @@ void Net::reset(int stream) {
   for (int k = s0; k < s1; ++k) ext_amax_[k] = 0.0f;
 }
 
+// Upload the per-stream thresholds and OR `rescan` into the device requests.
+void Net::upload_taus(const std::vector<uint8_t>& rescan) {
+  cudaStream_t st = ctx_->stream;
+  CK(cudaStreamSynchronize(st));
+  CK(cudaMemcpy(taus_.p, stream_taus_.data(), stream_taus_.size() * sizeof(float), cudaMemcpyHostToDevice));
+  std::vector<uint8_t> cur(nodes_.size());
+  CK(cudaMemcpy(cur.data(), rescan_req_.p, nodes_.size(), cudaMemcpyDeviceToHost));
+  for (size_t i = 0; i < cur.size(); ++i) cur[i] |= rescan[i];
+  CK(cudaMemcpy(rescan_req_.p, cur.data(), nodes_.size(), cudaMemcpyHostToDevice));
+}
+
 void Net::set_thresholds(const std::vector<float>& taus) {
   std::vector<int> conv_nodes;
   for (size_t i = 0; i < nodes_.size(); ++i)
@@ -1011,17 +1031,32 @@ void Net::set_thresholds(const std::vector<float>& taus) {
     const int i = conv_nodes[k];
     // Sparse detection is exact only while tau does not decrease:
     // a lowered threshold re-detects every pixel once.
-    if (taus[k] < host_taus_[i]) rescan[i] = 1;
+    for (int s = 0; s < S_; ++s) {
+      float& cur = stream_taus_[static_cast<size_t>(i) * S_ + s];
+      if (taus[k] < cur) rescan[i] = 1;
+      cur = taus[k];
+    }
     host_taus_[i] = taus[k];
     nodes_[i].d.tau = taus[k];
   }
-  cudaStream_t st = ctx_->stream;
-  CK(cudaStreamSynchronize(st));
-  CK(cudaMemcpy(taus_.p, host_taus_.data(), host_taus_.size() * sizeof(float), cudaMemcpyHostToDevice));
-  std::vector<uint8_t> cur(nodes_.size());
-  CK(cudaMemcpy(cur.data(), rescan_req_.p, nodes_.size(), cudaMemcpyDeviceToHost));
-  for (size_t i = 0; i < cur.size(); ++i) cur[i] |= rescan[i];
-  CK(cudaMemcpy(rescan_req_.p, cur.data(), nodes_.size(), cudaMemcpyHostToDevice));
+  upload_taus(rescan);
+}
+
+void Net::set_stream_thresholds(int stream, const std::vector<float>& taus) {
+  if (stream < 0 || stream >= S_) throw_invalid("set_stream_thresholds: stream out of range");
+  std::vector<int> conv_nodes;
+  for (size_t i = 0; i < nodes_.size(); ++i)
+    if (nodes_[i].d.kind == CBG_LAYER_CONV) conv_nodes.push_back(static_cast<int>(i));
+  if (taus.size() != conv_nodes.size()) throw_invalid("set_stream_thresholds: expected one tau per conv layer");
+  for (float t : taus)
+    if (!(t >= 0.0f)) throw_invalid("set_stream_thresholds: tau must be >= 0");
+  std::vector<uint8_t> rescan(nodes_.size(), 0);
+  for (size_t k = 0; k < conv_nodes.size(); ++k) {
+    float& cur = stream_taus_[static_cast<size_t>(conv_nodes[k]) * S_ + stream];
+    if (taus[k] < cur) rescan[conv_nodes[k]] = 1;  // (dense re-detection of the node, all streams: exact)
+    cur = taus[k];
+  }
+  upload_taus(rescan);
 }
 
 std::vector<float> Net::thresholds() const {

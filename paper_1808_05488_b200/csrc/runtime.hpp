@@ -129,6 +129,7 @@ class Net {
   void set_external(const float* x_chw, const uint8_t* map, const int32_t* rowcol, int64_t n, bool full = false);
   void reset(int stream);
   void set_thresholds(const std::vector<float>& taus);
+  void set_stream_thresholds(int stream, const std::vector<float>& taus);  // one stream's thresholds
   std::vector<float> thresholds() const;
   void set_dense(bool dense);
 
@@ -151,7 +152,7 @@ class Net {
 
  private:
   void build();
-  void enqueue_frame(unsigned flags, bool u8 = false);  // kernels of one frame (graph body)
+  void enqueue_frame(unsigned flags, bool u8 = false, bool bcast = false);  // kernels of one frame (graph body)
   int launch_count(unsigned flags) const;
   void clear_maps();
 
@@ -166,6 +167,7 @@ class Net {
   DevBuf amax_;
   DevBuf frame8_, frame8_slot_;        // 8-bit ingest: staging + device pointer slot
   const uint8_t* slot8_value_ = nullptr;
+  void upload_taus(const std::vector<uint8_t>& rescan);
   void run_frame(unsigned flags, unsigned graph_key);
   float* amax_entry(int node) const { return amax_.as<float>() + static_cast<size_t>(node + 1) * S_; }
   int amax_origin(int node) const;  // node whose entry bounds node's output values (pools pass through)
@@ -175,7 +177,8 @@ class Net {
   unsigned last_flags_ = 0;
   int last_launches_ = 0;
   std::map<unsigned, cudaGraphExec_t> graphs_;
-  std::vector<float> host_taus_;
+  std::vector<float> host_taus_;      // network thresholds per node (thresholds())
+  std::vector<float> stream_taus_;    // [node][S] mirror of the device thresholds
   bool dense_ = false;
   // kernel timing (bench instrumentation)
   template <class F> void timed(const std::string& label, F&& launch);
@@ -186,5 +189,14 @@ class Net {
   int timed_frames_ = 0;
   const float* slot_value_ = nullptr;
 };
+
+// Threshold calibration with the replays on the GPU (calib.cpp;
+// reference calibration.cpp:95-180).
+void select_thresholds(Ctx* ctx, const Topology& topo, const cbg_eval_sequence* seqs, int n_seqs,
+                       const cbg_calib_config& cfg, std::vector<float>& taus, std::vector<uint8_t>& hit_cap,
+                       std::vector<cbg_calib_trace_point>& trace);
+void sweep_threshold_factor(Ctx* ctx, const Topology& topo, const std::vector<float>& base_tau,
+                            const std::vector<double>& factors, const cbg_eval_sequence* seqs, int n_seqs, int metric,
+                            std::vector<cbg_tradeoff_row>& rows);
 
 }  // namespace cbg

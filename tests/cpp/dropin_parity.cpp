@@ -5,12 +5,14 @@
 // Exit 0 = parity holds: layer-1 change maps/index lists bit-exact every frame,
 // final map max_rel_err <= 1e-4 (tests/oracles.hpp:59-66 metric), identical
 // changed_px per node, and the reference error categories on bad wiring.
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <vector>
 
 #include "cbg/cbi_gpu.hpp"
 #include "cbi/io.hpp"
+#include "cbi/calibration.hpp"
 #include "cbi/network.hpp"
 
 namespace {
@@ -123,6 +125,53 @@ int main() {
                        taus, &pol);
     ++bad;
   } catch (const cbg::ConfigError&) {
+  }
+  // calibration (calibration.cpp:95-141): the drop-in's GPU select_thresholds
+  // against the reference's on the same sequences and dense references
+  {
+    cbi::DenseNetwork dense = cbi::build_network(rspec);
+    std::vector<cbi::EvalSequence> rseqs(2);
+    std::vector<cbg::EvalSequence> gseqs(2);
+    for (int q = 0; q < 2; ++q) {
+      cbi::SyntheticConfig c2 = sc;
+      c2.n_frames = 4;
+      c2.seed = 300 + q;
+      c2.noise_std = 0.01f;
+      rseqs[q].frames = cbi::gen_synthetic(c2);
+      rseqs[q].reference = cbi::make_reference(dense, rseqs[q].frames);
+      for (size_t t = 0; t < rseqs[q].frames.size(); ++t) {
+        const cbi::Tensor3& f = rseqs[q].frames[t];
+        const cbi::Tensor3& r = rseqs[q].reference[t];
+        cbg::Tensor3 gf(f.channels, f.height, f.width), gr(r.channels, r.height, r.width);
+        gf.data = f.data;
+        gr.data = r.data;
+        gseqs[q].frames.push_back(gf);
+        gseqs[q].reference.push_back(gr);
+      }
+    }
+    cbi::CalibConfig rc;
+    rc.initial_tau = 0.01;
+    rc.growth_factor = 2.0;
+    rc.per_layer_budget = 1e-3;
+    rc.max_steps = 6;
+    cbg::CalibConfig gc;
+    gc.initial_tau = rc.initial_tau;
+    gc.growth_factor = rc.growth_factor;
+    gc.per_layer_budget = rc.per_layer_budget;
+    gc.max_steps = rc.max_steps;
+    const cbi::CalibResult want = cbi::select_thresholds(ref, rseqs, rc);
+    const cbg::CalibResult got = cbg::select_thresholds(gpu, gseqs, gc);
+    if (got.taus != want.taus || got.trace.size() != want.trace.size()) {
+      std::printf("select_thresholds differs\n");
+      ++bad;
+    }
+    for (size_t i = 0; i < std::min(got.trace.size(), want.trace.size()); ++i)
+      if (got.trace[i].tau != want.trace[i].tau ||
+          std::abs(got.trace[i].loss - want.trace[i].loss) > 1e-3 * std::abs(want.trace[i].loss) + 1e-9) {
+        std::printf("trace %zu: tau %g/%g loss %g/%g\n", i, got.trace[i].tau, want.trace[i].tau, got.trace[i].loss,
+                    want.trace[i].loss);
+        ++bad;
+      }
   }
   std::printf("dropin_parity: %s (%d problems)\n", bad ? "FAIL" : "PASS", bad);
   return bad ? 1 : 0;

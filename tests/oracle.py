@@ -59,6 +59,11 @@ def ref():
         lib.ref_net_read_state.argtypes = [_vp, C.c_int, _vp]
         lib.ref_net_read_stats.argtypes = [_vp, C.c_int] + [C.POINTER(C.c_int64)] * 3 + [_vp, _vp]
         lib.ref_dense_forward_row.argtypes = [_vp, _vp, C.c_int, _vp]
+        lib.ref_select_thresholds.argtypes = [_vp, C.POINTER(_lib.EvalSequenceC), C.c_int,
+                                              C.POINTER(_lib.CalibConfigC), _vp, _vp,
+                                              C.POINTER(_lib.CalibTracePointC), C.c_int, C.POINTER(C.c_int)]
+        lib.ref_sweep_threshold_factor.argtypes = [_vp, _vp, C.c_int, _vp, C.c_int, C.POINTER(_lib.EvalSequenceC),
+                                                   C.c_int, C.c_int, C.POINTER(_lib.TradeoffRowC)]
         lib.ref_conv_create.argtypes = [C.POINTER(_lib.ConvSpecC), C.c_float, C.c_int, C.c_int, C.c_int, C.c_int,
                                         C.c_int, C.POINTER(_vp)]
         lib.ref_conv_destroy.argtypes = [_vp]
@@ -198,6 +203,37 @@ class RefNet(_NetBase):
     def set_thresholds(self, taus):
         t = f32(taus)
         _check(self.lib, "ref_", self.lib.ref_net_set_thresholds(self.h, p(t), len(t)))
+
+    def select_thresholds(self, sequences, cfg):
+        """The reference's select_thresholds (calibration.cpp:95-141) on this net."""
+        keep: list = []
+        seqs = cbi._sequences_c(list(sequences), keep)
+        ov = np.ascontiguousarray(cfg.budget_overrides, dtype=np.float64)
+        c = _lib.CalibConfigC(cfg.initial_tau, cfg.growth_factor, cfg.per_layer_budget,
+                              ov.ctypes.data if len(ov) else None, len(ov), int(cfg.metric), int(cfg.aggregation),
+                              cfg.max_steps)
+        n_conv = sum(1 for d in self.spec.layers if d.kind == cbi.LayerKind.Conv)
+        taus = np.zeros(n_conv, np.float32)
+        cap = np.zeros(n_conv, np.uint8)
+        ncap = max(1, n_conv * cfg.max_steps)
+        trace = (_lib.CalibTracePointC * ncap)()
+        n = C.c_int(0)
+        _check(self.lib, "ref_", self.lib.ref_select_thresholds(self.h, seqs, len(sequences), C.byref(c), p(taus),
+                                                                 cap.ctypes.data, trace, ncap, C.byref(n)))
+        return cbi.CalibResult([float(t) for t in taus], [bool(x) for x in cap],
+                               [cbi.CalibTracePoint(trace[i].layer, trace[i].tau, trace[i].loss)
+                                for i in range(min(n.value, ncap))])
+
+    def sweep_threshold_factor(self, base_tau, factors, sequences, metric=cbi.LossMetric.Mse):
+        keep: list = []
+        seqs = cbi._sequences_c(list(sequences), keep)
+        bt = f32(base_tau)
+        fa = np.ascontiguousarray(factors, np.float64)
+        rows = (_lib.TradeoffRowC * max(1, len(fa)))()
+        _check(self.lib, "ref_", self.lib.ref_sweep_threshold_factor(self.h, p(bt), len(bt), fa.ctypes.data, len(fa),
+                                                                      seqs, len(sequences), int(metric), rows))
+        return [cbi.TradeoffRow(rows[i].factor, rows[i].loss, rows[i].total_eff_ops, rows[i].wall_ns)
+                for i in range(len(fa))]
 
     def dense_forward(self, frame, row=-1):
         """DenseNetwork::forward_all(frame)[row] (row indexes the spec, Act rows included)."""
