@@ -19,6 +19,8 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <ostream>
+#include <cstdio>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -493,6 +495,92 @@ inline CBNetwork convert_to_cb(const DenseNetwork& net, const std::vector<float>
 
 // ---- calibration (calibration.hpp:16-84), replays on the GPU --------------------
 enum class LossMetric { Mse, PixelAccuracyDelta };
+
+// ---- sequences and stats CSV (network.hpp:119-126,183-195; io.cpp:660-672) --------
+struct RunStats {
+  std::vector<FrameStats> frames;
+  std::int64_t total_eff_ops(int first_frame = 1) const {
+    std::int64_t n = 0;
+    for (const FrameStats& f : frames)
+      if (f.frame >= first_frame)
+        for (const LayerFrameStats& l : f.layers) n += l.eff_ops;
+    return n;
+  }
+};
+struct SequenceResult {
+  std::vector<Tensor3> outputs;
+  RunStats stats;
+};
+
+namespace detail {
+inline int argmax_channel(const Tensor3& t, int j, int i) {  // calibration.cpp:11-22
+  int best = 0;
+  float best_v = t.at(0, j, i);
+  for (int c = 1; c < t.channels; ++c)
+    if (t.at(c, j, i) > best_v) best_v = t.at(c, j, i), best = c;
+  return best;
+}
+// loss_value, calibration.cpp:26-53
+inline double loss_value(LossMetric metric, const Tensor3& pred, const Tensor3& ref) {
+  if (metric == LossMetric::Mse) {
+    if (pred.channels != ref.channels || pred.height != ref.height || pred.width != ref.width)
+      throw InvalidInputError("mse: shapes differ");
+    double acc = 0.0;
+    for (size_t i = 0; i < pred.data.size(); ++i) {
+      const double d = static_cast<double>(pred.data[i]) - ref.data[i];
+      acc += d * d;
+    }
+    return acc / static_cast<double>(pred.data.size());
+  }
+  if (pred.height != ref.height || pred.width != ref.width) throw InvalidInputError("pixel_accuracy: spatial dims differ");
+  if (ref.channels != 1 && ref.channels != pred.channels)
+    throw InvalidInputError("pixel_accuracy: reference channels must be 1 (labels) or match");
+  std::int64_t hits = 0;
+  for (int j = 0; j < pred.height; ++j)
+    for (int i = 0; i < pred.width; ++i)
+      hits += argmax_channel(pred, j, i) ==
+              (ref.channels == 1 ? static_cast<int>(ref.at(0, j, i)) : argmax_channel(ref, j, i));
+  return 1.0 - static_cast<double>(hits) / (static_cast<std::int64_t>(pred.height) * pred.width);
+}
+}  // namespace detail
+
+// forward_sequence, network.cpp:505-525
+inline SequenceResult forward_sequence(CBNetwork& net, const std::vector<Tensor3>& frames,
+                                       const std::vector<Tensor3>* reference = nullptr,
+                                       LossMetric metric = LossMetric::Mse, const StatsConfig& cfg = {}) {
+  if (reference && reference->size() != frames.size())
+    throw InvalidInputError("forward_sequence: reference count != frame count");
+  SequenceResult result;
+  for (size_t t = 0; t < frames.size(); ++t) {
+    FrameStats fs;
+    const Tensor3& out = net.forward_frame(frames[t], cfg, &fs);
+    fs.frame = static_cast<int>(t) + 1;
+    if (reference) {
+      fs.loss = detail::loss_value(metric, out, (*reference)[t]);
+      fs.has_loss = true;
+    }
+    result.outputs.push_back(out);
+    result.stats.frames.push_back(std::move(fs));
+  }
+  return result;
+}
+
+// write_stats_csv, io.cpp:660-672 (same columns and number formats)
+inline void write_stats_csv(std::ostream& os, const RunStats& run) {
+  os << "frame,layer,changed_px,change_frac,eff_ops,wall_ns,loss\n";
+  char frac[32], loss[48];
+  for (const FrameStats& f : run.frames)
+    for (const LayerFrameStats& l : f.layers) {
+      std::snprintf(frac, sizeof frac, "%.6f", l.change_frac);
+      os << f.frame << "," << l.layer << "," << l.changed_px << "," << frac << "," << l.eff_ops << "," << l.wall_ns
+         << ",";
+      if (f.has_loss) {
+        std::snprintf(loss, sizeof loss, "%.9g", f.loss);
+        os << loss;
+      }
+      os << "\n";
+    }
+}
 enum class LossAggregation { Mean, Worst };
 
 struct EvalSequence {

@@ -15,6 +15,7 @@
 
 #include "cbg.h"
 #include <algorithm>
+#include <sstream>
 
 #include "cbi/calibration.hpp"
 #include "cbi/change.hpp"

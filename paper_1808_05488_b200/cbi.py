@@ -28,7 +28,8 @@ __all__ = [
     "LayerKind", "DetectionPolicy", "DetectMode", "ConvSpec", "LayerDesc", "NetworkSpec",
     "SyntheticConfig", "UpstreamChange", "ConvForwardResult", "PoolForwardResult", "StatsConfig",
     "LayerFrameStats", "FrameStats", "RunStats", "SequenceResult", "Context", "CBConvLayer",
-    "CBPoolLayer", "CBNetwork", "convert_to_cb", "validate_network", "forward_sequence",
+    "CBPoolLayer", "CBNetwork", "convert_to_cb", "validate_network", "forward_sequence", "write_stats_csv",
+    "loss_value", "select_thresholds", "sweep_threshold_factor",
     "gen_synthetic", "fill_random_weights", "make_seg7_spec", "make_seg_spec", "make_small_spec",
     "InvalidInputError", "ConfigError", "device_available",
 ]
@@ -923,8 +924,27 @@ class SequenceResult:
     stats: RunStats = field(default_factory=RunStats)
 
 
-def forward_sequence(net: CBNetwork, frames, reference=None, cfg: StatsConfig = None) -> SequenceResult:
-    """forward_sequence, network.cpp:505-525 (MSE loss when a reference is given)."""
+def loss_value(metric, pred: np.ndarray, ref: np.ndarray) -> float:
+    """loss_value (calibration.cpp:51-53): mse (calibration.cpp:41-49) or
+    1 - pixel_accuracy (argmax over channels, first maximum wins; a 1-channel
+    reference holds class ids, calibration.cpp:26-39)."""
+    pred = np.asarray(pred, np.float32)
+    ref = np.asarray(ref, np.float32)
+    if int(metric) == 0:
+        if pred.shape != ref.shape:
+            raise InvalidInputError("mse: shapes differ")
+        return float(np.mean((pred.astype(np.float64) - ref.astype(np.float64)) ** 2))
+    if pred.shape[1:] != ref.shape[1:]:
+        raise InvalidInputError("pixel_accuracy: spatial dims differ")
+    if ref.shape[0] != 1 and ref.shape[0] != pred.shape[0]:
+        raise InvalidInputError("pixel_accuracy: reference channels must be 1 (labels) or match")
+    a = np.argmax(pred, axis=0)  # numpy argmax returns the first maximum, as argmax_channel
+    r = ref[0].astype(np.int64) if ref.shape[0] == 1 else np.argmax(ref, axis=0)
+    return 1.0 - float(np.mean(a == r))
+
+
+def forward_sequence(net: CBNetwork, frames, reference=None, metric=0, cfg: StatsConfig = None) -> SequenceResult:
+    """forward_sequence, network.cpp:505-525 (per-frame loss under `metric` when a reference is given)."""
     if reference is not None and len(reference) != len(frames):
         raise InvalidInputError("forward_sequence: reference count != frame count")
     res = SequenceResult()
@@ -933,8 +953,19 @@ def forward_sequence(net: CBNetwork, frames, reference=None, cfg: StatsConfig = 
         out = net.forward_frame(f, cfg, fs)
         fs.frame = t + 1
         if reference is not None:
-            fs.loss = float(np.mean((out.astype(np.float64) - np.asarray(reference[t], np.float64)) ** 2))
+            fs.loss = loss_value(metric, out, reference[t])
             fs.has_loss = True
         res.outputs.append(out)
         res.stats.frames.append(fs)
     return res
+
+
+def write_stats_csv(run: RunStats) -> str:
+    """write_stats_csv (io.cpp:660-672): the same columns and number formats
+    (change_frac "%.6f", loss "%.9g")."""
+    out = ["frame,layer,changed_px,change_frac,eff_ops,wall_ns,loss\n"]
+    for f in run.frames:
+        for l in f.layers:
+            out.append(f"{f.frame},{l.layer},{l.changed_px},{l.change_frac:.6f},{l.eff_ops},{l.wall_ns},"
+                       + (f"{f.loss:.9g}" if f.has_loss else "") + "\n")
+    return "".join(out)

@@ -8,6 +8,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <sstream>
 #include <vector>
 
 #include "cbg/cbi_gpu.hpp"
@@ -172,6 +173,27 @@ int main() {
                     want.trace[i].loss);
         ++bad;
       }
+  }
+  // forward_sequence + write_stats_csv (io.cpp:660-672): byte-identical with timing off
+  {
+    cbi::CBNetwork r2 = cbi::convert_to_cb(cbi::build_network(rspec), taus);
+    cbg::CBNetwork g2 = cbg::convert_to_cb(
+        cbg::build_network(seg_spec<cbg::NetworkSpec, cbg::LayerDesc, cbg::LayerKind>(rspec)), taus);
+    cbi::StatsConfig rc;
+    rc.timing = false;
+    std::vector<cbg::Tensor3> gframes;
+    for (const cbi::Tensor3& f : frames) {
+      cbg::Tensor3 x(f.channels, f.height, f.width);
+      x.data = f.data;
+      gframes.push_back(x);
+    }
+    std::ostringstream ro, go;
+    cbi::write_stats_csv(ro, cbi::forward_sequence(r2, frames, nullptr, cbi::LossMetric::Mse, rc).stats);
+    cbg::write_stats_csv(go, cbg::forward_sequence(g2, gframes).stats);
+    if (ro.str() != go.str()) {
+      std::printf("stats CSV differs:\n%s---\n%s", ro.str().c_str(), go.str().c_str());
+      ++bad;
+    }
   }
   std::printf("dropin_parity: %s (%d problems)\n", bad ? "FAIL" : "PASS", bad);
   return bad ? 1 : 0;

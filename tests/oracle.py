@@ -440,6 +440,21 @@ def ref_fill_random_weights(spec: cbi.NetworkSpec, seed: int):
 # ---------------------------------------------------------------------------
 # metrics (reference tests/oracles.hpp:59-66)
 # ---------------------------------------------------------------------------
+REF_STATS_CSV = os.path.join(os.path.dirname(REF_SO), "ref_stats_csv")
+
+
+def ref_seg_stats_csv(seed, height, width, taus, synth: "cbi.SyntheticConfig", with_reference=False) -> str:
+    """The reference's forward_sequence + write_stats_csv (timing off) for the
+    seg net (make_seg7_spec layers at derived dims, fill_random_weights(seed)) on
+    gen_synthetic(synth), run by oracle/_ref/ref_stats_csv."""
+    import subprocess
+    c = synth
+    args = [REF_STATS_CSV, str(seed), str(height), str(width)] + [repr(float(t)) for t in taus] + [
+        str(c.n_frames), str(c.n_objects), str(c.object_size), str(c.velocity_y), str(c.velocity_x),
+        repr(float(c.noise_std)), str(c.seed), "1" if with_reference else "0"]
+    return subprocess.run(args, capture_output=True, text=True, check=True).stdout
+
+
 def max_rel_err(a, b) -> float:
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)

@@ -208,3 +208,30 @@ def test_yolo_style_detector_cfg4(gpu):
         assert oracle.max_rel_err(got, want) <= 1e-4, t
         for i in range(len(net.nodes())):
             assert float(np.mean(net.node_changes(i)[0] == ref.stats(i)["map"])) >= 0.999, (t, i)
+
+
+def test_stats_csv_byte_identical(gpu):
+    """forward_sequence + write_stats_csv (network.cpp:505-525, io.cpp:660-672) from
+    the GPU's device counts is byte-identical to the reference's CSV (timing off,
+    so wall_ns is 0 on both sides); with dense references, the per-frame losses
+    agree to the GEMM's accuracy and every other column is identical."""
+    H, W = 96, 128
+    spec = cbi.make_seg_spec(6, H, W)
+    taus = [0.05] * 5
+    sc = cbi.SyntheticConfig(H, W, 3, 5, 3, 10, 3, 3, 0.003, 91)
+    frames = cbi.gen_synthetic(sc)
+    net = cbi.convert_to_cb(spec, taus)
+    got = cbi.write_stats_csv(cbi.forward_sequence(net, frames).stats)
+    want = oracle.ref_seg_stats_csv(6, H, W, taus, sc)
+    assert got == want
+    assert got.count("\n") == 1 + 5 * 7
+    ref = oracle.RefNet(spec, taus)
+    dense = np.stack([ref.dense_forward(f) for f in frames])
+    net.reset()
+    g = cbi.write_stats_csv(cbi.forward_sequence(net, frames, dense).stats).splitlines()
+    w = oracle.ref_seg_stats_csv(6, H, W, taus, sc, with_reference=True).splitlines()
+    assert len(g) == len(w)
+    for a, b in zip(g[1:], w[1:]):
+        ga, wa = a.split(","), b.split(",")
+        assert ga[:6] == wa[:6]
+        assert float(ga[6]) == pytest.approx(float(wa[6]), rel=1e-3, abs=1e-8)  # mse of a <=1e-4 deviation
