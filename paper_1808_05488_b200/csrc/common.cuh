@@ -113,7 +113,7 @@ CBG_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
 // (no "memory" clobber: ordering w.r.t. consumers is carried by the mbarrier /
 // wait_group that completes the copy, so the compiler may hoist address math)
 CBG_DEV void cp_async16(uint32_t dst_smem, const void* src, uint32_t src_bytes) {
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(src_bytes));
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(src_bytes));
 }
 CBG_DEV uint32_t lds_u32(uint32_t addr) {
   uint32_t v;

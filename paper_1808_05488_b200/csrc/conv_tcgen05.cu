@@ -247,11 +247,6 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         mbar_wait(&empty[stage], phase ^ 1);
         if (ftid == 0) TRACE(4, g);
         uint8_t* sA = smem + stage * C::kStageBytes;
-        if (ftid == 0) {
-          mbar_arrive_expect_tx(&full[stage], 2 * C::kBBytes);
-          bulk_g2s(sA + kABytes, bimg + static_cast<long long>(kb) * 2 * C::kBBytes, 2 * C::kBBytes,
-                   &full[stage]);
-        }
         const uint32_t base = smem_u32(sA);
 #pragma unroll
         for (int i = 0; i < kFetchChunks; ++i) {
@@ -261,6 +256,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
           cp_async16(base + r * 128 + ((q ^ (r & 7)) << 4), ok ? src + (roff[i] + toff) : src, ok ? 16u : 0u);
         }
         cp_async_mbar_arrive(&raw[stage]);
+        // the weight K-block on the TMA engine, after this thread's gather copies
+        // are queued (issuing it first delayed the whole warp's copies)
+        if (ftid == 32) {
+          mbar_arrive_expect_tx(&full[stage], 2 * C::kBBytes);
+          bulk_g2s(sA + kABytes, bimg + static_cast<long long>(kb) * 2 * C::kBBytes, 2 * C::kBBytes,
+                   &full[stage]);
+        }
         if (ftid == 0) TRACE(0, g);
       }
     }

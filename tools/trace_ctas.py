@@ -77,3 +77,11 @@ c = chk[:, :min(64, nt0 * nch)]
 print("epilogue chunks (cycles): TMEM ld+wait", (c[1] - c[0]).tolist()[:16])
 print("                          compute+stage ", (c[2] - c[1]).tolist()[:16])
 print("                          stores        ", (c[3] - c[2]).tolist()[:16])
+if len(sys.argv) > 3 and sys.argv[3] == "window":
+    names = ["issued", "conv_saw_raw", "mma_saw_full", "mma_issued", "fetch_got_empty", "conv_done"]
+    lo = min(100, tr.shape[1] - 20)
+    base = int(tr[4, lo])
+    print("K-block window (cycles relative to fetch_got_empty of block %d):" % lo)
+    print("  kb " + " ".join(f"{n:>15s}" for n in names))
+    for kb in range(lo, lo + 16):
+        print(f"{kb:4d} " + " ".join(f"{int(tr[e, kb]) - base:15d}" for e in range(6)))
