@@ -231,10 +231,18 @@ def main():
     import numpy as np
     import torch
 
+    # BENCH_DEVICE_MOD / BENCH_DIST_BACKEND only exist to exercise the N>1 code
+    # path on a one-GPU box (ranks share the device over gloo); the driver's runs
+    # use one GPU per rank over NCCL.
+    local = local % int(os.environ.get("BENCH_DEVICE_MOD", "1000000"))
     torch.cuda.set_device(local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     from paper_1808_05488_b200 import cbi
     from paper_1808_05488_b200.sharding import max_over_ranks as _max_over_ranks
     from paper_1808_05488_b200.sharding import weak_shard
