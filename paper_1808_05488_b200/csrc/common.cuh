@@ -115,6 +115,17 @@ CBG_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
 CBG_DEV void cp_async16(uint32_t dst_smem, const void* src, uint32_t src_bytes) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst_smem), "l"(src), "r"(src_bytes));
 }
+// Shared-memory vector accesses without "memory" clobbers (callers order them
+// with warp_sync_mem / barriers), so several can be in flight at once.
+CBG_DEV float4 lds_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(addr));
+  return v;
+}
+CBG_DEV void sts_f4(uint32_t addr, float4 v) {
+  asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
+}
+CBG_DEV void warp_sync_mem() { asm volatile("bar.warp.sync 0xffffffff;" ::: "memory"); }
 CBG_DEV uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
   asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));

@@ -402,7 +402,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     constexpr int CH = NPAD >= 32 ? 32 : 16;
     constexpr int LPR = CH / 4;     // lanes per pixel row in the store phase
     constexpr int RPI = 32 / LPR;   // pixel rows per store instruction
-    float* tbuf = epi_buf + warp * 32 * (CH + 4);
+    const uint32_t tbuf_u32 = smem_u32(epi_buf + warp * 32 * (CH + 4));
+    const uint32_t s_bias_u32 = smem_u32(s_bias);
     int acc = 0;
     uint32_t acc_phase = 0;
     int tile_no = 0;
@@ -416,9 +417,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       const int p = valid ? a.idx[s * HWout + k] : -1;
       float* obase = a.out + s * HWout * a.Co4;
       const int nbase = nt * NPAD;
-      float ys = 1.0f;  // undo the fp16 operand scales: 2^(e + ew), two exact steps
-      if constexpr (PREC == kPrecF16) ys = exp2i(f16_scale_exp(__ldg(a.amax_in + s)));
-      const float ws = PREC == kPrecF16 ? exp2i(a.w_exp) : 1.0f;
+      float ys = 1.0f, ws = 1.0f;  // undo the fp16 operand scales: y * 2^e * 2^ew (both exact)
+      if constexpr (PREC == kPrecF16) {
+        ys = exp2i(f16_scale_exp(__ldg(a.amax_in + s)));
+        ws = exp2i(a.w_exp);
+      }
       float vmax = 0.0f;  // |written value| bound for the consumers' scales
       mbar_wait(&tfull[acc], acc_phase);
       EPI_MARK(0, tile_no);
@@ -440,23 +443,30 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
           if (lane == 0) mbar_arrive(&tempty[acc]);
           EPI_MARK(1, tile_no);
         }
-        const float4* bias4 = reinterpret_cast<const float4*>(s_bias + nbase + n0);
+        // shared-memory traffic as explicit ld/st.shared (the buffers' generic
+        // pointers compiled to generic LD/ST); no "memory" clobbers, so the
+        // compiler keeps them in flight together; bar.warp.sync orders them
+        const uint32_t bias_s = s_bias_u32 + 4u * static_cast<uint32_t>(nbase + n0);
+        const uint32_t row_s = tbuf_u32 + 4u * static_cast<uint32_t>(lane * (CH + 4));
 #pragma unroll
         for (int j = 0; j < CH / 4; ++j) {
-          const float4 b = bias4[j];  // broadcast
+          const float4 b = lds_f4(bias_s + 16u * j);  // broadcast
           float o[4];
 #pragma unroll
           for (int u = 0; u < 4; ++u) {
             float y = __uint_as_float(r[4 * j + u]);
-            if constexpr (PREC == kPrecF16) y = (y * ys) * ws;
-            y = y + (&b.x)[u];
+            // (y * 2^e) * 2^ew + b: the products are exact, so the fused form
+            // rounds once, like the reference's y + b
+            if constexpr (PREC == kPrecF16) y = fmaf(y * ys, ws, (&b.x)[u]);
+            else y = y + (&b.x)[u];
             if (a.relu) y = (y < 0.0f) ? 0.0f : y;  // std::max(v, 0.f)
             o[u] = y;
-            vmax = fmaxf(vmax, valid ? fabsf(y) : 0.0f);
+            vmax = fmaxf(vmax, fabsf(y));
           }
-          *reinterpret_cast<float4*>(tbuf + lane * (CH + 4) + 4 * j) = make_float4(o[0], o[1], o[2], o[3]);
+          sts_f4(row_s + 16u * j, make_float4(o[0], o[1], o[2], o[3]));
         }
-        __syncwarp();
+        if (!valid) vmax = 0.0f;
+        warp_sync_mem();
         CHUNK_MARK(2, cidx);
         const int c4 = lane % LPR;
         const int n = nbase + n0 + 4 * c4;
@@ -466,12 +476,12 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         for (int i = 0; i < 32 / RPI; ++i) {
           const int rr = i * RPI + lane / LPR;
           pr[i] = __shfl_sync(0xffffffffu, p, rr);
-          v[i] = *reinterpret_cast<const float4*>(tbuf + rr * (CH + 4) + 4 * c4);
+          v[i] = lds_f4(tbuf_u32 + 4u * static_cast<uint32_t>(rr * (CH + 4) + 4 * c4));
         }
 #pragma unroll
         for (int i = 0; i < 32 / RPI; ++i)
           if (pr[i] >= 0 && n < a.Co4) *reinterpret_cast<float4*>(obase + static_cast<long long>(pr[i]) * a.Co4 + n) = v[i];
-        __syncwarp();
+        warp_sync_mem();
         CHUNK_MARK(3, cidx);
       }
 #pragma unroll
