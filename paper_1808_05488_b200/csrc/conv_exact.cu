@@ -33,21 +33,49 @@ constexpr int kThreads = 128;
 constexpr int kPix = 2;
 constexpr int kMaxStreams = 1024;  // changed pixels per thread (each weight broadcast feeds both)
 
+// Packed fp32x2 arithmetic (sm_100 FMUL2 / FFMA2): two lanes per instruction.
+// mul.rn rounds each product like the reference's `kr[o] * xv`; the add is an
+// fma with a multiplier of 1.0 that ptxas cannot see (`one` is a kernel
+// argument), i.e. RN(acc * 1 + prod) = RN(acc + prod), the reference's
+// `acc[o] += ...`. A plain add.rn.f32x2 after mul.rn.f32x2 is contracted into
+// FFMA2 by ptxas (one rounding: not the reference's result).
+CBG_DEV unsigned long long f2_pack(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+CBG_DEV void f2_unpack(unsigned long long v, float& lo, float& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(lo), "=f"(hi) : "l"(v));
+}
+CBG_DEV unsigned long long f2_mul(unsigned long long a, unsigned long long b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+  return r;
+}
+CBG_DEV unsigned long long f2_fma(unsigned long long a, unsigned long long b, unsigned long long c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+  return r;
+}
+
 // One kernel row (KW taps of one input channel and kernel row) of the sum for
-// kPix pixels.
+// kPix pixels; acc holds output-channel pairs.
 template <int G, int KW>
-CBG_DEV void exact_row(float (&acc)[kPix][G], const float (&xv)[kPix][KW], const float4* w4) {
+CBG_DEV void exact_row(unsigned long long (&acc)[kPix][G / 2], const float (&xv)[kPix][KW], const float4* w4,
+                       unsigned long long one) {
 #pragma unroll
   for (int ki = 0; ki < KW; ++ki) {
+    unsigned long long xx[kPix];
+#pragma unroll
+    for (int u = 0; u < kPix; ++u) xx[u] = f2_pack(xv[u][ki], xv[u][ki]);
 #pragma unroll
     for (int q = 0; q < G / 4; ++q) {
       const float4 w = w4[ki * (G / 4) + q];
+      const unsigned long long w01 = f2_pack(w.x, w.y), w23 = f2_pack(w.z, w.w);
 #pragma unroll
       for (int u = 0; u < kPix; ++u) {
-        acc[u][4 * q + 0] = __fadd_rn(acc[u][4 * q + 0], __fmul_rn(w.x, xv[u][ki]));
-        acc[u][4 * q + 1] = __fadd_rn(acc[u][4 * q + 1], __fmul_rn(w.y, xv[u][ki]));
-        acc[u][4 * q + 2] = __fadd_rn(acc[u][4 * q + 2], __fmul_rn(w.z, xv[u][ki]));
-        acc[u][4 * q + 3] = __fadd_rn(acc[u][4 * q + 3], __fmul_rn(w.w, xv[u][ki]));
+        acc[u][2 * q + 0] = f2_fma(acc[u][2 * q + 0], one, f2_mul(w01, xx[u]));
+        acc[u][2 * q + 1] = f2_fma(acc[u][2 * q + 1], one, f2_mul(w23, xx[u]));
       }
     }
   }
@@ -156,11 +184,12 @@ __global__ void __launch_bounds__(kThreads) conv_exact_kernel(ConvExactArgs a) {
         off += cwrap;
       }
     };
-    float acc[kPix][G];
+    unsigned long long acc[kPix][G / 2];
 #pragma unroll
     for (int u = 0; u < kPix; ++u)
 #pragma unroll
-      for (int o = 0; o < G; ++o) acc[u][o] = 0.0f;
+      for (int o = 0; o < G / 2; ++o) acc[u][o] = 0ull;  // +0.0f pairs
+    const unsigned long long one = a.one_x2;
     if constexpr (KW == 1 && PS == 0 && !CHECK) {
       if (a.kh == 1 && a.cstride == 1) {
         // 1x1 on NHWC: r = c, a pixel's channel vector is contiguous and
@@ -184,7 +213,7 @@ __global__ void __launch_bounds__(kThreads) conv_exact_kernel(ConvExactArgs a) {
               float xv[kPix][1];
 #pragma unroll
               for (int u = 0; u < kPix; ++u) xv[u][0] = (&xq[0][u].x)[e];
-              exact_row<G, 1>(acc, xv, sw4 + (4 * c4 + e) * (G / 4));
+              exact_row<G, 1>(acc, xv, sw4 + (4 * c4 + e) * (G / 4), one);
             }
           }
 #pragma unroll
@@ -205,14 +234,14 @@ __global__ void __launch_bounds__(kThreads) conv_exact_kernel(ConvExactArgs a) {
     for (; row + 2 <= rows; row += 2) {
       load_row(off, kj, xb);
       advance();
-      exact_row<G, KW>(acc, xa, sw4 + row * KW * (G / 4));
+      exact_row<G, KW>(acc, xa, sw4 + row * KW * (G / 4), one);
       if (row + 2 < rows) {
         load_row(off, kj, xa);
         advance();
       }
-      exact_row<G, KW>(acc, xb, sw4 + (row + 1) * KW * (G / 4));
+      exact_row<G, KW>(acc, xb, sw4 + (row + 1) * KW * (G / 4), one);
     }
-    if (row < rows) exact_row<G, KW>(acc, xa, sw4 + row * KW * (G / 4));
+    if (row < rows) exact_row<G, KW>(acc, xa, sw4 + row * KW * (G / 4), one);
     }
   epilogue:
 #pragma unroll
@@ -226,7 +255,9 @@ __global__ void __launch_bounds__(kThreads) conv_exact_kernel(ConvExactArgs a) {
           float v[4];
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            float y = __fadd_rn(acc[u][4 * q + e], o + e < a.Cout ? __ldg(a.bias + o + e) : 0.0f);
+            float alo, ahi;
+            f2_unpack(acc[u][2 * q + (e >> 1)], alo, ahi);
+            float y = __fadd_rn((e & 1) ? ahi : alo, o + e < a.Cout ? __ldg(a.bias + o + e) : 0.0f);
             if (a.relu) y = (y < 0.0f) ? 0.0f : y;  // std::max(v, 0.f)
             v[e] = o + e < a.Cout ? y : 0.0f;
             vmax = fmaxf(vmax, fabsf(v[e]));
