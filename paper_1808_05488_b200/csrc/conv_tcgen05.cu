@@ -70,20 +70,31 @@ CBG_DEV unsigned long long gtimer() {
 
 namespace {
 
-constexpr int kFetchWarps = 8;
-constexpr int kConvWarps = 8;
-constexpr int kFetch = kFetchWarps * 32;
-constexpr int kConv = kConvWarps * 32;
-constexpr int kFirstConvWarp = 4 + kFetchWarps;
-constexpr int kMmaWarp = kFirstConvWarp + kConvWarps;
-constexpr int kThreads = (kMmaWarp + 1) * 32;
-// Fetch and convert warps each form 2 groups that take alternating K-blocks,
-// so two K-blocks are in flight per role (a single group serialized on the
-// per-K-block latency of its waits, loads and proxy fence).
-constexpr int kGroups = 2;
-constexpr int kFetchG = kFetch / kGroups;        // fetch threads per group
-constexpr int kConvG = kConv / kGroups;          // convert threads per group
-constexpr int kFetchChunks = 128 * 8 / kFetchG;  // 16-B A chunks per fetch thread per K-block
+// Warp roles per N tile (21 warps = 672 threads either way):
+//   N <= 128: 4 epilogue, 8 fetch (2 groups), 8 convert (2 groups), 1 MMA
+//   N == 256: 8 epilogue (2 per TMEM lane quarter, half the columns each: the
+//             single accumulator stalls the MMAs until it is drained), 8 fetch,
+//             4 convert (1 group: 128 rows of a K-block convert in ~560 cycles,
+//             within the 768-cycle fp16 MMA time), 1 MMA
+template <int NPAD>
+struct Roles {
+  static constexpr int kEpiWarps = NPAD >= 256 ? 8 : 4;
+  static constexpr int kFetchWarps = 8;
+  static constexpr int kConvWarps = NPAD >= 256 ? 4 : 8;
+  static constexpr int kFirstFetchWarp = kEpiWarps;
+  static constexpr int kFirstConvWarp = kFirstFetchWarp + kFetchWarps;
+  static constexpr int kMmaWarp = kFirstConvWarp + kConvWarps;
+  static constexpr int kFetchGroups = 2;                   // fetch groups take alternating K-blocks
+  static constexpr int kConvGroups = kConvWarps / 4;       // convert groups (128 rows each)
+  static constexpr int kFetchG = kFetchWarps * 32 / kFetchGroups;
+  static constexpr int kConvG = 128;
+  static constexpr int kFetchChunks = 128 * 8 / kFetchG;   // 16-B A chunks per fetch thread per K-block
+  static_assert(kMmaWarp == 20, "21 warps");
+};
+constexpr int kThreads = 21 * 32;
+constexpr int kGroups = 2;  // stage counts are multiples of this (fetch and convert groups)
+// epilogue transpose buffers: one [32][CH + 4] per epilogue warp (CH = 32, or 16 for N = 16)
+__host__ __device__ constexpr int epi_buf_floats(int npad) { return (npad >= 256 ? 8 : 4) * 32 * 36; }
 constexpr int kBM = 128;                 // UMMA M
 constexpr int kBK = 32;                  // fp32 elements per K-block (= one 128-B swizzle row)
 constexpr int kABytes = kBM * kBK * 4;   // raw fp32 A rows of one K-block: 16 KB
@@ -112,9 +123,11 @@ struct Cfg {
   // group: with an odd count, a convert group could reach a stage one lap ahead
   // of the other group's fetch and take that stage's previous `raw` phase
   // (mbarrier parity aliases modulo 2) as complete.
-  static constexpr int kStages = PREC == kPrecF16 ? (NPAD >= 256 ? 4 : NPAD >= 128 ? 6 : 8)
+  // (N = 256 has one convert group, so any count works there; 3 leaves room
+  // for its 8 epilogue warps' transpose buffers)
+  static constexpr int kStages = PREC == kPrecF16 ? (NPAD >= 256 ? 3 : NPAD >= 128 ? 6 : 8)
                                                   : (NPAD >= 256 ? 2 : NPAD >= 128 ? 4 : 6);
-  static_assert(kStages % kGroups == 0, "stages must be a multiple of the producer groups");
+  static_assert(kStages % Roles<NPAD>::kConvGroups == 0, "stages must be a multiple of the convert groups");
   static constexpr int kNAcc = NPAD >= 256 ? 1 : 2;  // TMEM accumulator buffers
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kAColBase = kNAcc * NPAD;  // first A stage column
@@ -131,13 +144,14 @@ CBG_DEV int f16_scale_exp(float bound) {
 }
 CBG_DEV float exp2i(int e) { return __uint_as_float(static_cast<uint32_t>(e + 127) << 23); }
 
-__host__ __device__ constexpr int tail_bytes(int stages, int KB, int S, int nbias) {
-  return 8 * (3 * stages + 4) + 16 + kBM * 8 + (S + 1) * 4 + 16 + 4 * 32 * 36 * 4 + 4 * nbias + 0 * KB;
+__host__ __device__ constexpr int tail_bytes(int stages, int KB, int S, int nbias, int npad) {
+  return 8 * (3 * stages + 4) + 16 + kBM * 8 + (S + 1) * 4 + 16 + 4 * epi_buf_floats(npad) + 4 * nbias + 0 * KB;
 }
 
 template <int NPAD, int PREC>
 __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) {
   using C = Cfg<NPAD, PREC>;
+  using R = Roles<NPAD>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tail = smem + C::kStages * C::kStageBytes;
@@ -151,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   int* tprefix = reinterpret_cast<int*>(rowinfo + kBM);
   float* epi_buf = reinterpret_cast<float*>(
       (reinterpret_cast<uintptr_t>(tprefix + a.S + 1) + 15) & ~uintptr_t(15));  // [4 warps][32][CH + 4]
-  float* s_bias = epi_buf + 4 * 32 * 36;                                       // [n_tiles * NPAD]
+  float* s_bias = epi_buf + epi_buf_floats(NPAD);                              // [n_tiles * NPAD]
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -162,17 +176,17 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   // ---- setup -----------------------------------------------------------------
   if (tid == 0) {
     for (int i = 0; i < C::kStages; ++i) {
-      mbar_init(&full[i], kConvWarps / kGroups + 1);  // one convert group + 1 expect_tx arrive
+      mbar_init(&full[i], R::kConvWarps / R::kConvGroups + 1);  // one convert group + 1 expect_tx arrive
       mbar_init(&empty[i], 1);              // tcgen05.commit
-      mbar_init(&raw[i], kFetchG);          // one cp.async.mbarrier.arrive per fetch thread of a group
+      mbar_init(&raw[i], R::kFetchG);       // one cp.async.mbarrier.arrive per fetch thread of a group
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
-      mbar_init(&tempty[i], 4);    // 4 epilogue warps
+      mbar_init(&tempty[i], R::kEpiWarps);
     }
     fence_mbar_init();
   }
-  if (warp == kMmaWarp) tmem_alloc(tmem_holder, C::kTmemCols);
+  if (warp == R::kMmaWarp) tmem_alloc(tmem_holder, C::kTmemCols);
   for (int i = tid; i < a.n_tiles * NPAD; i += kThreads) s_bias[i] = a.bias[i];  // zero-padded to n_tiles*NPAD
   if (warp == 0) {
     int carry = 0;
@@ -210,10 +224,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     nt = local - mt * a.n_tiles;
   };
 
-  if (warp >= 4 && warp < kFirstConvWarp) {
+  if (warp >= R::kFirstFetchWarp && warp < R::kFirstConvWarp) {
     // ========================= fetch =========================
-    const int fgrp = (tid - 128) / kFetchG;  // K-blocks g with g % kGroups == fgrp
-    const int ftid = (tid - 128) % kFetchG;
+    constexpr int kFetchG = R::kFetchG, kFetchChunks = R::kFetchChunks;
+    const int fgrp = (tid - 32 * R::kFirstFetchWarp) / kFetchG;  // K-blocks g with g % groups == fgrp
+    const int ftid = (tid - 32 * R::kFirstFetchWarp) % kFetchG;
     const int q = ftid & 7;
     const uint2* ktab = reinterpret_cast<const uint2*>(a.ktab);  // (tap code, element offset) per 16-B chunk
     uint32_t g = 0;  // global K-block counter (stage = g % kStages)
@@ -236,7 +251,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       const uint8_t* bimg = a.wimg + static_cast<long long>(nt) * a.KB * 2 * C::kBBytes;
 #pragma unroll 1
       for (int kb = 0; kb < a.KB; ++kb, ++g) {
-        if (static_cast<int>(g % kGroups) != fgrp) continue;
+        if (static_cast<int>(g % R::kFetchGroups) != fgrp) continue;
         const int stage = g % C::kStages;
         const uint32_t phase = (g / C::kStages) & 1;
         const uint2 tk = __ldg(ktab + kb * 8 + q);
@@ -266,10 +281,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         if (ftid == 0) TRACE(0, g);
       }
     }
-  } else if (warp >= kFirstConvWarp && warp < kMmaWarp) {
+  } else if (warp >= R::kFirstConvWarp && warp < R::kMmaWarp) {
     // ========================= convert =========================
-    const int cgrp = (tid - kFirstConvWarp * 32) / kConvG;
-    const int ctid = (tid - kFirstConvWarp * 32) % kConvG;
+    const int cgrp = (tid - R::kFirstConvWarp * 32) / R::kConvG;
+    const int ctid = (tid - R::kFirstConvWarp * 32) % R::kConvG;
     uint32_t g = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       float xs = 1.0f;  // fp16 operand scale 2^-e of this tile's stream
@@ -280,7 +295,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       }
 #pragma unroll 1
       for (int kb = 0; kb < a.KB; ++kb, ++g) {
-        if (static_cast<int>(g % kGroups) != cgrp) continue;
+        if (static_cast<int>(g % R::kConvGroups) != cgrp) continue;
         const int stage = g % C::kStages;
         const uint32_t phase = (g / C::kStages) & 1;
         mbar_wait(&raw[stage], phase);
@@ -349,7 +364,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         if (ctid == 0) TRACE(5, g);
       }
     }
-  } else if (warp == kMmaWarp) {
+  } else if (warp == R::kMmaWarp) {
     // ========================= MMA issuer =========================
     // The whole warp runs the loop (warp-uniform control flow and operands);
     // elect.sync inside the asm picks the issuing lane.
@@ -393,7 +408,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       }
     }
     if (lane == 0) CTA_MARK(2);
-  } else if (warp < 4) {
+  } else if (warp < R::kEpiWarps) {
     // ========================= epilogue =========================
     // Per chunk of CH accumulator columns: tcgen05.ld (lane = row) -> scale,
     // bias, ReLU -> the warp's smem transpose buffer -> global stores in which
@@ -402,6 +417,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     constexpr int CH = NPAD >= 32 ? 32 : 16;
     constexpr int LPR = CH / 4;     // lanes per pixel row in the store phase
     constexpr int RPI = 32 / LPR;   // pixel rows per store instruction
+    constexpr int NCOL = NPAD / (R::kEpiWarps / 4);  // accumulator columns of this warp
+    const int quarter = warp & 3;                     // TMEM lanes 32*quarter .. +31 (= warp % 4)
+    const int col0 = (warp >> 2) * NCOL;
     const uint32_t tbuf_u32 = smem_u32(epi_buf + warp * 32 * (CH + 4));
     const uint32_t s_bias_u32 = smem_u32(s_bias);
     int acc = 0;
@@ -412,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       int s, mt, nt;
       decode(w, s, mt, nt);
       const int cnt = a.count[s];
-      const int k = mt * kBM + warp * 32 + lane;
+      const int k = mt * kBM + quarter * 32 + lane;
       const bool valid = k < cnt;
       const int p = valid ? a.idx[s * HWout + k] : -1;
       float* obase = a.out + s * HWout * a.Co4;
@@ -426,10 +444,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       mbar_wait(&tfull[acc], acc_phase);
       EPI_MARK(0, tile_no);
       tc_fence_after();
-      const uint32_t tb = tmem_base + (static_cast<uint32_t>(warp * 32) << 16) + acc * NPAD;
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * NPAD;
 #pragma unroll 1
-      for (int n0 = 0; n0 < NPAD; n0 += CH) {
-        const int cidx = tile_no * (NPAD / CH) + n0 / CH;
+      for (int n0 = col0; n0 < col0 + NCOL; n0 += CH) {
+        const int cidx = tile_no * (NCOL / CH) + (n0 - col0) / CH;
         (void)cidx;
         CHUNK_MARK(0, cidx);
         uint32_t r[CH];
@@ -437,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         else tmem_ld16(tb + n0, r);
         tmem_ld_wait();
         CHUNK_MARK(1, cidx);
-        if (n0 + CH >= NPAD) {  // last TMEM read of the tile: hand the accumulator back
+        if (n0 + CH >= col0 + NCOL) {  // this warp's last TMEM read of the tile: hand its part back
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tempty[acc]);
@@ -499,7 +517,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   tc_fence_before();
   __syncthreads();
   if (tid == 0) CTA_MARK(3);
-  if (warp == kMmaWarp) {
+  if (warp == R::kMmaWarp) {
     tc_fence_after();
     tmem_dealloc(tmem_base, C::kTmemCols);
   }
@@ -569,7 +587,7 @@ int conv_gemm_stages(int npad, int prec) {
 int conv_gemm_smem_bytes(int npad, int KB, int S, int prec, int n_tiles) {
   const int stages = conv_gemm_stages(npad, prec);
   const int stage_bytes = kABytes + 2 * npad * (prec == kPrecF16 ? 64 : 128);
-  return 1024 + stages * stage_bytes + tail_bytes(stages, KB, S, n_tiles * npad);
+  return 1024 + stages * stage_bytes + tail_bytes(stages, KB, S, n_tiles * npad, npad);
 }
 
 void launch_conv_gemm(const ConvGemmArgs& a, cudaStream_t st) {
