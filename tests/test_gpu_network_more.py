@@ -235,3 +235,55 @@ def test_stats_csv_byte_identical(gpu):
         ga, wa = a.split(","), b.split(",")
         assert ga[:6] == wa[:6]
         assert float(ga[6]) == pytest.approx(float(wa[6]), rel=1e-3, abs=1e-8)  # mse of a <=1e-4 deviation
+
+
+def _conv(name, cin, cout, k, stride, pad, relu, rng, frm=None):
+    s = cbi.ConvSpec(cin, cout, k, k, stride, pad)
+    a = 1.0 / np.sqrt(cin * k * k)
+    s.weights = rng.uniform(-a, a, s.weight_count()).astype(np.float32)
+    s.bias = rng.uniform(-0.1, 0.1, cout).astype(np.float32)
+    d = cbi.LayerDesc(cbi.LayerKind.Conv, name, list(frm or []), s, relu)
+    return d
+
+
+@pytest.mark.parametrize("prec", ["f16", "tf32"])
+def test_wide_strided_and_reused_layers(gpu, monkeypatch, prec):
+    """Tensor-path corners under both operand splits: Cout 300 (two N tiles of
+    256), stride-2 5x5 with padding, K > 4000 (a 9x9 over 56 channels), Cout
+    40 / 24 (N tiles 64 / 32), a Reuse1x1 layer whose GEMM source is the
+    producer's output (magnitude bound through amax_origin), and inputs of
+    magnitude ~40 (fp16 operands need scaling)."""
+    monkeypatch.setenv("CBG_GEMM_PREC", prec)
+    rng = np.random.default_rng(91)
+    L = [_conv("A", 3, 40, 3, 1, 1, True, rng), _conv("B", 40, 300, 5, 2, 2, True, rng),
+         _conv("C", 300, 56, 1, 1, 0, True, rng), _conv("D", 56, 24, 9, 1, 4, True, rng),
+         _conv("E", 24, 24, 1, 1, 0, False, rng)]
+    spec = cbi.NetworkSpec(3, 44, 52, L)
+    taus = [0.5, 0.05, 0.05, 0.02, 0.02]
+    pol = [cbi.DetectionPolicy.Detect] * 4 + [cbi.DetectionPolicy.Reuse1x1]
+    frames = 40.0 * cbi.gen_synthetic(cbi.SyntheticConfig(44, 52, 3, 5, 2, 9, 2, 3, 0.002, 17))
+    run_pair(spec, taus, frames, pol)
+
+
+def test_many_streams_mixed_activity(gpu):
+    """33 streams in one set (odd count, not a multiple of the GEMM grid's
+    structure), some static, some with motion, some after a reset."""
+    S, H, W = 33, 48, 64
+    spec = cbi.make_seg_spec(7, H, W)
+    taus = [0.05] * 5
+    seqs = []
+    for s in range(S):
+        n_obj = 0 if s % 3 == 0 else (s % 5) + 1
+        seqs.append(cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, 4, n_obj, 8, 2, 2, 0.0, 50 + s)))
+    net = cbi.convert_to_cb(spec, taus, n_streams=S)
+    refs = [oracle.RefNet(spec, taus) for _ in range(S)]
+    for t in range(4):
+        if t == 2:
+            net.reset(5)
+            refs[5].reset()
+        net.enqueue(np.stack([seqs[s][t] for s in range(S)]))
+        counts = net.counts()
+        for s in range(S):
+            want = refs[s].forward(seqs[s][t])
+            assert oracle.max_rel_err(net.output(s), want) <= TOL, (t, s)
+            assert counts[0, s] == refs[s].stats(0)["changed_px"], (t, s)
