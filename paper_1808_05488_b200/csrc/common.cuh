@@ -125,6 +125,11 @@ CBG_DEV float4 lds_f4(uint32_t addr) {
 CBG_DEV void sts_f4(uint32_t addr, float4 v) {
   asm volatile("st.shared.v4.f32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w));
 }
+CBG_DEV uint2 lds_u2(uint32_t addr) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(addr));
+  return v;
+}
 CBG_DEV void warp_sync_mem() { asm volatile("bar.warp.sync 0xffffffff;" ::: "memory"); }
 CBG_DEV uint32_t lds_u32(uint32_t addr) {
   uint32_t v;
@@ -286,6 +291,13 @@ CBG_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
       "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
       "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
+}
+// 16 lanes x 512 bit: thread t writes lane t/4 (+8) columns 2(t%4)..+1 and 8+2(t%4)..+1
+// (registers: [lane, cols 2c..] [lane+8, 2c..] [lane, 8+2c..] [lane+8, 8+2c..]).
+CBG_DEV void tmem_st_16x256b_x2(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.16x256b.x2.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
 }
 CBG_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 

@@ -70,23 +70,34 @@ CBG_DEV unsigned long long gtimer() {
 
 namespace {
 
+constexpr int kPrecTF32 = 0;
+constexpr int kPrecF16 = 1;        // fp16 split, A staged through shared memory by fetch warps
+constexpr int kPrecF16Direct = 2;  // fp16 split, A loaded by the convert warps straight from global
+__host__ __device__ constexpr bool is_f16(int p) { return p != kPrecTF32; }
+__host__ __device__ constexpr bool is_direct(int p) { return p == kPrecF16Direct; }
+
 // Warp roles per N tile (21 warps = 672 threads either way):
 //   N <= 128: 4 epilogue, 8 fetch (2 groups), 8 convert (2 groups), 1 MMA
 //   N == 256: 8 epilogue (2 per TMEM lane quarter, half the columns each: the
 //             single accumulator stalls the MMAs until it is drained), 8 fetch,
 //             4 convert (1 group: 128 rows of a K-block convert in ~560 cycles,
 //             within the 768-cycle fp16 MMA time), 1 MMA
-template <int NPAD>
+//   direct (kPrecF16Direct): no fetch warps; 16 (N <= 128) or 12 (N = 256)
+//             convert warps in groups of 4 that load their K-block's rows from
+//             global memory into registers, split them and store them into
+//             TMEM with tcgen05.st.16x256b (4 threads per row, 2 rows per
+//             thread per store); A never touches shared memory
+template <int NPAD, int PREC>
 struct Roles {
   static constexpr int kEpiWarps = NPAD >= 256 ? 8 : 4;
-  static constexpr int kFetchWarps = 8;
-  static constexpr int kConvWarps = NPAD >= 256 ? 4 : 8;
+  static constexpr int kFetchWarps = is_direct(PREC) ? 0 : 8;
+  static constexpr int kConvWarps = is_direct(PREC) ? 20 - kEpiWarps : NPAD >= 256 ? 4 : 8;
   static constexpr int kFirstFetchWarp = kEpiWarps;
   static constexpr int kFirstConvWarp = kFirstFetchWarp + kFetchWarps;
   static constexpr int kMmaWarp = kFirstConvWarp + kConvWarps;
   static constexpr int kFetchGroups = 2;                   // fetch groups take alternating K-blocks
   static constexpr int kConvGroups = kConvWarps / 4;       // convert groups (128 rows each)
-  static constexpr int kFetchG = kFetchWarps * 32 / kFetchGroups;
+  static constexpr int kFetchG = is_direct(PREC) ? 128 : kFetchWarps * 32 / kFetchGroups;
   static constexpr int kConvG = 128;
   static constexpr int kFetchChunks = 128 * 8 / kFetchG;   // 16-B A chunks per fetch thread per K-block
   static_assert(kMmaWarp == 20, "21 warps");
@@ -109,15 +120,12 @@ constexpr int kMaxS = 1024;
 //              scaled by 2^-ew on the host; kind::f16 at twice the tf32 rate,
 //              K = 16 per MMA, B rows of 64 B (32 fp16) per K-block (SW64);
 //              the epilogue multiplies by 2^(e+ew) (exact).
-constexpr int kPrecTF32 = 0;
-constexpr int kPrecF16 = 1;
-
 template <int NPAD, int PREC>
 struct Cfg {
-  static constexpr int kBRow = PREC == kPrecF16 ? 64 : 128;  // B bytes per row per K-block
+  static constexpr int kBRow = is_f16(PREC) ? 64 : 128;  // B bytes per row per K-block
   static constexpr int kBBytes = NPAD * kBRow;
-  static constexpr int kStageBytes = kABytes + 2 * kBBytes;
-  static constexpr int kACols = PREC == kPrecF16 ? kBK : 2 * kBK;  // TMEM columns of A_hi | A_lo
+  static constexpr int kStageBytes = (is_direct(PREC) ? 0 : kABytes) + 2 * kBBytes;
+  static constexpr int kACols = is_f16(PREC) ? kBK : 2 * kBK;  // TMEM columns of A_hi | A_lo
   static constexpr int kALo = kACols / 2;                          // A_lo column offset
   // A multiple of kGroups, so a stage is always filled and converted by the same
   // group: with an odd count, a convert group could reach a stage one lap ahead
@@ -125,9 +133,10 @@ struct Cfg {
   // (mbarrier parity aliases modulo 2) as complete.
   // (N = 256 has one convert group, so any count works there; 3 leaves room
   // for its 8 epilogue warps' transpose buffers)
-  static constexpr int kStages = PREC == kPrecF16 ? (NPAD >= 256 ? 3 : NPAD >= 128 ? 6 : 8)
-                                                  : (NPAD >= 256 ? 2 : NPAD >= 128 ? 4 : 6);
-  static_assert(kStages % Roles<NPAD>::kConvGroups == 0, "stages must be a multiple of the convert groups");
+  static constexpr int kStages = is_direct(PREC) ? (NPAD >= 256 ? 3 : 8)
+                                 : is_f16(PREC)  ? (NPAD >= 256 ? 3 : NPAD >= 128 ? 6 : 8)
+                                                 : (NPAD >= 256 ? 2 : NPAD >= 128 ? 4 : 6);
+  static_assert(kStages % Roles<NPAD, PREC>::kConvGroups == 0, "stages must be a multiple of the convert groups");
   static constexpr int kNAcc = NPAD >= 256 ? 1 : 2;  // TMEM accumulator buffers
   static constexpr uint32_t kTmemCols = 512;
   static constexpr uint32_t kAColBase = kNAcc * NPAD;  // first A stage column
@@ -144,14 +153,15 @@ CBG_DEV int f16_scale_exp(float bound) {
 }
 CBG_DEV float exp2i(int e) { return __uint_as_float(static_cast<uint32_t>(e + 127) << 23); }
 
-__host__ __device__ constexpr int tail_bytes(int stages, int KB, int S, int nbias, int npad) {
-  return 8 * (3 * stages + 4) + 16 + kBM * 8 + (S + 1) * 4 + 16 + 4 * epi_buf_floats(npad) + 4 * nbias + 0 * KB;
+__host__ __device__ constexpr int tail_bytes(int stages, int KB, int S, int nbias, int npad, bool direct) {
+  return 8 * (3 * stages + 4) + 16 + kBM * 8 + (S + 1) * 4 + 16 + 4 * epi_buf_floats(npad) + 4 * nbias +
+         (direct ? 8 * 8 * KB : 0);
 }
 
 template <int NPAD, int PREC>
 __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) {
   using C = Cfg<NPAD, PREC>;
-  using R = Roles<NPAD>;
+  using R = Roles<NPAD, PREC>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tail = smem + C::kStages * C::kStageBytes;
@@ -166,6 +176,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   float* epi_buf = reinterpret_cast<float*>(
       (reinterpret_cast<uintptr_t>(tprefix + a.S + 1) + 15) & ~uintptr_t(15));  // [4 warps][32][CH + 4]
   float* s_bias = epi_buf + epi_buf_floats(NPAD);                              // [n_tiles * NPAD]
+  uint2* s_ktab = reinterpret_cast<uint2*>(s_bias + a.n_tiles * NPAD);          // direct: [KB * 8]
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
@@ -188,6 +199,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   }
   if (warp == R::kMmaWarp) tmem_alloc(tmem_holder, C::kTmemCols);
   for (int i = tid; i < a.n_tiles * NPAD; i += kThreads) s_bias[i] = a.bias[i];  // zero-padded to n_tiles*NPAD
+  if constexpr (is_direct(PREC))
+    for (int i = tid; i < a.KB * 8; i += kThreads) s_ktab[i] = reinterpret_cast<const uint2*>(a.ktab)[i];
   if (warp == 0) {
     int carry = 0;
     if (lane == 0) tprefix[0] = 0;
@@ -281,6 +294,99 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         if (ftid == 0) TRACE(0, g);
       }
     }
+  } else if (is_direct(PREC) && warp >= R::kFirstConvWarp && warp < R::kMmaWarp) {
+    // ===================== direct load + convert =====================
+    // Group `grp` (4 warps, one per TMEM lane quarter) owns K-blocks g with
+    // g % groups == grp. A thread holds chunks c and c+4 (16 B each) of rows
+    // a, a+8 (+16, +24) of its quarter: exactly the register layout of
+    // tcgen05.st.16x256b.x2 (lane a: cols 2c..2c+1 and 8+2c..; lane a+8: same).
+    // Each load instruction reads 4 consecutive chunks (64 B) of 8 rows.
+    const int grp = (warp - R::kFirstConvWarp) >> 2;
+    const int quarter = warp & 3;
+    const int c = lane & 3, arow = lane >> 2;
+    const uint32_t ktab_s = smem_u32(s_ktab);
+    const bool leader = (warp & 3) == 0 && lane == 0;  // issues the group's weight copies
+    constexpr int G = R::kConvGroups;
+    uint32_t g = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int s, mt, nt;
+      decode(w, s, mt, nt);
+      const int cnt = a.count[s];
+      const float xs = exp2i(-f16_scale_exp(__ldg(a.amax_in + s)));
+      // rows (h, b) = 32*quarter + 16*h + 8*b + arow
+      int jb[4], ib[4], roff[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int k = mt * kBM + 32 * quarter + 8 * i + arow;
+        const int p = k < cnt ? __ldg(a.idx + s * HWout + k) : -1;
+        const int jo = p / a.Wout, io = p - jo * a.Wout;
+        jb[i] = p >= 0 ? jo * a.stride - a.pad : INT_MIN / 2;
+        ib[i] = io * a.stride - a.pad;
+        roff[i] = (jb[i] * a.Win + ib[i]) * a.Cs;
+      }
+      const float* src = a.src + s * HWin * a.Cs;
+      const uint8_t* bimg = a.wimg + static_cast<long long>(nt) * a.KB * 2 * C::kBBytes;
+      // rows 2h, 2h+1 of K-block kb -> v[2h..2h+1]
+      auto load_half = [&](int kb, int h, float4 (&v)[4][2]) {
+        const uint2 t0 = lds_u2(ktab_s + 8u * (kb * 8 + c)), t1 = lds_u2(ktab_s + 8u * (kb * 8 + c + 4));
+#pragma unroll
+        for (int b = 0; b < 2; ++b) {
+          const int i = 2 * h + b;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            const uint2 tk = j ? t1 : t0;
+            const int dj = tk.x & 0xFF, di = (tk.x >> 8) & 0xFF;
+            const bool ok = (tk.x >> 31) == 0 && static_cast<unsigned>(jb[i] + dj) < static_cast<unsigned>(a.Hin) &&
+                            static_cast<unsigned>(ib[i] + di) < static_cast<unsigned>(a.Win);
+            v[i][j] = ok ? ldg_nc_f4(src + (roff[i] + static_cast<int>(tk.y))) : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+        }
+      };
+#pragma unroll 1
+      for (int kb = 0; kb < a.KB; ++kb, ++g) {
+        if (static_cast<int>(g % G) != grp) continue;
+        const int stage = g % C::kStages;
+        const uint32_t phase = (g / C::kStages) & 1;
+        float4 v[4][2];
+        load_half(kb, 0, v);  // loads first: they do not depend on the stage being free
+        load_half(kb, 1, v);
+        mbar_wait(&empty[stage], phase ^ 1);  // TMEM A stage and B smem free
+        if (leader) {
+          TRACE(4, g);
+          mbar_arrive_expect_tx(&full[stage], 2 * C::kBBytes);
+          bulk_g2s(smem + stage * C::kStageBytes, bimg + static_cast<long long>(kb) * 2 * C::kBBytes,
+                   2 * C::kBBytes, &full[stage]);
+        }
+        const uint32_t ta = tmem_base + (static_cast<uint32_t>(32 * quarter) << 16) + C::kAColBase +
+                            stage * C::kACols;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {  // TMEM lanes 32q + 16h .. +15
+          uint32_t hi[8], lo[8];
+#pragma unroll
+          for (int j = 0; j < 2; ++j)      // chunk c, c+4 -> column pairs 2c.., 8+2c..
+#pragma unroll
+            for (int b = 0; b < 2; ++b) {  // row a, a+8 -> registers 0-1 / 2-3 (+4 for chunk c+4)
+              const float4 x = v[2 * h + b][j];
+              const float x0 = x.x * xs, x1 = x.y * xs, x2 = x.z * xs, x3 = x.w * xs;
+              const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
+              const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+              const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y);
+              const __half2 l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
+              hi[4 * j + 2 * b] = *reinterpret_cast<const uint32_t*>(&h01);
+              hi[4 * j + 2 * b + 1] = *reinterpret_cast<const uint32_t*>(&h23);
+              lo[4 * j + 2 * b] = *reinterpret_cast<const uint32_t*>(&l01);
+              lo[4 * j + 2 * b + 1] = *reinterpret_cast<const uint32_t*>(&l23);
+            }
+          tmem_st_16x256b_x2(ta + (static_cast<uint32_t>(16 * h) << 16), hi);
+          tmem_st_16x256b_x2(ta + (static_cast<uint32_t>(16 * h) << 16) + C::kALo, lo);
+        }
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[stage]);
+        if (leader) TRACE(5, g);
+      }
+    }
   } else if (warp >= R::kFirstConvWarp && warp < R::kMmaWarp) {
     // ========================= convert =========================
     const int cgrp = (tid - R::kFirstConvWarp * 32) / R::kConvG;
@@ -288,7 +394,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     uint32_t g = 0;
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       float xs = 1.0f;  // fp16 operand scale 2^-e of this tile's stream
-      if constexpr (PREC == kPrecF16) {
+      if constexpr (is_f16(PREC)) {
         int s, mt, nt;
         decode(w, s, mt, nt);
         xs = exp2i(-f16_scale_exp(__ldg(a.amax_in + s)));
@@ -307,7 +413,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         const uint32_t row = smem_u32(sA) + r * 128;
         const uint32_t ta = tmem_base + (static_cast<uint32_t>(32 * (warp & 3)) << 16) + C::kAColBase +
                             stage * C::kACols;
-        if constexpr (PREC == kPrecF16) {
+        if constexpr (is_f16(PREC)) {
 #pragma unroll
           for (int half = 0; half < 2; ++half) {  // 16 elements -> 8 packed columns each of hi and lo
             uint32_t h[8], l[8];
@@ -368,9 +474,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     // ========================= MMA issuer =========================
     // The whole warp runs the loop (warp-uniform control flow and operands);
     // elect.sync inside the asm picks the issuing lane.
-    constexpr uint32_t idesc = PREC == kPrecF16 ? umma_idesc_f16(kBM, NPAD) : umma_idesc_tf32(kBM, NPAD);
+    constexpr uint32_t idesc = is_f16(PREC) ? umma_idesc_f16(kBM, NPAD) : umma_idesc_tf32(kBM, NPAD);
     // stage 0 base; B by offset (K-major, 128-B rows for tf32, 64-B rows for fp16)
-    const uint64_t desc0 = PREC == kPrecF16 ? umma_desc_sw64(smem_u32(smem)) : umma_desc_sw128(smem_u32(smem));
+    const uint64_t desc0 = is_f16(PREC) ? umma_desc_sw64(smem_u32(smem)) : umma_desc_sw128(smem_u32(smem));
     const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
     int stage = 0;
     uint32_t phase = 0;
@@ -386,10 +492,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         TRACE(2, gm);
         tc_fence_after();
         // B descriptors: start addresses advance in 16-B units; A in TMEM
-        const uint64_t b_hi = desc0 + static_cast<uint64_t>((stage * C::kStageBytes + kABytes) >> 4);
+        const uint64_t b_hi =
+            desc0 + static_cast<uint64_t>((stage * C::kStageBytes + (is_direct(PREC) ? 0 : kABytes)) >> 4);
         const uint64_t b_lo = b_hi + (C::kBBytes >> 4);
         const uint32_t a_hi = tbase + C::kAColBase + stage * C::kACols;
-        if constexpr (PREC == kPrecF16)
+        if constexpr (is_f16(PREC))
           umma_f16x3_kblock_ts(d, a_hi, a_hi + C::kALo, b_hi, b_lo, idesc, kb != 0);
         else
           umma_tf32x3_kblock_ts(d, a_hi, a_hi + C::kALo, b_hi, b_lo, idesc, kb != 0);
@@ -436,7 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       float* obase = a.out + s * HWout * a.Co4;
       const int nbase = nt * NPAD;
       float ys = 1.0f, ws = 1.0f;  // undo the fp16 operand scales: y * 2^e * 2^ew (both exact)
-      if constexpr (PREC == kPrecF16) {
+      if constexpr (is_f16(PREC)) {
         ys = exp2i(f16_scale_exp(__ldg(a.amax_in + s)));
         ws = exp2i(a.w_exp);
       }
@@ -475,7 +582,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
             float y = __uint_as_float(r[4 * j + u]);
             // (y * 2^e) * 2^ew + b: the products are exact, so the fused form
             // rounds once, like the reference's y + b
-            if constexpr (PREC == kPrecF16) y = fmaf(y * ys, ws, (&b.x)[u]);
+            if constexpr (is_f16(PREC)) y = fmaf(y * ys, ws, (&b.x)[u]);
             else y = y + (&b.x)[u];
             if (a.relu) y = (y < 0.0f) ? 0.0f : y;  // std::max(v, 0.f)
             o[u] = y;
@@ -581,17 +688,20 @@ int conv_gemm_read_trace(unsigned long long* host, int n) {
 }
 
 int conv_gemm_stages(int npad, int prec) {
-  return prec == kPrecF16 ? stages_prec<kPrecF16>(npad) : stages_prec<kPrecTF32>(npad);
+  return prec == kPrecF16Direct ? stages_prec<kPrecF16Direct>(npad)
+         : prec == kPrecF16     ? stages_prec<kPrecF16>(npad)
+                                : stages_prec<kPrecTF32>(npad);
 }
 
 int conv_gemm_smem_bytes(int npad, int KB, int S, int prec, int n_tiles) {
   const int stages = conv_gemm_stages(npad, prec);
-  const int stage_bytes = kABytes + 2 * npad * (prec == kPrecF16 ? 64 : 128);
-  return 1024 + stages * stage_bytes + tail_bytes(stages, KB, S, n_tiles * npad, npad);
+  const int stage_bytes = (is_direct(prec) ? 0 : kABytes) + 2 * npad * (is_f16(prec) ? 64 : 128);
+  return 1024 + stages * stage_bytes + tail_bytes(stages, KB, S, n_tiles * npad, npad, is_direct(prec));
 }
 
 void launch_conv_gemm(const ConvGemmArgs& a, cudaStream_t st) {
-  if (a.prec == kPrecF16) launch_prec<kPrecF16>(a, st);
+  if (a.prec == kPrecF16Direct) launch_prec<kPrecF16Direct>(a, st);
+  else if (a.prec == kPrecF16) launch_prec<kPrecF16>(a, st);
   else launch_prec<kPrecTF32>(a, st);
 }
 

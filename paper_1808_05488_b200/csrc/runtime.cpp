@@ -358,7 +358,7 @@ void build_weight_image(const NodeRT& n, std::vector<uint8_t>& img, std::vector<
   const ConvDesc& c = n.d.conv;
   const int taps = c.kernel_h * c.kernel_w;
   const int Kreal = taps * n.Csi;
-  const bool f16 = n.prec == 1;
+  const bool f16 = n.prec != 0;
   const int Brow = f16 ? 64 : 128;
   const int Bbytes = n.npad * Brow;
   img.assign(static_cast<size_t>(n.n_tiles) * n.KB * 2 * Bbytes, 0);
@@ -422,9 +422,19 @@ void build_weight_image(const NodeRT& n, std::vector<uint8_t>& img, std::vector<
 
 // tcgen05 operand split: 3xFP16 with power-of-two scaling (default) or 3xTF32
 // (CBG_GEMM_PREC=tf32); both fp32-accurate, DESIGN.md §3.3.
-int gemm_prec() {
+// A operand path of the fp16 split: loaded by the convert warps straight from
+// global memory (2, default) or staged through shared memory by fetch warps
+// (1, CBG_GEMM_DIRECT=0). Measured on the bench (64 streams, 4 overlapped
+// stream groups): direct 50.0-50.6k frames/s, staged 48.7-49.2k, direct for
+// N = 256 only 48.8-49.5k, although in an isolated launch the staged path is
+// faster for N = 64 (L3 188 vs 204 us) and slower for N = 256 (L5 573 vs 552).
+int gemm_prec(int npad) {
   const char* e = std::getenv("CBG_GEMM_PREC");
-  return (e && std::strcmp(e, "tf32") == 0) ? 0 : 1;
+  if (e && std::strcmp(e, "tf32") == 0) return 0;
+  const char* d = std::getenv("CBG_GEMM_DIRECT");
+  if (d && std::strcmp(d, "0") == 0) return 1;
+  (void)npad;
+  return 2;
 }
 
 // Layers with at most this many output channels take the bit-exact CUDA-core
@@ -526,12 +536,12 @@ void Net::build() {
       } else {
         if (r.KB > 512) throw Error(CBG_ERR_UNSUPPORTED, "Cin*kh*kw too large for the GEMM kernel (K > 16384)");
         if (r.Csi >= 32768) throw Error(CBG_ERR_UNSUPPORTED, "too many input channels");
-        r.prec = gemm_prec();
+        r.prec = gemm_prec(r.npad);
         constexpr int kSmemMax = 232448;  // 227 KB opt-in per CTA
         if (conv_gemm_smem_bytes(r.npad, r.KB, S_, r.prec, r.n_tiles) > kSmemMax) r.prec = 0;  // fewer stages (tf32)
         if (conv_gemm_smem_bytes(r.npad, r.KB, S_, r.prec, r.n_tiles) > kSmemMax)
           throw Error(CBG_ERR_UNSUPPORTED, "conv layer too large for the GEMM kernel's shared memory (K or streams)");
-        r.w_exp = r.prec == 1 ? weight_exp(c.weights) : 0;
+        r.w_exp = r.prec != 0 ? weight_exp(c.weights) : 0;
         std::vector<uint8_t> img;
         std::vector<uint32_t> ktab;
         build_weight_image(r, img, ktab, bias);
