@@ -503,8 +503,7 @@ __global__ void __launch_bounds__(kThreads) dilate_compact_kernel(DilateCompactA
       s_out[i] = valid >= 32 ? 0xffffffffu : ((1u << valid) - 1u);
     }
   } else {
-    // 1. stage input rows as bits: one thread per 32-pixel word, 32
-    //    independent byte loads in flight per thread
+    // 1. stage input rows as bits: one thread per 32-pixel word
     for (int i = threadIdx.x; i < nin * nwi; i += blockDim.x) {
       const int r = i / nwi, w = i - r * nwi;
       const long long rowoff = static_cast<long long>(s) * HWin + static_cast<long long>(in_lo + r) * a.Win;
@@ -512,11 +511,30 @@ __global__ void __launch_bounds__(kThreads) dilate_compact_kernel(DilateCompactA
       uint32_t word = 0;
       for (int q = 0; q < a.n_in; ++q) {
         const uint8_t* src = a.in_map[q] + rowoff + c0;
-        uint8_t v[32];
+        if (n == 32) {
+          // 9 aligned 32-bit loads cover the 32 bytes at any alignment (map
+          // buffers carry 16 B of slack); funnel shifts realign them, and a
+          // byte-exact zero test of (bytes ^ epoch) gives 4 flags per word
+          const uintptr_t ad = reinterpret_cast<uintptr_t>(src);
+          const uint32_t* base = reinterpret_cast<const uint32_t*>(ad & ~uintptr_t(3));
+          const uint32_t sh = 8u * static_cast<uint32_t>(ad & 3);
+          uint32_t wd[9];
 #pragma unroll
-        for (int b = 0; b < 32; ++b) v[b] = b < n ? src[b] : 0;
+          for (int k = 0; k < 9; ++k) wd[k] = __ldg(base + k);
+          const uint32_t e4 = 0x01010101u * e;
 #pragma unroll
-        for (int b = 0; b < 32; ++b) word |= static_cast<uint32_t>(v[b] == e) << b;
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t x = __funnelshift_r(wd[j], wd[j + 1], sh) ^ e4;
+            const uint32_t z = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);  // 0x80 where byte == 0
+            word |= (((z >> 7) * 0x10204080u) >> 28) << (4 * j);
+          }
+        } else {
+          uint8_t v[32];
+#pragma unroll
+          for (int b = 0; b < 32; ++b) v[b] = b < n ? src[b] : 0;
+#pragma unroll
+          for (int b = 0; b < 32; ++b) word |= static_cast<uint32_t>(v[b] == e) << b;
+        }
       }
       s_in[i] = word;
     }

@@ -511,7 +511,7 @@ void Net::build() {
       r.idx = prod.idx;
       r.count_slot = prod.count_slot;
     } else {
-      r.outmap_own.alloc(static_cast<size_t>(S_) * HWo);
+      r.outmap_own.alloc(static_cast<size_t>(S_) * HWo + 16);  // +16: dilate_compact's aligned word loads
       r.idx_own.alloc(static_cast<size_t>(S_) * HWo * sizeof(int32_t));
       r.outmap = r.outmap_own.as<uint8_t>();
       r.idx = r.idx_own.as<int32_t>();
@@ -555,7 +555,7 @@ void Net::build() {
       if (d.policy == CBG_POLICY_DETECT) {
         r.state_chw = r.exact && d.inputs[0] < 0;
         r.state.alloc(static_cast<size_t>(S_) * HWi * (r.state_chw ? d.Ci : r.Csi) * sizeof(float));
-        r.inmap.alloc(static_cast<size_t>(S_) * HWi);
+        r.inmap.alloc(static_cast<size_t>(S_) * HWi + 16);
       }
       if (!reuse) {
         if (d.policy == CBG_POLICY_DETECT || d.policy == CBG_POLICY_PROPAGATE)
@@ -565,7 +565,7 @@ void Net::build() {
       // worst-case map buffers (record_worst_case, layers.cpp:108-117)
       if (d.inputs[0] >= 0) {
         dc_tiling(d.Hi, d.Wi, d.H, d.W, c.kernel_h, c.stride, S_, &r.dc_wc_rows, &r.dc_wc_tiles, &r.dc_wc_smem);
-        r.wc_map.alloc(static_cast<size_t>(S_) * HWo);
+        r.wc_map.alloc(static_cast<size_t>(S_) * HWo + 16);
         r.wc_idx.alloc(static_cast<size_t>(S_) * HWo * sizeof(int32_t));
         r.wc_tilestat.alloc(static_cast<size_t>(S_) * r.dc_wc_tiles * 8);
       }
