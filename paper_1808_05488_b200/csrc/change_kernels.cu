@@ -23,6 +23,10 @@ namespace cbg {
 namespace {
 
 constexpr int kThreads = 256;
+// The 4-pixel frame-ingest kernels hold 8 float4 per thread (~80 registers):
+// 128-thread CTAs (10k registers) still fit on an SM beside a resident GEMM
+// CTA of another stream group (672 x 80 of the 64k registers).
+constexpr int kFrameThreads = 128;
 
 int blocks_for(long long work, int per_block, int S, int sm_count) {
   long long b = (work + per_block - 1) / per_block;
@@ -139,7 +143,7 @@ __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs 
 // where a pixel of the 4-pixel group changed. One thread = 4 consecutive
 // pixels (HW % 4 == 0), C <= 4 kept in registers.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(kThreads) detect_frame_chw_kernel(DetectFrameArgs a) {
+__global__ void __launch_bounds__(kFrameThreads) detect_frame_chw_kernel(DetectFrameArgs a) {
   const int s = blockIdx.y;
   const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(kThreads) detect_frame_chw_scalar_kernel(Detec
 // frame; the state is CHW planes (state_chw) or NHWC (Cs == 4). C <= 4.
 // ---------------------------------------------------------------------------
 template <bool kChw>
-__global__ void __launch_bounds__(kThreads) detect_frame_u8_kernel(DetectFrameArgs a) {
+__global__ void __launch_bounds__(kFrameThreads) detect_frame_u8_kernel(DetectFrameArgs a) {
   const int s = blockIdx.y;
   const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
@@ -756,9 +760,9 @@ void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
   const long long HW = static_cast<long long>(a.H) * a.W;
   if (a.x8_slot) {
     if (HW % 4 == 0 && (a.state_chw || a.Cs == 4)) {
-      dim3 grid(blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
-      if (a.state_chw) detect_frame_u8_kernel<true><<<grid, kThreads, 0, st>>>(a);
-      else detect_frame_u8_kernel<false><<<grid, kThreads, 0, st>>>(a);
+      dim3 grid(2 * blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
+      if (a.state_chw) detect_frame_u8_kernel<true><<<grid, kFrameThreads, 0, st>>>(a);
+      else detect_frame_u8_kernel<false><<<grid, kFrameThreads, 0, st>>>(a);
     } else {
       dim3 grid(blocks_for(HW, kThreads, a.S, sm_count()), a.S);
       detect_frame_u8_scalar_kernel<<<grid, kThreads, 0, st>>>(a);
@@ -767,8 +771,8 @@ void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
   }
   if (a.state_chw) {
     if (a.C <= 4 && HW % 4 == 0) {
-      dim3 grid(blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
-      detect_frame_chw_kernel<<<grid, kThreads, 0, st>>>(a);
+      dim3 grid(2 * blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
+      detect_frame_chw_kernel<<<grid, kFrameThreads, 0, st>>>(a);
     } else {
       dim3 grid(blocks_for(HW, kThreads, a.S, sm_count()), a.S);
       detect_frame_chw_scalar_kernel<<<grid, kThreads, 0, st>>>(a);
