@@ -92,7 +92,8 @@ CBG_DEV void exact_row(unsigned long long (&acc)[kPix][G / 2], const float (&xv)
 // the device counts, computed per CTA), split into blocks of kThreads*kPix
 // pixels that the persistent grid strides over, so uneven streams balance.
 template <int G, int KW, bool CHECK, int PS>
-__global__ void __launch_bounds__(kThreads) conv_exact_kernel(ConvExactArgs a) {
+// <= 88 registers: a 128-thread CTA (11k) still fits beside a resident GEMM CTA
+__global__ void __maxnreg__(88) conv_exact_kernel(ConvExactArgs a) {  // launched with kThreads = 128
   extern __shared__ __align__(16) float sw[];  // [K][G] weights of this output group, reference r order
   __shared__ int s_prefix[kMaxStreams + 1];
   const int og = blockIdx.y;  // output-channel group
