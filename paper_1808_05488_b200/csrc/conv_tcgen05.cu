@@ -143,6 +143,31 @@ struct Cfg {
   static_assert(kNAcc * NPAD + kStages * kACols <= 512, "TMEM budget");
 };
 
+CBG_DEV unsigned long long pack_f32x2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+// Two fp32 values -> packed fp16 hi and lo parts of (x * 2^-e), packed fp32x2
+// arithmetic: x*s exact (power of two), hi = fp16_rn, lo = fp16_rn(x*s - hi)
+// (ptxas may fuse the multiply into the subtraction: x*s is exact, so the
+// result is the same).
+CBG_DEV void f16_split2(float x0, float x1, unsigned long long s2, uint32_t& hi, uint32_t& lo) {
+  unsigned long long p;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(pack_f32x2(x0, x1)), "l"(s2));
+  float p0, p1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(p0), "=f"(p1) : "l"(p));
+  const __half2 hh = __floats2half2_rn(p0, p1);
+  const float2 hf = __half22float2(hh);
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(p), "l"(pack_f32x2(hf.x, hf.y)));
+  float d0, d1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+  const __half2 ll = __floats2half2_rn(d0, d1);
+  hi = *reinterpret_cast<const uint32_t*>(&hh);
+  lo = *reinterpret_cast<const uint32_t*>(&ll);
+}
+
 // Exponent e with bound * 2^-e < 2^15 (fp16 operands stay finite), clamped so
 // 2^-e and 2^e are normal floats.
 CBG_DEV int f16_scale_exp(float bound) {
@@ -313,8 +338,11 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       decode(w, s, mt, nt);
       const int cnt = a.count[s];
       const float xs = exp2i(-f16_scale_exp(__ldg(a.amax_in + s)));
+      const unsigned long long xs2 = pack_f32x2(xs, xs);
       // rows (h, b) = 32*quarter + 16*h + 8*b + arow
-      int jb[4], ib[4], roff[4];
+      int jb[4], ib[4];
+      const float* rowp[4];  // the row's receptive-field origin (may point before the image: offsets are added)
+      const float* src = a.src + s * HWin * a.Cs;
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int k = mt * kBM + 32 * quarter + 8 * i + arow;
@@ -322,9 +350,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         const int jo = p / a.Wout, io = p - jo * a.Wout;
         jb[i] = p >= 0 ? jo * a.stride - a.pad : INT_MIN / 2;
         ib[i] = io * a.stride - a.pad;
-        roff[i] = (jb[i] * a.Win + ib[i]) * a.Cs;
+        rowp[i] = src + static_cast<long long>(p >= 0 ? (jb[i] * a.Win + ib[i]) * a.Cs : 0);
       }
-      const float* src = a.src + s * HWin * a.Cs;
       const uint8_t* bimg = a.wimg + static_cast<long long>(nt) * a.KB * 2 * C::kBBytes;
       // rows 2h, 2h+1 of K-block kb -> v[2h..2h+1]
       auto load_half = [&](int kb, int h, float4 (&v)[4][2]) {
@@ -338,7 +365,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
             const int dj = tk.x & 0xFF, di = (tk.x >> 8) & 0xFF;
             const bool ok = (tk.x >> 31) == 0 && static_cast<unsigned>(jb[i] + dj) < static_cast<unsigned>(a.Hin) &&
                             static_cast<unsigned>(ib[i] + di) < static_cast<unsigned>(a.Win);
-            v[i][j] = ok ? ldg_nc_f4(src + (roff[i] + static_cast<int>(tk.y))) : make_float4(0.f, 0.f, 0.f, 0.f);
+            v[i][j] = ok ? ldg_nc_f4(rowp[i] + static_cast<int>(tk.y)) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
       };
@@ -367,15 +394,8 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
 #pragma unroll
             for (int b = 0; b < 2; ++b) {  // row a, a+8 -> registers 0-1 / 2-3 (+4 for chunk c+4)
               const float4 x = v[2 * h + b][j];
-              const float x0 = x.x * xs, x1 = x.y * xs, x2 = x.z * xs, x3 = x.w * xs;
-              const __half2 h01 = __floats2half2_rn(x0, x1), h23 = __floats2half2_rn(x2, x3);
-              const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
-              const __half2 l01 = __floats2half2_rn(x0 - f01.x, x1 - f01.y);
-              const __half2 l23 = __floats2half2_rn(x2 - f23.x, x3 - f23.y);
-              hi[4 * j + 2 * b] = *reinterpret_cast<const uint32_t*>(&h01);
-              hi[4 * j + 2 * b + 1] = *reinterpret_cast<const uint32_t*>(&h23);
-              lo[4 * j + 2 * b] = *reinterpret_cast<const uint32_t*>(&l01);
-              lo[4 * j + 2 * b + 1] = *reinterpret_cast<const uint32_t*>(&l23);
+              f16_split2(x.x, x.y, xs2, hi[4 * j + 2 * b], lo[4 * j + 2 * b]);
+              f16_split2(x.z, x.w, xs2, hi[4 * j + 2 * b + 1], lo[4 * j + 2 * b + 1]);
             }
           tmem_st_16x256b_x2(ta + (static_cast<uint32_t>(16 * h) << 16), hi);
           tmem_st_16x256b_x2(ta + (static_cast<uint32_t>(16 * h) << 16) + C::kALo, lo);
