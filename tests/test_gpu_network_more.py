@@ -287,3 +287,34 @@ def test_many_streams_mixed_activity(gpu):
             want = refs[s].forward(seqs[s][t])
             assert oracle.max_rel_err(net.output(s), want) <= TOL, (t, s)
             assert counts[0, s] == refs[s].stats(0)["changed_px"], (t, s)
+
+
+def test_odd_resolution_scalar_ingest_paths(gpu):
+    """H*W not a multiple of 4: the frame-ingest detect falls back to its scalar
+    kernels (fp32 CHW state and 8-bit PNM ingest); results still match the
+    reference, the first layer bit-exact."""
+    H, W = 63, 85
+    spec = cbi.make_seg_spec(8, H, W)
+    taus = [0.05] * 5
+    raw = cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, 4, 2, 9, 2, 3, 0.01, 33))
+    pnm = cbi.to_pnm8(raw)
+    f32 = cbi.from_pnm8(pnm)
+    a = cbi.convert_to_cb(spec, taus)
+    b = cbi.convert_to_cb(spec, taus)
+    ref = oracle.RefNet(spec, taus)
+    for t in range(len(raw)):
+        a.forward_frame(f32[t])
+        b.forward_frame_u8(pnm[t])
+        want = ref.forward(f32[t])
+        assert np.array_equal(a.output(), b.output())
+        assert np.array_equal(a.node_output(0), ref.output(0))
+        assert oracle.max_rel_err(a.output(), want) <= TOL
+
+
+@pytest.mark.parametrize("direct", ["0", "1"])
+def test_a_operand_paths(gpu, monkeypatch, direct):
+    """Both producers of the tcgen05 A operand (direct global->TMEM, the default;
+    shared-memory staging with fetch warps, CBG_GEMM_DIRECT=0) on the seg net."""
+    monkeypatch.setenv("CBG_GEMM_DIRECT", direct)
+    spec = cbi.make_seg_spec(9, 80, 112)
+    run_pair(spec, [0.05] * 5, frames_for(80, 112, noise=0.003))
