@@ -7,6 +7,9 @@
 #include <cuda_runtime.h>
 
 #define CBG_DEV __device__ __forceinline__
+#ifndef CBG_MBAR_SUSPEND_NS
+#define CBG_MBAR_SUSPEND_NS 20000
+#endif
 
 namespace cbg {
 
@@ -58,14 +61,17 @@ CBG_DEV void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
                "r"(bytes)
                : "memory");
 }
+// The suspend-time hint lets a waiting warp sleep in try_wait (woken when the
+// phase completes) instead of re-issuing the probe: many role warps of the GEMM
+// wait most of the time, and their spinning took issue slots from the others.
 CBG_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
       "@!p bra WAIT_%=;\n\t}" ::"r"(a),
-      "r"(parity)
+      "r"(parity), "n"(CBG_MBAR_SUSPEND_NS)
       : "memory");
 }
 // Make generic-proxy shared-memory writes visible to the async proxy (UMMA reads).
