@@ -28,8 +28,8 @@ for k, x in zip(h, v):
     if k in ("dram__bytes_read.sum", "dram__bytes_write.sum", "sm__inst_executed.sum", "smsp__inst_executed.sum",
              "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
              "sm__inst_executed_pipe_lsu.avg.pct_of_peak_sustained_active",
-             "TPC.TriageCompute.sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
              "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed",
+             "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
              "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
              "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
              "sm__inst_executed_pipe_tmem.avg.pct_of_peak_sustained_active"):
