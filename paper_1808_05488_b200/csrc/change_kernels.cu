@@ -361,6 +361,9 @@ __global__ void __launch_bounds__(kThreads) detect_frame_u8_scalar_kernel(Detect
 // detect on NHWC inputs. A group of g lanes handles one pixel (g float4 per
 // step); the group's verdict is reduced with a warp ballot.
 // ---------------------------------------------------------------------------
+// kCache = float4 of x each lane keeps in registers for the state write
+// (ceil(Cs/4 / g), 1, 2 or 4; wider pixels re-read the rest)
+template <int kCache>
 __global__ void __launch_bounds__(kThreads) detect_list_kernel(DetectListArgs a, int glog) {
   const int s = blockIdx.y;
   const uint8_t e = epoch8(*a.frame);
@@ -392,20 +395,46 @@ __global__ void __launch_bounds__(kThreads) detect_list_kernel(DetectListArgs a,
     if (active) p = list ? list[k] : k;
     const float* xp = x + p * a.Cs;
     float* sp = st + p * a.Cs;
+    // up to kCache float4 of x per lane stay in registers for the state write;
+    // all loads are issued before the comparisons
+    float4 xc[kCache];
     bool changed = false;
-    if (active && !boot) {
-      for (int v = sub; v < nv; v += g) {
-        const float4 xv = ldg_nc_f4(xp + 4 * v);
-        const float4 sv = *reinterpret_cast<const float4*>(sp + 4 * v);
-        changed |= fabsf(xv.x - sv.x) > tau;
-        changed |= fabsf(xv.y - sv.y) > tau;
-        changed |= fabsf(xv.z - sv.z) > tau;
-        changed |= fabsf(xv.w - sv.w) > tau;
+    if (active) {
+      float4 sc[kCache];
+#pragma unroll
+      for (int j = 0; j < kCache; ++j) {
+        const int v = sub + j * g;
+        if (v < nv) {
+          xc[j] = ldg_nc_f4(xp + 4 * v);
+          if (!boot) sc[j] = *reinterpret_cast<const float4*>(sp + 4 * v);
+        }
+      }
+      if (!boot) {
+#pragma unroll
+        for (int j = 0; j < kCache; ++j) {
+          if (sub + j * g < nv) {
+            changed |= fabsf(xc[j].x - sc[j].x) > tau;
+            changed |= fabsf(xc[j].y - sc[j].y) > tau;
+            changed |= fabsf(xc[j].z - sc[j].z) > tau;
+            changed |= fabsf(xc[j].w - sc[j].w) > tau;
+          }
+        }
+        for (int v = sub + kCache * g; v < nv; v += g) {  // wide pixels beyond the cache
+          const float4 xv = ldg_nc_f4(xp + 4 * v);
+          const float4 sv = *reinterpret_cast<const float4*>(sp + 4 * v);
+          changed |= fabsf(xv.x - sv.x) > tau;
+          changed |= fabsf(xv.y - sv.y) > tau;
+          changed |= fabsf(xv.z - sv.z) > tau;
+          changed |= fabsf(xv.w - sv.w) > tau;
+        }
       }
     }
     const bool any = (__ballot_sync(0xffffffffu, changed) & gmask) != 0;
     if (active && (any || write_all)) {
-      for (int v = sub; v < nv; v += g)
+#pragma unroll
+      for (int j = 0; j < kCache; ++j)
+        if (sub + j * g < nv) *reinterpret_cast<float4*>(sp + 4 * (sub + j * g)) = xc[j];
+      for (int v = sub + kCache * g; v < nv; v += g)
         *reinterpret_cast<float4*>(sp + 4 * v) = ldg_nc_f4(xp + 4 * v);
     }
     if (active && any && !boot && sub == 0) m[p] = e;
@@ -791,7 +820,10 @@ void launch_detect_list(const DetectListArgs& a, cudaStream_t st) {
   const long long HW = static_cast<long long>(a.H) * a.W;
   const int px_per_block = (kThreads >> glog);
   dim3 grid(blocks_for(HW, px_per_block, a.S, sm_count()), a.S);
-  detect_list_kernel<<<grid, kThreads, 0, st>>>(a, glog);
+  const int per_lane = (a.Cs / 4 + (1 << glog) - 1) >> glog;
+  if (per_lane <= 1) detect_list_kernel<1><<<grid, kThreads, 0, st>>>(a, glog);
+  else if (per_lane <= 2) detect_list_kernel<2><<<grid, kThreads, 0, st>>>(a, glog);
+  else detect_list_kernel<4><<<grid, kThreads, 0, st>>>(a, glog);
 }
 
 int dilate_compact_smem(int Win, int Wout, int rows_per_tile, int kh, int stride) {
