@@ -698,6 +698,25 @@ __global__ void __launch_bounds__(kThreads) pool_kernel(PoolArgs a, int glog) {
     const int jo = p / a.Wout, io = p - jo * a.Wout;
     const int j0 = jo * a.stride, i0 = io * a.stride;
     const int j1 = min(j0 + a.size, a.Hin), i1 = min(i0 + a.size, a.Win);
+    if (j1 - j0 == 2 && i1 - i0 == 2) {  // full 2x2 window: the four loads in flight together
+      const float* q0 = x + (static_cast<long long>(j0) * a.Win + i0) * a.Cs;
+      const float* q1 = q0 + static_cast<long long>(a.Win) * a.Cs;
+      for (int v = sub; v < nv; v += g) {
+        const float4 u00 = ldg_nc_f4(q0 + 4 * v), u01 = ldg_nc_f4(q0 + a.Cs + 4 * v);
+        const float4 u10 = ldg_nc_f4(q1 + 4 * v), u11 = ldg_nc_f4(q1 + a.Cs + 4 * v);
+        float4 m = u00;  // the reference's order: start at (j0, i0), then the window row-major
+        const float4* us[4] = {&u00, &u01, &u10, &u11};
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          m.x = ref_max(m.x, us[t]->x);
+          m.y = ref_max(m.y, us[t]->y);
+          m.z = ref_max(m.z, us[t]->z);
+          m.w = ref_max(m.w, us[t]->w);
+        }
+        *reinterpret_cast<float4*>(y + static_cast<long long>(p) * a.Cs + 4 * v) = m;
+      }
+      continue;
+    }
     for (int v = sub; v < nv; v += g) {
       float4 m = ldg_nc_f4(x + (static_cast<long long>(j0) * a.Win + i0) * a.Cs + 4 * v);
       for (int j = j0; j < j1; ++j)
