@@ -343,6 +343,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       int jb[4], ib[4];
       const float* rowp[4];  // the row's receptive-field origin (may point before the image: offsets are added)
       const float* src = a.src + s * HWin * a.Cs;
+      bool inside = true;    // all four rows valid with their whole window inside the image
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int k = mt * kBM + 32 * quarter + 8 * i + arow;
@@ -351,7 +352,10 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         jb[i] = p >= 0 ? jo * a.stride - a.pad : INT_MIN / 2;
         ib[i] = io * a.stride - a.pad;
         rowp[i] = src + static_cast<long long>(p >= 0 ? (jb[i] * a.Win + ib[i]) * a.Cs : 0);
+        inside = inside && p >= 0 && jb[i] >= 0 && jb[i] + a.kh <= a.Hin && ib[i] >= 0 && ib[i] + a.kw <= a.Win;
       }
+      // warp-uniform: the whole warp takes the unchecked loads or none of it
+      const bool fast = __all_sync(0xffffffffu, inside);
       const uint8_t* bimg = a.wimg + static_cast<long long>(nt) * a.KB * 2 * C::kBBytes;
       // rows 2h, 2h+1 of K-block kb -> v[2h..2h+1]
       auto load_half = [&](int kb, int h, float4 (&v)[4][2]) {
@@ -362,24 +366,30 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
 #pragma unroll
           for (int j = 0; j < 2; ++j) {
             const uint2 tk = j ? t1 : t0;
-            const int dj = tk.x & 0xFF, di = (tk.x >> 8) & 0xFF;
-            const bool ok = (tk.x >> 31) == 0 && static_cast<unsigned>(jb[i] + dj) < static_cast<unsigned>(a.Hin) &&
-                            static_cast<unsigned>(ib[i] + di) < static_cast<unsigned>(a.Win);
+            bool ok = (tk.x >> 31) == 0;  // K padding
+            if (!fast) {
+              const int dj = tk.x & 0xFF, di = (tk.x >> 8) & 0xFF;
+              ok = ok && static_cast<unsigned>(jb[i] + dj) < static_cast<unsigned>(a.Hin) &&
+                   static_cast<unsigned>(ib[i] + di) < static_cast<unsigned>(a.Win);
+            }
             v[i][j] = ok ? ldg_nc_f4(rowp[i] + static_cast<int>(tk.y)) : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
       };
+      const uint32_t g0 = g;  // K-block counter at the tile's start; this group's first is kb0
+      const int kb0 = static_cast<int>((grp + G - g0 % G) % G);
+      g = g0 + a.KB;
 #pragma unroll 1
-      for (int kb = 0; kb < a.KB; ++kb, ++g) {
-        if (static_cast<int>(g % G) != grp) continue;
-        const int stage = g % C::kStages;
-        const uint32_t phase = (g / C::kStages) & 1;
+      for (int kb = kb0; kb < a.KB; kb += G) {
+        const uint32_t gk = g0 + kb;
+        const int stage = gk % C::kStages;
+        const uint32_t phase = (gk / C::kStages) & 1;
         float4 v[4][2];
         load_half(kb, 0, v);  // loads first: they do not depend on the stage being free
         load_half(kb, 1, v);
         mbar_wait(&empty[stage], phase ^ 1);  // TMEM A stage and B smem free
         if (leader) {
-          TRACE(4, g);
+          TRACE(4, gk);
           mbar_arrive_expect_tx(&full[stage], 2 * C::kBBytes);
           bulk_g2s(smem + stage * C::kStageBytes, bimg + static_cast<long long>(kb) * 2 * C::kBBytes,
                    2 * C::kBBytes, &full[stage]);
@@ -404,7 +414,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&full[stage]);
-        if (leader) TRACE(5, g);
+        if (leader) TRACE(5, gk);
       }
     }
   } else if (warp >= R::kFirstConvWarp && warp < R::kMmaWarp) {

@@ -111,6 +111,7 @@ struct ConvGemmArgs {
   const float* bias;       // [n_tiles*NPAD]
   int Cs, Hin, Win, Hout, Wout, Co4;
   int stride, pad;
+  int kh, kw;              // kernel extent (rows whose whole window is inside the image skip the bounds checks)
   int KB;                  // K blocks of 32 fp32
   int npad;                // N tile: 16, 32, 64, 128 or 256
   int n_tiles;             // ceil(Co4 / npad)

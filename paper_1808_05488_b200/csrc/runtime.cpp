@@ -752,6 +752,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast) {
       g.bias = r.bias.as<float>();
       g.Cs = r.Csi, g.Hin = d.Hi, g.Win = d.Wi, g.Hout = d.H, g.Wout = d.W, g.Co4 = r.Cs;
       g.stride = c.stride, g.pad = c.padding;
+      g.kh = c.kernel_h, g.kw = c.kernel_w;
       g.KB = r.KB, g.npad = r.npad, g.n_tiles = r.n_tiles;
       g.relu = d.relu;
       g.S = S_;
