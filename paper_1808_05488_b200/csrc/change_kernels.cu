@@ -364,7 +364,7 @@ __global__ void __launch_bounds__(kThreads) detect_frame_u8_scalar_kernel(Detect
 // kCache = float4 of x each lane keeps in registers for the state write
 // (ceil(Cs/4 / g), 1, 2 or 4; wider pixels re-read the rest)
 template <int kCache>
-__global__ void __launch_bounds__(kThreads) detect_list_kernel(DetectListArgs a, int glog) {
+__global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListArgs a, int glog) {
   const int s = blockIdx.y;
   const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
@@ -506,7 +506,8 @@ CBG_DEV uint32_t even_bits(uint32_t lo, uint32_t hi) {
 // word, built with warp ballots), dilated separably in the bit domain
 // (horizontal: funnel-shift ORs, vertical: word ORs), counted with popc and
 // compacted in row-major order with a single-pass decoupled look-back.
-__global__ void __launch_bounds__(kThreads) dilate_compact_kernel(DilateCompactArgs a) {
+// <= 40 registers: a 256-thread CTA fits beside a persistent GEMM CTA (672 x 80)
+__global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompactArgs a) {
   extern __shared__ __align__(16) uint32_t smw[];
   __shared__ int s_warp[33];
   __shared__ int s_prefix;
@@ -680,7 +681,7 @@ __global__ void __launch_bounds__(kThreads) dilate_compact_kernel(DilateCompactA
 // ---------------------------------------------------------------------------
 __device__ __forceinline__ float ref_max(float m, float v) { return (m < v) ? v : m; }
 
-__global__ void __launch_bounds__(kThreads) pool_kernel(PoolArgs a, int glog) {
+__global__ void __launch_bounds__(kFrameThreads) pool_kernel(PoolArgs a, int glog) {
   const int s = blockIdx.y;
   const long long n = a.count[s];
   const long long HWi = static_cast<long long>(a.Hin) * a.Win;
@@ -837,12 +838,12 @@ void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
 void launch_detect_list(const DetectListArgs& a, cudaStream_t st) {
   const int glog = group_log2(a.Cs);
   const long long HW = static_cast<long long>(a.H) * a.W;
-  const int px_per_block = (kThreads >> glog);
-  dim3 grid(blocks_for(HW, px_per_block, a.S, sm_count()), a.S);
+  // 128-thread CTAs (<= 88 registers) co-reside with a persistent GEMM CTA
+  dim3 grid(2 * blocks_for(HW, kThreads >> glog, a.S, sm_count()), a.S);
   const int per_lane = (a.Cs / 4 + (1 << glog) - 1) >> glog;
-  if (per_lane <= 1) detect_list_kernel<1><<<grid, kThreads, 0, st>>>(a, glog);
-  else if (per_lane <= 2) detect_list_kernel<2><<<grid, kThreads, 0, st>>>(a, glog);
-  else detect_list_kernel<4><<<grid, kThreads, 0, st>>>(a, glog);
+  if (per_lane <= 1) detect_list_kernel<1><<<grid, kFrameThreads, 0, st>>>(a, glog);
+  else if (per_lane <= 2) detect_list_kernel<2><<<grid, kFrameThreads, 0, st>>>(a, glog);
+  else detect_list_kernel<4><<<grid, kFrameThreads, 0, st>>>(a, glog);
 }
 
 int dilate_compact_smem(int Win, int Wout, int rows_per_tile, int kh, int stride) {
@@ -859,8 +860,8 @@ void launch_dilate_compact(const DilateCompactArgs& a, cudaStream_t st) {
 void launch_pool(const PoolArgs& a, cudaStream_t st) {
   const int glog = group_log2(a.Cs);
   const long long HWo = static_cast<long long>(a.Hout) * a.Wout;
-  dim3 grid(blocks_for(HWo, kThreads >> glog, a.S, sm_count()), a.S);
-  pool_kernel<<<grid, kThreads, 0, st>>>(a, glog);
+  dim3 grid(2 * blocks_for(HWo, kThreads >> glog, a.S, sm_count()), a.S);
+  pool_kernel<<<grid, kFrameThreads, 0, st>>>(a, glog);
 }
 
 void launch_join(const JoinArgs& a, cudaStream_t st) {
