@@ -347,7 +347,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int k = mt * kBM + 32 * quarter + 8 * i + arow;
-        const int p = k < cnt ? __ldg(a.idx + s * HWout + k) : -1;
+        // the list load does not wait for the count (rows past it are masked after)
+        const int pr = __ldg(a.idx + s * HWout + min(k, static_cast<int>(HWout) - 1));
+        const int p = k < cnt ? pr : -1;
         const int jo = p / a.Wout, io = p - jo * a.Wout;
         jb[i] = p >= 0 ? jo * a.stride - a.pad : INT_MIN / 2;
         ib[i] = io * a.stride - a.pad;

@@ -468,6 +468,14 @@ Net::Net(Ctx* ctx, Topology topo, int n_streams) : ctx_(ctx), topo_(std::move(to
 Net::~Net() {
   for (auto& g : graphs_) cudaGraphExecDestroy(g.second);
   for (auto& e : ev_pool_) cudaEventDestroy(e);
+  for (int b = 0; b < 2; ++b) {
+    if (ev_copied_[b]) cudaEventDestroy(ev_copied_[b]);
+    if (ev_consumed_[b]) cudaEventDestroy(ev_consumed_[b]);
+  }
+  if (copy_st_) {
+    cudaStreamSynchronize(copy_st_);
+    cudaStreamDestroy(copy_st_);
+  }
 }
 
 std::unique_ptr<Net> Net::clone() const {
@@ -633,7 +641,7 @@ int Net::launch_count(unsigned flags) const {
   return k;
 }
 
-void Net::enqueue_frame(unsigned flags, bool u8, bool bcast) {
+void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
   cudaStream_t st = ctx_->stream;
   int32_t* counts = counts_.as<int32_t>();
   const uint32_t* frame = frame_ctr_.as<uint32_t>();
@@ -658,7 +666,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast) {
           DetectFrameArgs a{frame_slot_.as<const float*>(), r.state.as<float>(), r.inmap.as<uint8_t>(), frame, boot,
                             d.Ci, r.Csi, d.Hi, d.Wi, S_, taus_.as<float>() + static_cast<size_t>(i) * S_,
                             topo_.mode == CBG_MODE_CLOSEDLOOP, r.state_chw, amax_entry(-1),
-                            u8 ? frame8_slot_.as<const uint8_t*>() : nullptr,
+                            u8 ? frame8_slot_.as<const uint8_t*>() + slot8 : nullptr,
                             bcast ? 0LL : static_cast<long long>(d.Ci) * d.Hi * d.Wi};
           timed(d.name + ".detect", [&] { launch_detect_frame(a, st); });
         } else {
@@ -846,19 +854,38 @@ void Net::forward_u8(const uint8_t* frames, unsigned flags) {
   for (const NodeRT& r : nodes_)
     if (r.d.kind == CBG_LAYER_CONV && r.d.inputs[0] < 0 && r.d.policy == CBG_POLICY_DETECT) first_detect = true;
   if (!first_detect) throw Error(CBG_ERR_UNSUPPORTED, "8-bit ingest needs a detect-policy first layer");
+  const size_t fbytes = static_cast<size_t>(S_) * topo_.H * topo_.W * topo_.C;
   if (!frame8_.bytes) {
-    frame8_.alloc(static_cast<size_t>(S_) * topo_.H * topo_.W * topo_.C);
-    frame8_slot_.alloc(sizeof(void*));
+    frame8_.alloc(2 * fbytes);
+    frame8_slot_.alloc(3 * sizeof(void*));
+    const uint8_t* v[3] = {frame8_.as<uint8_t>(), frame8_.as<uint8_t>() + fbytes, nullptr};
+    CK(cudaMemcpy(frame8_slot_.p, v, sizeof(v), cudaMemcpyHostToDevice));
+    CK(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaEventCreateWithFlags(&ev_copied_[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_consumed_[b], cudaEventDisableTiming));
+    }
   }
-  const uint8_t* want = (flags & CBG_FWD_INPUT_ON_DEVICE) ? frames : frame8_.as<uint8_t>();
-  if (want != slot8_value_) {
-    const uint8_t* v = want;
-    CK(cudaMemcpyAsync(frame8_slot_.p, &v, sizeof(v), cudaMemcpyHostToDevice, st));
-    slot8_value_ = want;
+  const unsigned key = (flags & CBG_FWD_RECORD_WORST_CASE) | (1u << 31);
+  if (flags & CBG_FWD_INPUT_ON_DEVICE) {
+    if (frames != slot8_value_) {
+      const uint8_t* v = frames;  // pageable source: consumed before cudaMemcpyAsync returns
+      CK(cudaMemcpyAsync(frame8_slot_.as<const uint8_t*>() + 2, &v, sizeof(v), cudaMemcpyHostToDevice, st));
+      slot8_value_ = frames;
+    }
+    run_frame(flags, key | (2u << 28));
+    return;
   }
-  if (!(flags & CBG_FWD_INPUT_ON_DEVICE))
-    CK(cudaMemcpyAsync(frame8_.p, frames, frame8_.bytes, cudaMemcpyHostToDevice, st));
-  run_frame(flags, (flags & CBG_FWD_RECORD_WORST_CASE) | (1u << 31));
+  // host frames: H2D into buffer b on the copy stream once the frame that last
+  // read b (two calls ago) is done, so the copy overlaps the previous frame
+  const int b = u8_buf_;
+  u8_buf_ ^= 1;
+  CK(cudaStreamWaitEvent(copy_st_, ev_consumed_[b], 0));
+  CK(cudaMemcpyAsync(frame8_.as<uint8_t>() + b * fbytes, frames, fbytes, cudaMemcpyHostToDevice, copy_st_));
+  CK(cudaEventRecord(ev_copied_[b], copy_st_));
+  CK(cudaStreamWaitEvent(st, ev_copied_[b], 0));
+  run_frame(flags, key | (static_cast<unsigned>(b) << 28));
+  CK(cudaEventRecord(ev_consumed_[b], st));
 }
 
 // One frame step: bookkeeping, then the captured graph for this flag set
@@ -871,10 +898,11 @@ void Net::run_frame(unsigned flags, unsigned graph_key) {
   const unsigned gflags = flags & CBG_FWD_RECORD_WORST_CASE;
   const bool u8 = (graph_key >> 31) != 0;
   const bool bcast = ((graph_key >> 30) & 1u) != 0;
+  const int slot8 = static_cast<int>((graph_key >> 28) & 3u);
   last_flags_ = flags;
   last_launches_ = launch_count(gflags);
   if (timing_) {
-    enqueue_frame(gflags, u8, bcast);
+    enqueue_frame(gflags, u8, bcast, slot8);
     CK(cudaStreamSynchronize(st));
     size_t k = 0;
     for (auto& p : pending_) {
@@ -896,7 +924,7 @@ void Net::run_frame(unsigned flags, unsigned graph_key) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     try {
-      enqueue_frame(gflags, u8, bcast);
+      enqueue_frame(gflags, u8, bcast, slot8);
     } catch (...) {
       cudaStreamEndCapture(st, &g);
       throw;

@@ -152,7 +152,8 @@ class Net {
 
  private:
   void build();
-  void enqueue_frame(unsigned flags, bool u8 = false, bool bcast = false);  // kernels of one frame (graph body)
+  // kernels of one frame (graph body); slot8 = which 8-bit ingest pointer slot the first detect reads
+  void enqueue_frame(unsigned flags, bool u8 = false, bool bcast = false, int slot8 = 0);
   int launch_count(unsigned flags) const;
   void clear_maps();
 
@@ -165,8 +166,14 @@ class Net {
   // running max |value| per stream: entry 0 = network input (state of the first
   // layer), entry i+1 = node i's output; the fp16 GEMM scales come from these
   DevBuf amax_;
-  DevBuf frame8_, frame8_slot_;        // 8-bit ingest: staging + device pointer slot
-  const uint8_t* slot8_value_ = nullptr;
+  // 8-bit ingest: two staging buffers filled on a copy stream while the other
+  // one is being consumed, and three device pointer slots (buffer 0, buffer 1,
+  // caller's device pointer) the first detect reads through
+  DevBuf frame8_, frame8_slot_;
+  const uint8_t* slot8_value_ = nullptr;  // host mirror of slot 2
+  cudaStream_t copy_st_ = nullptr;
+  cudaEvent_t ev_copied_[2] = {nullptr, nullptr}, ev_consumed_[2] = {nullptr, nullptr};
+  int u8_buf_ = 0;
   void upload_taus(const std::vector<uint8_t>& rescan);
   void run_frame(unsigned flags, unsigned graph_key);
   float* amax_entry(int node) const { return amax_.as<float>() + static_cast<size_t>(node + 1) * S_; }
