@@ -5,8 +5,8 @@
 //   detect_list     the same on NHWC inputs, walking only the producer's
 //                   update set                      ref change.cpp:20-43
 //   dilate_compact  window dilation of (OR-ed) change maps fused with the
-//                   ordered stream compaction into the row-major index list
-//                   (single pass, decoupled look-back)
+//                   stream compaction into the index list (row-major runs
+//                   per tile, one atomic offset per tile)
 //                                                   ref change.cpp:45-84
 //   pool            change-based max pooling       ref layers.cpp:148-179
 //   join            Add / Concat at changed pixels  ref network.cpp:364-398
@@ -470,16 +470,6 @@ __device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int& tot
   return s_warp[warp] + inc - v;
 }
 
-constexpr uint64_t kFlagAgg = 1ull << 30;
-constexpr uint64_t kFlagInc = 2ull << 30;
-constexpr uint64_t kValMask = (1ull << 30) - 1;
-
-CBG_DEV uint64_t ld_relaxed_u64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
 // 32 bits of a bit-row starting at bit position B (bits outside [0, 32*nw) are 0).
 CBG_DEV uint32_t bits_at(const uint32_t* row, int nw, int B) {
   const int w = B >> 5, o = B & 31;  // arithmetic shift: floor for negative B
@@ -502,10 +492,22 @@ CBG_DEV uint32_t even_bits(uint32_t lo, uint32_t hi) {
   return squeeze(lo) | (squeeze(hi) << 16);
 }
 
+#ifdef CBG_DCTRACE
+#define DCT_DECL long long dct_t[8] = {0}; const long long dct_s = clock64()
+#define DCT(i) dct_t[i] = clock64() - dct_s
+#define DCT_PRINT if (threadIdx.x == 0 && (blockIdx.x == 5 || blockIdx.x == 15) && blockIdx.y < 2) \
+  printf("DCT %d %d n_tiles %d: %lld %lld %lld %lld %lld %lld %lld\n", blockIdx.x, blockIdx.y, a.n_tiles, dct_t[0], \
+         dct_t[1], dct_t[2], dct_t[3], dct_t[4], dct_t[5], dct_t[6])
+#else
+#define DCT_DECL do { } while (0)
+#define DCT(i) do { } while (0)
+#define DCT_PRINT do { } while (0)
+#endif
+
 // Tile = rows_per_tile output rows. Maps are staged as bit-rows (32 pixels per
 // word, built with warp ballots), dilated separably in the bit domain
 // (horizontal: funnel-shift ORs, vertical: word ORs), counted with popc and
-// compacted in row-major order with a single-pass decoupled look-back.
+// compacted: row-major inside the tile, tiles placed by one atomicAdd each.
 // <= 40 registers: a 256-thread CTA fits beside a persistent GEMM CTA (672 x 80)
 __global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompactArgs a) {
   extern __shared__ __align__(16) uint32_t smw[];
@@ -513,9 +515,11 @@ __global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompa
   __shared__ int s_prefix;
   const int s = blockIdx.y, t = blockIdx.x;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  DCT_DECL;
   const uint32_t f = *a.frame;
   const uint8_t e = epoch8(f);
   const bool boot = a.boot[s] != 0;
+  DCT(0);
   const int r0 = t * a.rows_per_tile;
   const int r1 = min(r0 + a.rows_per_tile, a.Hout);
   const int nrows = r1 - r0;
@@ -573,6 +577,7 @@ __global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompa
       s_in[i] = word;
     }
     __syncthreads();
+  DCT(1);
     // 2. horizontal dilation (+ stride subsampling) per staged row
     for (int i = threadIdx.x; i < nin * nwo; i += blockDim.x) {
       const int r = i / nwo, wo = i - r * nwo;
@@ -604,6 +609,7 @@ __global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompa
       s_h[i] = v;
     }
     __syncthreads();
+  DCT(2);
     // 3. vertical dilation
     for (int i = threadIdx.x; i < nout; i += blockDim.x) {
       const int rr = i / nwo, wo = i - rr * nwo;
@@ -615,6 +621,7 @@ __global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompa
     }
   }
   __syncthreads();
+  DCT(3);
 
   // 4. count (contiguous run of words per thread) + block scan
   const int per = (nout + blockDim.x - 1) / blockDim.x;
@@ -623,41 +630,15 @@ __global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompa
   for (int i = w0; i < w1; ++i) mine += __popc(s_out[i]);
   int agg = 0;
   const int off = block_exclusive_scan(mine, s_warp, agg);
+  DCT(4);
 
-  // 5. decoupled look-back (one warp, 32 predecessors per step). The status
-  //    word carries its value, so relaxed polling suffices (no L1 invalidation).
-  uint64_t* stat = a.tile_status + static_cast<long long>(s) * a.n_tiles;
-  const uint64_t tag = static_cast<uint64_t>(f) << 32;
-  if (warp == 0) {
-    int prefix = 0;
-    if (t == 0) {
-      if (lane == 0) st_release_u64(&stat[0], tag | kFlagInc | static_cast<uint64_t>(agg));
-    } else {
-      if (lane == 0) st_release_u64(&stat[t], tag | kFlagAgg | static_cast<uint64_t>(agg));
-      for (int j = t - 1;; j -= 32) {
-        const int q = j - lane;
-        uint64_t v = 0;
-        if (q >= 0) {
-          do {
-            v = ld_relaxed_u64(&stat[q]);
-          } while ((v >> 32) != f);
-        }
-        const unsigned inc = __ballot_sync(0xffffffffu, q >= 0 && (v & kFlagInc) == kFlagInc);
-        int val = q >= 0 ? static_cast<int>(v & kValMask) : 0;
-        if (inc) val = lane <= (__ffs(inc) - 1) ? val : 0;  // up to the nearest inclusive predecessor
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
-        prefix += val;
-        if (inc) break;  // tile 0 is always inclusive, so this terminates
-      }
-      if (lane == 0) st_release_u64(&stat[t], tag | kFlagInc | static_cast<uint64_t>(prefix + agg));
-    }
-    if (lane == 0) {
-      s_prefix = prefix;
-      if (t == a.n_tiles - 1) a.count[s] = prefix + agg;
-    }
-  }
+  // 5. the tile's place in the list: one atomicAdd per tile. Tiles land in
+  //    completion order, each one a row-major run (readers that expose the
+  //    list sort it, Net::read_changes); no tile waits for its predecessors.
+  int32_t* ctr = a.tile_ctr + 2 * s;
+  if (threadIdx.x == 0) s_prefix = agg ? atomicAdd(ctr, agg) : 0;
   __syncthreads();
+  DCT(5);
 
   // 6. scatter the row-major index list and tag the output map
   int pos = s_prefix + off;
@@ -674,6 +655,13 @@ __global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompa
       om[base + b] = e;
     }
   }
+  // the last tile of the stream publishes the count (consumers are later kernels)
+  if (threadIdx.x == 0) {
+    __threadfence();
+    if (atomicAdd(ctr + 1, 1) == a.n_tiles - 1) a.count[s] = atomicAdd(ctr, 0);
+  }
+  DCT(6);
+  DCT_PRINT;
 }
 
 // ---------------------------------------------------------------------------
@@ -777,6 +765,7 @@ __global__ void begin_frame_kernel(BeginFrameArgs a) {
     a.rescan_now[i] = a.rescan_req[i];
     a.rescan_req[i] = 0;
   }
+  for (int i = threadIdx.x; i < a.n_dc_ctr; i += blockDim.x) a.dc_ctr[i] = 0;
   if (threadIdx.x == 0) *a.frame += 1u;
 }
 

@@ -28,15 +28,6 @@ CBG_DEV void warp_amax(float* dst, float v) {
   if ((threadIdx.x & 31) == 0 && dst != nullptr && v > 0.0f) atomicMax(reinterpret_cast<int*>(dst), __float_as_int(v));
 }
 
-// ---- global acquire / release --------------------------------------------------
-CBG_DEV uint64_t ld_acquire_u64(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-CBG_DEV void st_release_u64(uint64_t* p, uint64_t v) {
-  asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
 CBG_DEV float4 ldg_nc_f4(const float* p) {
   float4 r;
   asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"

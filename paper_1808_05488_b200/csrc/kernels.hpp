@@ -63,7 +63,7 @@ struct DilateCompactArgs {
   uint8_t* out_map;          // [S][Hout][Wout] epoch-tagged
   int32_t* idx;              // [S][Hout*Wout]
   int32_t* count;            // [S]
-  uint64_t* tile_status;     // [S][n_tiles] look-back state
+  int32_t* tile_ctr;         // [S][2] (list offset, tiles done), zeroed by begin_frame
   const uint32_t* frame;
   const uint8_t* boot;
   int Hin, Win, Hout, Wout, kh, kw, stride, pad;
@@ -160,6 +160,8 @@ struct BeginFrameArgs {
   const uint8_t* dense;  // device flag: every frame is a full update
   uint8_t* rescan_now;   // [n_nodes] out: dense re-detection after a tau change
   uint8_t* rescan_req;   // [n_nodes] in, cleared
+  int32_t* dc_ctr;       // compaction counters of every node, zeroed
+  int n_dc_ctr;
   int S, n_nodes;
 };
 void launch_begin_frame(const BeginFrameArgs& a, cudaStream_t st);

@@ -568,22 +568,18 @@ void Net::build() {
       if (!reuse) {
         if (d.policy == CBG_POLICY_DETECT || d.policy == CBG_POLICY_PROPAGATE)
           dc_tiling(d.Hi, d.Wi, d.H, d.W, c.kernel_h, c.stride, S_, &r.dc_rows, &r.dc_tiles, &r.dc_smem);
-        r.tilestat.alloc(static_cast<size_t>(S_) * r.dc_tiles * 8);
       }
       // worst-case map buffers (record_worst_case, layers.cpp:108-117)
       if (d.inputs[0] >= 0) {
         dc_tiling(d.Hi, d.Wi, d.H, d.W, c.kernel_h, c.stride, S_, &r.dc_wc_rows, &r.dc_wc_tiles, &r.dc_wc_smem);
         r.wc_map.alloc(static_cast<size_t>(S_) * HWo + 16);
         r.wc_idx.alloc(static_cast<size_t>(S_) * HWo * sizeof(int32_t));
-        r.wc_tilestat.alloc(static_cast<size_t>(S_) * r.dc_wc_tiles * 8);
       }
       r.wc_slot = n_slots_++;
     } else if (d.kind == CBG_LAYER_POOL) {
       dc_tiling(d.Hi, d.Wi, d.H, d.W, d.pool_size, d.pool_stride, S_, &r.dc_rows, &r.dc_tiles, &r.dc_smem);
-      r.tilestat.alloc(static_cast<size_t>(S_) * r.dc_tiles * 8);
     } else {  // joins: OR of the parents' maps, 1x1 identity window
       dc_tiling(d.H, d.W, d.H, d.W, 1, 1, S_, &r.dc_rows, &r.dc_tiles, &r.dc_smem);
-      r.tilestat.alloc(static_cast<size_t>(S_) * r.dc_tiles * 8);
     }
   }
   frame_.alloc(static_cast<size_t>(S_) * topo_.C * topo_.H * topo_.W * sizeof(float));
@@ -594,6 +590,7 @@ void Net::build() {
     slot_value_ = p;
   }
   frame_ctr_.alloc(4);
+  dc_ctr_.alloc(nodes_.size() * 2 * S_ * 2 * sizeof(int32_t));
   boot_req_.alloc(S_);
   CK(cudaMemset(boot_req_.p, 1, S_));
   boot_now_.alloc(S_);
@@ -649,7 +646,8 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
   const int n = static_cast<int>(nodes_.size());
   {
     BeginFrameArgs b{frame_ctr_.as<uint32_t>(), boot_now_.as<uint8_t>(), boot_req_.as<uint8_t>(),
-                     dense_flag_.as<uint8_t>(), rescan_now_.as<uint8_t>(), rescan_req_.as<uint8_t>(), S_, n};
+                     dense_flag_.as<uint8_t>(), rescan_now_.as<uint8_t>(), rescan_req_.as<uint8_t>(),
+                     dc_ctr_.as<int32_t>(), static_cast<int>(dc_ctr_.bytes / sizeof(int32_t)), S_, n};
     timed("frame.begin", [&] { launch_begin_frame(b, st); });
   }
   for (int i = 0; i < n; ++i) {
@@ -686,7 +684,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
         dc.out_map = r.outmap;
         dc.idx = r.idx;
         dc.count = counts + r.count_slot * S_;
-        dc.tile_status = r.tilestat.as<uint64_t>();
+        dc.tile_ctr = dc_ctr(i, false);
         dc.frame = frame;
         dc.boot = boot;
         dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
@@ -700,7 +698,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
         dc.out_map = r.outmap;
         dc.idx = r.idx;
         dc.count = counts + r.count_slot * S_;
-        dc.tile_status = r.tilestat.as<uint64_t>();
+        dc.tile_ctr = dc_ctr(i, false);
         dc.frame = frame;
         dc.boot = boot;
         dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
@@ -715,7 +713,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
         dc.out_map = r.wc_map.as<uint8_t>();
         dc.idx = r.wc_idx.as<int32_t>();
         dc.count = counts + r.wc_slot * S_;
-        dc.tile_status = r.wc_tilestat.as<uint64_t>();
+        dc.tile_ctr = dc_ctr(i, true);
         dc.frame = frame;
         dc.boot = boot;
         dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
@@ -777,7 +775,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
       dc.out_map = r.outmap;
       dc.idx = r.idx;
       dc.count = counts + r.count_slot * S_;
-      dc.tile_status = r.tilestat.as<uint64_t>();
+      dc.tile_ctr = dc_ctr(i, false);
       dc.frame = frame;
       dc.boot = boot;
       dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
@@ -794,7 +792,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
       dc.out_map = r.outmap;
       dc.idx = r.idx;
       dc.count = counts + r.count_slot * S_;
-      dc.tile_status = r.tilestat.as<uint64_t>();
+      dc.tile_ctr = dc_ctr(i, false);
       dc.frame = frame;
       dc.boot = boot;
       dc.Hin = d.H, dc.Win = d.W, dc.Hout = d.H, dc.Wout = d.W;
@@ -1171,6 +1169,9 @@ void Net::read_changes(int node, int stream, uint8_t* map, int32_t* rowcol, int6
   std::vector<int32_t> idx(static_cast<size_t>(std::max<int64_t>(n, 0)));
   if (n > 0)
     CK(cudaMemcpy(idx.data(), didx + static_cast<size_t>(stream) * HW, n * sizeof(int32_t), cudaMemcpyDeviceToHost));
+  // the device list is row-major per compaction tile, tiles in completion
+  // order; the reference's list (change.cpp:77-84) is row-major overall
+  std::sort(idx.begin(), idx.end());
   if (count) *count = n;
   if (map) {
     std::memset(map, 0, HW);

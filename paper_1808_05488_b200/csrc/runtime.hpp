@@ -100,13 +100,13 @@ struct NodeRT {
   DevBuf state, inmap;           // Detect policy
   // every node
   DevBuf out;                    // [S][H][W][Cs]
-  DevBuf outmap_own, idx_own, tilestat;
+  DevBuf outmap_own, idx_own;
   uint8_t* outmap = nullptr;     // may alias the producer (Reuse1x1)
   int32_t* idx = nullptr;
   int count_slot = 0;            // index into Net::counts ([slot][S])
   int dc_rows = 1, dc_tiles = 1, dc_smem = 0;
   // worst-case map (record_worst_case)
-  DevBuf wc_map, wc_idx, wc_tilestat;
+  DevBuf wc_map, wc_idx;
   int wc_slot = -1;
   int dc_wc_rows = 1, dc_wc_tiles = 1, dc_wc_smem = 0;
 };
@@ -166,6 +166,11 @@ class Net {
   // running max |value| per stream: entry 0 = network input (state of the first
   // layer), entry i+1 = node i's output; the fp16 GEMM scales come from these
   DevBuf amax_;
+  // compaction counters [node][main, worst-case][S][offset, tiles done], zeroed per frame
+  DevBuf dc_ctr_;
+  int32_t* dc_ctr(int node, bool worst) const {
+    return dc_ctr_.as<int32_t>() + (static_cast<size_t>(node) * 2 + (worst ? 1 : 0)) * S_ * 2;
+  }
   // 8-bit ingest: two staging buffers filled on a copy stream while the other
   // one is being consumed, and three device pointer slots (buffer 0, buffer 1,
   // caller's device pointer) the first detect reads through
