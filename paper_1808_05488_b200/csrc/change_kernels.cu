@@ -583,7 +583,28 @@ __global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompa
       const int r = i / nwo, wo = i - r * nwo;
       const uint32_t* row = s_in + r * nwi;
       uint32_t v = 0;
-      if (a.stride == 1) {
+      if (a.stride <= 2 && a.kw <= 33) {
+        // the window's source bits lie in 3 (stride 1) or 4 (stride 2)
+        // consecutive words: read them once, then funnel shifts in registers
+        const int B0 = wo * 32 * a.stride - a.pad, w0 = B0 >> 5, o0 = B0 & 31;
+        uint32_t x[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) x[k] = (w0 + k >= 0 && w0 + k < nwi && (k < 3 || a.stride == 2)) ? row[w0 + k] : 0u;
+        auto win = [&](int b) -> uint32_t {  // 32 bits from bit b of x[0..3]
+          return b < 32 ? __funnelshift_r(x[0], x[1], b)
+                        : (b < 64 ? __funnelshift_r(x[1], x[2], b - 32) : __funnelshift_r(x[2], x[3], b - 64));
+        };
+        if (a.stride == 1) {
+          for (int ki = 0; ki < a.kw; ++ki) v |= win(o0 + ki);
+        } else {
+          uint32_t lo = 0, hi = 0;
+          for (int ki = 0; ki < a.kw; ++ki) {
+            lo |= win(o0 + ki);
+            hi |= win(o0 + 32 + ki);
+          }
+          v = even_bits(lo, hi);
+        }
+      } else if (a.stride == 1) {
         for (int ki = 0; ki < a.kw; ++ki) v |= bits_at(row, nwi, wo * 32 - a.pad + ki);
       } else if (a.stride == 2) {
         uint32_t lo = 0, hi = 0;
