@@ -476,6 +476,11 @@ Net::~Net() {
     cudaStreamSynchronize(copy_st_);
     cudaStreamDestroy(copy_st_);
   }
+  for (auto& e : ev_map_) cudaEventDestroy(e);
+  if (side_st_) {
+    cudaStreamSynchronize(side_st_);
+    cudaStreamDestroy(side_st_);
+  }
 }
 
 std::unique_ptr<Net> Net::clone() const {
@@ -589,6 +594,10 @@ void Net::build() {
     CK(cudaMemcpy(frame_slot_.p, &p, sizeof(p), cudaMemcpyHostToDevice));
     slot_value_ = p;
   }
+  if (const char* e = std::getenv("CBG_SIDE_DILCOMP")) side_dc_ = std::atoi(e) != 0;
+  CK(cudaStreamCreateWithFlags(&side_st_, cudaStreamNonBlocking));
+  ev_map_.resize(nodes_.size());
+  for (auto& e : ev_map_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   frame_ctr_.alloc(4);
   dc_ctr_.alloc(nodes_.size() * 2 * S_ * 2 * sizeof(int32_t));
   boot_req_.alloc(S_);
@@ -650,6 +659,27 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
                      dc_ctr_.as<int32_t>(), static_cast<int>(dc_ctr_.bytes / sizeof(int32_t)), S_, n};
     timed("frame.begin", [&] { launch_begin_frame(b, st); });
   }
+  // node whose compaction wrote node k's map (Reuse1x1 nodes alias their producer's)
+  auto map_owner = [&](int k) {
+    while (nodes_[k].d.kind == CBG_LAYER_CONV && nodes_[k].d.policy == CBG_POLICY_REUSE1X1) k = nodes_[k].d.inputs[0];
+    return k;
+  };
+  // compaction of node k from its producers' maps: on the side stream once
+  // those maps exist (their GEMMs may still run), then joined back
+  auto map_compaction = [&](int k, const DilateCompactArgs& dc) {
+    const NodeDesc& dk = nodes_[k].d;
+    bool side = side_dc_;
+    for (int in : dk.inputs) side = side && nodes_[map_owner(in)].d.kind != kExternal;
+    if (!side) {
+      timed(dk.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
+      CK(cudaEventRecord(ev_map_[k], st));
+      return;
+    }
+    for (int in : dk.inputs) CK(cudaStreamWaitEvent(side_st_, ev_map_[map_owner(in)], 0));
+    timed(dk.name + ".dilcomp", [&] { launch_dilate_compact(dc, side_st_); }, side_st_);
+    CK(cudaEventRecord(ev_map_[k], side_st_));
+    CK(cudaStreamWaitEvent(st, ev_map_[k], 0));
+  };
   for (int i = 0; i < n; ++i) {
     NodeRT& r = nodes_[i];
     const NodeDesc& d = r.d;
@@ -691,6 +721,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
         dc.kh = c.kernel_h, dc.kw = c.kernel_w, dc.stride = c.stride, dc.pad = c.padding;
         dc.rows_per_tile = r.dc_rows, dc.n_tiles = r.dc_tiles, dc.S = S_, dc.smem_bytes = r.dc_smem;
         timed(d.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
+        CK(cudaEventRecord(ev_map_[i], st));
       } else if (d.policy == CBG_POLICY_PROPAGATE) {
         DilateCompactArgs dc{};
         dc.in_map[0] = prod->outmap;
@@ -704,7 +735,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
         dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
         dc.kh = c.kernel_h, dc.kw = c.kernel_w, dc.stride = c.stride, dc.pad = c.padding;
         dc.rows_per_tile = r.dc_rows, dc.n_tiles = r.dc_tiles, dc.S = S_, dc.smem_bytes = r.dc_smem;
-        timed(d.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
+        map_compaction(i, dc);
       }
       if ((flags & CBG_FWD_RECORD_WORST_CASE) && prod) {
         DilateCompactArgs dc{};
@@ -781,7 +812,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
       dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
       dc.kh = d.pool_size, dc.kw = d.pool_size, dc.stride = d.pool_stride, dc.pad = 0;
       dc.rows_per_tile = r.dc_rows, dc.n_tiles = r.dc_tiles, dc.S = S_, dc.smem_bytes = r.dc_smem;
-      timed(d.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
+      map_compaction(i, dc);
       PoolArgs pa{prod->out.as<float>(), r.out.as<float>(), r.idx, counts + r.count_slot * S_, r.Cs, d.Hi, d.Wi,
                   d.H, d.W, d.pool_size, d.pool_stride, S_};
       timed(d.name + ".pool", [&] { launch_pool(pa, st); });
@@ -798,7 +829,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
       dc.Hin = d.H, dc.Win = d.W, dc.Hout = d.H, dc.Wout = d.W;
       dc.kh = 1, dc.kw = 1, dc.stride = 1, dc.pad = 0;
       dc.rows_per_tile = r.dc_rows, dc.n_tiles = r.dc_tiles, dc.S = S_, dc.smem_bytes = r.dc_smem;
-      timed(d.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
+      map_compaction(i, dc);
       JoinArgs ja{};
       for (size_t k = 0; k < d.inputs.size(); ++k) {
         const NodeRT& p = nodes_[d.inputs[k]];
@@ -938,11 +969,12 @@ void Net::run_frame(unsigned flags, unsigned graph_key) {
 }
 
 template <class F>
-void Net::timed(const std::string& label, F&& launch) {
+void Net::timed(const std::string& label, F&& launch, cudaStream_t on) {
   if (!timing_) {
     launch();
     return;
   }
+  if (!on) on = ctx_->stream;
   const size_t need = 2 * (pending_.size() + 1);
   while (ev_pool_.size() < need) {
     cudaEvent_t e;
@@ -950,9 +982,9 @@ void Net::timed(const std::string& label, F&& launch) {
     ev_pool_.push_back(e);
   }
   cudaEvent_t a = ev_pool_[need - 2], b = ev_pool_[need - 1];
-  CK(cudaEventRecord(a, ctx_->stream));
+  CK(cudaEventRecord(a, on));
   launch();
-  CK(cudaEventRecord(b, ctx_->stream));
+  CK(cudaEventRecord(b, on));
   pending_.push_back({label, {a, b}});
 }
 

@@ -193,7 +193,13 @@ class Net {
   std::vector<float> stream_taus_;    // [node][S] mirror of the device thresholds
   bool dense_ = false;
   // kernel timing (bench instrumentation)
-  template <class F> void timed(const std::string& label, F&& launch);
+  template <class F> void timed(const std::string& label, F&& launch, cudaStream_t on = nullptr);
+  // Compactions that only read producers' maps (pools, joins, propagate
+  // convs) run on a side stream from the moment those maps exist, beside the
+  // producer's GEMM; ev_map_[i] = node i's map and list are complete.
+  cudaStream_t side_st_ = nullptr;
+  std::vector<cudaEvent_t> ev_map_;
+  bool side_dc_ = true;
   bool timing_ = false;
   std::vector<cudaEvent_t> ev_pool_;
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending_;
