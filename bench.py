@@ -62,6 +62,9 @@ def parse():
     ap.add_argument("--cpu-budget", type=float, default=20.0, help="seconds of CPU-baseline work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--ingest", choices=["u8", "f32"], default="u8",
+                    help="device-resident frame format of the value / roofline / dense / sweep passes: the 8-bit "
+                         "PNM payload (cbg_net_forward_u8) or its fp32 conversion (cbg_net_forward)")
     ap.add_argument("--sweep-steps", type=int, default=6,
                     help="timed steps per point of the change-rate sweep (0 disables the sweep)")
     return ap.parse_args()
@@ -81,6 +84,9 @@ def config_dict(a, world):
             "objects": a.objects, "object_size": a.object_size,
             "velocity": a.velocity, "noise_std": a.noise, "tau": a.tau,
             "frames": "gen_synthetic quantized to 8-bit PNM payloads; fp32 arms see load_pnm's byte/255.0f",
+            "ingest": (f"value/roofline/dense/sweep: device-resident {getattr(a, 'ingest', 'u8')} frames "
+                       "(u8 = the PNM payload through cbg_net_forward_u8, f32 = its byte/255.0f through "
+                       "cbg_net_forward)"),
             "parallelism": f"streams sharded over {world} GPU(s), no collective",
             "l2": "inputs larger than L2 (frame ring + per-stream state >> 126 MB)"}
 
@@ -278,7 +284,16 @@ def main():
         h8np[:, s] = cbi.to_pnm8(raw)
         hnp[:, s] = cbi.from_pnm8(h8np[:, s])
     dev = host.to(f"cuda:{local}")
+    dev8 = host8.to(f"cuda:{local}")
     torch.cuda.synchronize()
+    u8_in = a.ingest == "u8"
+
+    def feed(net_, t, g=None):
+        """one frame of the device-resident workload (all streams of group g, or of the whole set)"""
+        if u8_in:
+            net_.enqueue_device_u8((dev8[t] if g is None else dev8[t, g * Sg]).data_ptr())
+        else:
+            net_.enqueue_device((dev[t] if g is None else dev[t, g * Sg]).data_ptr())
     order = list(range(1, L)) + list(range(L - 2, 1, -1))
 
     def frame_at(k):  # frame index of post-bootstrap step k
@@ -327,10 +342,10 @@ def main():
 
     # ---- value: frames resident in HBM ---------------------------------------
     for g in range(G):
-        nets[g].enqueue_device(dptr(0, g))  # bootstrap (untimed)
+        feed(nets[g], 0, g)  # bootstrap (untimed)
     for k in range(a.warmup):
         for g in range(G):
-            nets[g].enqueue_device(dptr(frame_at(k), g))
+            feed(nets[g], frame_at(k), g)
     for c in ctxs:
         c.synchronize()
     barrier()
@@ -338,7 +353,7 @@ def main():
 
     def value_step(k):
         for g in range(G):
-            nets[g].enqueue_device(dptr(frame_at(base_k + k), g))
+            feed(nets[g], frame_at(base_k + k), g)
             nets[g].copy_counts_async(counts_pinned[g, k].data_ptr())
 
     with ClockSampler(local) as clocks:
@@ -357,15 +372,15 @@ def main():
     # one stream set holding all S streams (the launch shape of the ncu capture
     # in profiles/), eager launches with an event pair around every kernel
     pnet = cbi.convert_to_cb(spec, taus, n_streams=S, ctx=ctx)
-    pnet.enqueue_device(dev[0].data_ptr())
+    feed(pnet, 0)
     for k in range(2):
-        pnet.enqueue_device(dev[frame_at(next_k + k)].data_ptr())
+        feed(pnet, frame_at(next_k + k))
     ctx.synchronize()
     pnet.set_kernel_timing(True)
     work = {}
     prof_counts = torch.empty((n_slots, S), dtype=torch.int32, pin_memory=True)
     for k in range(a.profile_steps):
-        pnet.enqueue_device(dev[frame_at(next_k + 2 + k)].data_ptr())
+        feed(pnet, frame_at(next_k + 2 + k))
         pnet.copy_counts_async(prof_counts.data_ptr())
         ctx.synchronize()
         c = prof_counts.numpy()
@@ -441,14 +456,14 @@ def main():
         dnets = [cbi.convert_to_cb(spec, taus, n_streams=Sg, ctx=ctxs[g]) for g in range(G)]
         for g in range(G):
             dnets[g].set_dense(True)
-            dnets[g].enqueue_device(dptr(0, g))
-            dnets[g].enqueue_device(dptr(1, g))
+            feed(dnets[g], 0, g)
+            feed(dnets[g], 1, g)
         for c in ctxs:
             c.synchronize()
 
         def dense_step(k):
             for g in range(G):
-                dnets[g].enqueue_device(dptr(frame_at(k), g))
+                feed(dnets[g], frame_at(k), g)
 
         dms = max_over_ranks(timed_region(dense_step, a.dense_steps))
         dense_fps = S * world * a.dense_steps / (dms / 1000.0)
@@ -464,31 +479,43 @@ def main():
         for pt in SWEEP:
             if pt == "random":
                 gen = torch.Generator(device=f"cuda:{local}").manual_seed(4242 + rank)
-                sdev = torch.rand((R, S, 3, H, W), generator=gen, device=f"cuda:{local}")
+                if u8_in:
+                    sdev = torch.randint(0, 256, (R, S, H, W, 3), generator=gen, device=f"cuda:{local}",
+                                         dtype=torch.uint8)
+                else:
+                    sdev = torch.rand((R, S, 3, H, W), generator=gen, device=f"cuda:{local}")
             else:
                 ob, sz = pt
-                sh = torch.empty((R, S, 3, H, W), dtype=torch.float32, pin_memory=True)
+                sh = torch.empty((R, S, H, W, 3) if u8_in else (R, S, 3, H, W),
+                                 dtype=torch.uint8 if u8_in else torch.float32, pin_memory=True)
                 shn = sh.numpy()
 
                 def _gen(s_, ob=ob, sz=sz, shn=shn):
-                    shn[:, s_] = cbi.from_pnm8(cbi.to_pnm8(cbi.gen_synthetic(cbi.SyntheticConfig(
-                        H, W, 3, R, ob, sz, a.velocity, a.velocity, a.noise, shard.seed(s_)))))
+                    p8 = cbi.to_pnm8(cbi.gen_synthetic(cbi.SyntheticConfig(
+                        H, W, 3, R, ob, sz, a.velocity, a.velocity, a.noise, shard.seed(s_))))
+                    shn[:, s_] = p8 if u8_in else cbi.from_pnm8(p8)
                 with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as pool:
                     list(pool.map(_gen, range(S)))
                 sdev = sh.to(f"cuda:{local}")
+
+            def sfeed(net_, t, g, sdev=None):
+                if u8_in:
+                    net_.enqueue_device_u8(sdev[t, g * Sg].data_ptr())
+                else:
+                    net_.enqueue_device(sdev[t, g * Sg].data_ptr())
             snets = [cbi.convert_to_cb(spec, taus, n_streams=Sg, ctx=ctxs[g]) for g in range(G)]
             for g in range(G):
-                snets[g].enqueue_device(sdev[0, g * Sg].data_ptr())
+                sfeed(snets[g], 0, g, sdev)
             for k in range(3):
                 for g in range(G):
-                    snets[g].enqueue_device(sdev[sorder[k % len(sorder)], g * Sg].data_ptr())
+                    sfeed(snets[g], sorder[k % len(sorder)], g, sdev)
             for c in ctxs:
                 c.synchronize()
             barrier()
 
             def sweep_step(k, snets=snets, sdev=sdev):
                 for g in range(G):
-                    snets[g].enqueue_device(sdev[sorder[(3 + k) % len(sorder)], g * Sg].data_ptr())
+                    sfeed(snets[g], sorder[(3 + k) % len(sorder)], g, sdev)
 
             sms = max_over_ranks(timed_region(sweep_step, a.sweep_steps))
             for g in range(G):

@@ -237,14 +237,19 @@ __global__ void __launch_bounds__(kThreads) detect_frame_chw_scalar_kernel(Detec
 // IEEE division. One thread = 4 consecutive pixels = C 32-bit words of the
 // frame; the state is CHW planes (state_chw) or NHWC (Cs == 4). C <= 4.
 // ---------------------------------------------------------------------------
-template <bool kChw>
-__global__ void __launch_bounds__(kFrameThreads) detect_frame_u8_kernel(DetectFrameArgs a) {
+constexpr float kInv255 = 1.0f / 255.0f;  // fp32(1/255)
+// kC: channel count known at compile time (3 = RGB PNM, the common case; 0 =
+// runtime a.C <= 4). <= 64 registers: 8 CTAs per SM keep enough loads in flight.
+template <bool kChw, int kC>
+__global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(DetectFrameArgs a) {
+  constexpr int CM = kC ? kC : 4;  // register arrays
   const int s = blockIdx.y;
+  const int CC = kC ? kC : a.C;
   const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
-  const uint8_t* x8 = *a.x8_slot + static_cast<long long>(s) * a.C * HW;
-  float* st = a.state + static_cast<long long>(s) * (kChw ? a.C : a.Cs) * HW;
+  const uint8_t* x8 = *a.x8_slot + static_cast<long long>(s) * CC * HW;
+  float* st = a.state + static_cast<long long>(s) * (kChw ? CC : a.Cs) * HW;
   uint8_t* m = a.map + static_cast<long long>(s) * HW;
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
@@ -254,30 +259,35 @@ __global__ void __launch_bounds__(kFrameThreads) detect_frame_u8_kernel(DetectFr
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long p0 = q << 2;
     // 4 pixels x C bytes = C words, 4-byte aligned (byte offset 4*C*q)
-    uint32_t wd[4];
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(x8 + p0 * a.C);
+    uint32_t wd[CM];
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(x8 + p0 * CC);
 #pragma unroll
-    for (int i = 0; i < 4; ++i) wd[i] = i < a.C ? __ldg(src + i) : 0u;
-    float px[4][4];  // [pixel][channel]
+    for (int i = 0; i < CM; ++i) wd[i] = i < CC ? __ldg(src + i) : 0u;
+    float px[4][CM];  // [pixel][channel]
 #pragma unroll
     for (int j = 0; j < 4; ++j)
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (c < a.C) {
-          const int b = j * a.C + c;  // byte index within the 4-pixel group
-          const uint32_t v = (wd[b >> 2] >> (8 * (b & 3))) & 0xffu;
-          px[j][c] = __fdiv_rn(static_cast<float>(v), 255.0f);
+      for (int c = 0; c < CM; ++c) {
+        if (c < CC) {
+          const int b = j * CC + c;  // byte index within the 4-pixel group
+          // load_pnm's byte / 255.0f: float(byte) via the 2^23 magic, then
+          // q = byte * fp32(1/255) and one FMA residual step, which is the
+          // correctly rounded quotient for all 256 bytes
+          // (tests/test_ingest_math.py::test_byte_div255_sequence)
+          const float fv = __uint_as_float(__byte_perm(wd[b >> 2], 0x4B000000u, (b & 3) | 0x7540u)) - 8388608.0f;
+          const float q = __fmul_rn(fv, kInv255);
+          px[j][c] = fmaf(fmaf(-q, 255.0f, fv), kInv255, q);
         } else {
           px[j][c] = 0.0f;
         }
       }
     uint32_t ch = 0;
-    float sv[4][4];
+    float sv[4][CM];
     if (!boot) {
       if constexpr (kChw) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (c < a.C) {
+        for (int c = 0; c < CM; ++c)
+          if (c < CC) {
             const float4 v = *reinterpret_cast<const float4*>(st + c * HW + p0);
             sv[0][c] = v.x, sv[1][c] = v.y, sv[2][c] = v.z, sv[3][c] = v.w;
           }
@@ -285,25 +295,27 @@ __global__ void __launch_bounds__(kFrameThreads) detect_frame_u8_kernel(DetectFr
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
           const float4 v = *reinterpret_cast<const float4*>(st + (p0 + j) * 4);
-          sv[j][0] = v.x, sv[j][1] = v.y, sv[j][2] = v.z, sv[j][3] = v.w;
+          const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+          for (int c = 0; c < CM; ++c) sv[j][c] = vv[c];
         }
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j)
 #pragma unroll
-        for (int c = 0; c < 4; ++c)
-          if (c < a.C && fabsf(px[j][c] - sv[j][c]) > tau) ch |= 1u << j;
+        for (int c = 0; c < CM; ++c)
+          if (c < CC && fabsf(px[j][c] - sv[j][c]) > tau) ch |= 1u << j;
     }
     if (write_all || ch) {
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if (write_all || ((ch >> j) & 1u))
 #pragma unroll
-          for (int c = 0; c < 4; ++c) vmax = fmaxf(vmax, px[j][c]);
+          for (int c = 0; c < CM; ++c) vmax = fmaxf(vmax, px[j][c]);
       if constexpr (kChw) {
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          if (c < a.C) {
+        for (int c = 0; c < CM; ++c) {
+          if (c < CC) {
             float v[4];
 #pragma unroll
             for (int j = 0; j < 4; ++j) v[j] = (write_all || ((ch >> j) & 1u)) ? px[j][c] : sv[j][c];
@@ -314,7 +326,7 @@ __global__ void __launch_bounds__(kFrameThreads) detect_frame_u8_kernel(DetectFr
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           if (write_all || ((ch >> j) & 1u))
-            *reinterpret_cast<float4*>(st + (p0 + j) * 4) = make_float4(px[j][0], px[j][1], px[j][2], px[j][3]);
+            *reinterpret_cast<float4*>(st + (p0 + j) * 4) = make_float4(px[j][0], CM > 1 ? px[j][1 % CM] : 0.f, CM > 2 ? px[j][2 % CM] : 0.f, CM > 3 ? px[j][3 % CM] : 0.f);
       }
     }
     if (ch) {
@@ -820,8 +832,9 @@ void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
   if (a.x8_slot) {
     if (HW % 4 == 0 && (a.state_chw || a.Cs == 4)) {
       dim3 grid(2 * blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
-      if (a.state_chw) detect_frame_u8_kernel<true><<<grid, kFrameThreads, 0, st>>>(a);
-      else detect_frame_u8_kernel<false><<<grid, kFrameThreads, 0, st>>>(a);
+      if (a.state_chw && a.C == 3) detect_frame_u8_kernel<true, 3><<<grid, kFrameThreads, 0, st>>>(a);
+      else if (a.state_chw) detect_frame_u8_kernel<true, 0><<<grid, kFrameThreads, 0, st>>>(a);
+      else detect_frame_u8_kernel<false, 0><<<grid, kFrameThreads, 0, st>>>(a);
     } else {
       dim3 grid(blocks_for(HW, kThreads, a.S, sm_count()), a.S);
       detect_frame_u8_scalar_kernel<<<grid, kThreads, 0, st>>>(a);
