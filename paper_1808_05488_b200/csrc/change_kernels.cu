@@ -240,8 +240,20 @@ __global__ void __launch_bounds__(kThreads) detect_frame_chw_scalar_kernel(Detec
 constexpr float kInv255 = 1.0f / 255.0f;  // fp32(1/255)
 // kC: channel count known at compile time (3 = RGB PNM, the common case; 0 =
 // runtime a.C <= 4). <= 64 registers: 8 CTAs per SM keep enough loads in flight.
-template <bool kChw, int kC>
+// kS8 (kChw, kC = 3): compare against the 8-bit state shadow (1 byte per
+// value read instead of 4; the fp32 state is only written).
+CBG_DEV float byte_to_unit(uint32_t word, int b) {
+  // load_pnm's byte / 255.0f: float(byte) via the 2^23 magic, then
+  // q = byte * fp32(1/255) and one FMA residual step, which is the
+  // correctly rounded quotient for all 256 bytes
+  // (tests/test_ingest_math.py::test_byte_div255_sequence)
+  const float fv = __uint_as_float(__byte_perm(word, 0x4B000000u, (b & 3) | 0x7540u)) - 8388608.0f;
+  const float q = __fmul_rn(fv, kInv255);
+  return fmaf(fmaf(-q, 255.0f, fv), kInv255, q);
+}
+template <bool kChw, int kC, bool kS8 = false>
 __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(DetectFrameArgs a) {
+  static_assert(!kS8 || (kChw && kC == 3), "8-bit state shadow: CHW state, 3 channels");
   constexpr int CM = kC ? kC : 4;  // register arrays
   const int s = blockIdx.y;
   const int CC = kC ? kC : a.C;
@@ -251,6 +263,7 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(Detec
   const uint8_t* x8 = *a.x8_slot + static_cast<long long>(s) * CC * HW;
   float* st = a.state + static_cast<long long>(s) * (kChw ? CC : a.Cs) * HW;
   uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  uint8_t* s8 = a.state8 ? a.state8 + static_cast<long long>(s) * CC * HW : nullptr;
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
   const long long n4 = HW >> 2;
@@ -259,7 +272,14 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(Detec
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long p0 = q << 2;
     // 4 pixels x C bytes = C words, 4-byte aligned (byte offset 4*C*q)
-    uint32_t wd[CM];
+    uint32_t wd[CM], sw[CM];
+    if constexpr (kS8) {
+      if (!boot) {
+        const uint32_t* ssrc = reinterpret_cast<const uint32_t*>(s8 + p0 * CC);
+#pragma unroll
+        for (int i = 0; i < CM; ++i) sw[i] = ssrc[i];
+      }
+    }
     const uint32_t* src = reinterpret_cast<const uint32_t*>(x8 + p0 * CC);
 #pragma unroll
     for (int i = 0; i < CM; ++i) wd[i] = i < CC ? __ldg(src + i) : 0u;
@@ -270,13 +290,7 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(Detec
       for (int c = 0; c < CM; ++c) {
         if (c < CC) {
           const int b = j * CC + c;  // byte index within the 4-pixel group
-          // load_pnm's byte / 255.0f: float(byte) via the 2^23 magic, then
-          // q = byte * fp32(1/255) and one FMA residual step, which is the
-          // correctly rounded quotient for all 256 bytes
-          // (tests/test_ingest_math.py::test_byte_div255_sequence)
-          const float fv = __uint_as_float(__byte_perm(wd[b >> 2], 0x4B000000u, (b & 3) | 0x7540u)) - 8388608.0f;
-          const float q = __fmul_rn(fv, kInv255);
-          px[j][c] = fmaf(fmaf(-q, 255.0f, fv), kInv255, q);
+          px[j][c] = byte_to_unit(wd[b >> 2], b);
         } else {
           px[j][c] = 0.0f;
         }
@@ -284,7 +298,12 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(Detec
     uint32_t ch = 0;
     float sv[4][CM];
     if (!boot) {
-      if constexpr (kChw) {
+      if constexpr (kS8) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int c = 0; c < CM; ++c) sv[j][c] = byte_to_unit(sw[(j * CM + c) >> 2], j * CM + c);
+      } else if constexpr (kChw) {
 #pragma unroll
         for (int c = 0; c < CM; ++c)
           if (c < CC) {
@@ -327,6 +346,27 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(Detec
         for (int j = 0; j < 4; ++j)
           if (write_all || ((ch >> j) & 1u))
             *reinterpret_cast<float4*>(st + (p0 + j) * 4) = make_float4(px[j][0], CM > 1 ? px[j][1 % CM] : 0.f, CM > 2 ? px[j][2 % CM] : 0.f, CM > 3 ? px[j][3 % CM] : 0.f);
+      }
+    }
+    // the 8-bit shadow: the frame's words on a full update; the changed
+    // pixels' bytes merged into the old words otherwise (kS8 only: without it
+    // the shadow is stale until the stream's next full update)
+    if (s8 && (write_all || (kS8 && ch))) {
+      uint32_t* sdst = reinterpret_cast<uint32_t*>(s8 + p0 * CC);
+#pragma unroll
+      for (int i = 0; i < CM; ++i) {
+        if (i >= CC) continue;
+        uint32_t v = wd[i];
+        if constexpr (kS8) {
+          if (!write_all) {
+            uint32_t keep = 0;  // bytes of unchanged pixels keep the old state
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (!((ch >> ((4 * i + k) / CM)) & 1u)) keep |= 0xFFu << (8 * k);
+            v = (v & ~keep) | (sw[i] & keep);
+          }
+        }
+        sdst[i] = v;
       }
     }
     if (ch) {
@@ -832,7 +872,9 @@ void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
   if (a.x8_slot) {
     if (HW % 4 == 0 && (a.state_chw || a.Cs == 4)) {
       dim3 grid(2 * blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
-      if (a.state_chw && a.C == 3) detect_frame_u8_kernel<true, 3><<<grid, kFrameThreads, 0, st>>>(a);
+      if (a.state_chw && a.C == 3 && a.use_state8 && a.state8)
+        detect_frame_u8_kernel<true, 3, true><<<grid, kFrameThreads, 0, st>>>(a);
+      else if (a.state_chw && a.C == 3) detect_frame_u8_kernel<true, 3><<<grid, kFrameThreads, 0, st>>>(a);
       else if (a.state_chw) detect_frame_u8_kernel<true, 0><<<grid, kFrameThreads, 0, st>>>(a);
       else detect_frame_u8_kernel<false, 0><<<grid, kFrameThreads, 0, st>>>(a);
     } else {

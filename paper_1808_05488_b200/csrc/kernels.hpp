@@ -32,6 +32,12 @@ struct DetectFrameArgs {
   float* amax;         // [S] running max |value written to the state| (atomicMax)
   const uint8_t* const* x8_slot;  // non-null: 8-bit frames [S][H][W][C] (PNM payload order), x = byte/255
   long long x_sstride;  // fp32 frames: elements between streams' frames (C*H*W, or 0 = one frame for all)
+  // 8-bit shadow of the state ([S][H][W][C] bytes, the frames' layout), kept
+  // by the 8-bit ingest: every state value it writes is byte/255, so the byte
+  // is the state. Written on full updates (always) and at changed pixels
+  // (when use_state8); use_state8: compare against it instead of the fp32 state.
+  uint8_t* state8;
+  int use_state8;
 };
 void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st);
 

@@ -491,7 +491,10 @@ std::unique_ptr<Net> Net::clone() const {
     NodeRT& b = c->nodes_[i];
     if (a.out.bytes) CK(cudaMemcpy(b.out.p, a.out.p, a.out.bytes, cudaMemcpyDeviceToDevice));
     if (a.state.bytes) CK(cudaMemcpy(b.state.p, a.state.p, a.state.bytes, cudaMemcpyDeviceToDevice));
+    if (a.state8.bytes) CK(cudaMemcpy(b.state8.p, a.state8.p, a.state8.bytes, cudaMemcpyDeviceToDevice));
   }
+  c->s8_valid_ = s8_valid_;
+  c->s8_pending_ = s8_pending_;
   CK(cudaMemcpy(c->boot_req_.p, boot_req_.p, S_, cudaMemcpyDeviceToDevice));
   CK(cudaMemcpy(c->amax_.p, amax_.p, amax_.bytes, cudaMemcpyDeviceToDevice));
   c->ext_amax_ = ext_amax_;
@@ -568,6 +571,7 @@ void Net::build() {
       if (d.policy == CBG_POLICY_DETECT) {
         r.state_chw = r.exact && d.inputs[0] < 0;
         r.state.alloc(static_cast<size_t>(S_) * HWi * (r.state_chw ? d.Ci : r.Csi) * sizeof(float));
+        if (r.state_chw && d.Ci == 3 && HWi % 4 == 0) r.state8.alloc(static_cast<size_t>(S_) * HWi * 3 + 16);
         r.inmap.alloc(static_cast<size_t>(S_) * HWi + 16);
       }
       if (!reuse) {
@@ -602,6 +606,8 @@ void Net::build() {
   dc_ctr_.alloc(nodes_.size() * 2 * S_ * 2 * sizeof(int32_t));
   boot_req_.alloc(S_);
   CK(cudaMemset(boot_req_.p, 1, S_));
+  s8_valid_.assign(S_, 0);
+  s8_pending_.assign(S_, 1);
   boot_now_.alloc(S_);
   dense_flag_.alloc(1);
   rescan_req_.alloc(std::max(1, n));
@@ -647,7 +653,7 @@ int Net::launch_count(unsigned flags) const {
   return k;
 }
 
-void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
+void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8) {
   cudaStream_t st = ctx_->stream;
   int32_t* counts = counts_.as<int32_t>();
   const uint32_t* frame = frame_ctr_.as<uint32_t>();
@@ -695,7 +701,8 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8) {
                             d.Ci, r.Csi, d.Hi, d.Wi, S_, taus_.as<float>() + static_cast<size_t>(i) * S_,
                             topo_.mode == CBG_MODE_CLOSEDLOOP, r.state_chw, amax_entry(-1),
                             u8 ? frame8_slot_.as<const uint8_t*>() + slot8 : nullptr,
-                            bcast ? 0LL : static_cast<long long>(d.Ci) * d.Hi * d.Wi};
+                            bcast ? 0LL : static_cast<long long>(d.Ci) * d.Hi * d.Wi,
+                            u8 ? r.state8.as<uint8_t>() : nullptr, (u8 && s8) ? 1 : 0};
           timed(d.name + ".detect", [&] { launch_detect_frame(a, st); });
         } else {
           const bool ext = prod->d.kind == kExternal;  // standalone layer: arbitrary x, dense detect
@@ -871,6 +878,10 @@ void Net::forward(const float* frames, unsigned flags) {
                          cudaMemcpyHostToDevice, st));
   }
   run_frame(flags, (flags & CBG_FWD_RECORD_WORST_CASE) | ((flags & CBG_FWD_BROADCAST_INPUT) ? (1u << 30) : 0u));
+  // fp32 values in the state: the 8-bit shadow is stale until a full update
+  // goes through the 8-bit ingest (a boot here consumed the pending requests)
+  std::fill(s8_valid_.begin(), s8_valid_.end(), 0);
+  std::fill(s8_pending_.begin(), s8_pending_.end(), 0);
 }
 
 void Net::forward_u8(const uint8_t* frames, unsigned flags) {
@@ -895,7 +906,21 @@ void Net::forward_u8(const uint8_t* frames, unsigned flags) {
       CK(cudaEventCreateWithFlags(&ev_consumed_[b], cudaEventDisableTiming));
     }
   }
-  const unsigned key = (flags & CBG_FWD_RECORD_WORST_CASE) | (1u << 31);
+  if (flags & CBG_FWD_FORCE_FULL) std::fill(s8_pending_.begin(), s8_pending_.end(), 1);
+  bool s8 = true;  // every first layer keeps a valid 8-bit shadow for every stream
+  for (const NodeRT& r : nodes_)
+    if (r.d.kind == CBG_LAYER_CONV && r.d.inputs[0] < 0 && r.d.policy == CBG_POLICY_DETECT)
+      s8 = s8 && r.state8.bytes != 0;
+  for (uint8_t v : s8_valid_) s8 = s8 && v;
+  const unsigned key = (flags & CBG_FWD_RECORD_WORST_CASE) | (1u << 31) | (s8 ? (1u << 27) : 0u);
+  // after the frame: streams that took a full update hold a valid shadow
+  auto s8_after = [&] {
+    const bool all = dense_ || topo_.mode != CBG_MODE_CLOSEDLOOP;
+    for (size_t k = 0; k < s8_valid_.size(); ++k) {
+      if (all || s8_pending_[k]) s8_valid_[k] = 1;
+      s8_pending_[k] = 0;
+    }
+  };
   if (flags & CBG_FWD_INPUT_ON_DEVICE) {
     if (frames != slot8_value_) {
       const uint8_t* v = frames;  // pageable source: consumed before cudaMemcpyAsync returns
@@ -903,6 +928,7 @@ void Net::forward_u8(const uint8_t* frames, unsigned flags) {
       slot8_value_ = frames;
     }
     run_frame(flags, key | (2u << 28));
+    s8_after();
     return;
   }
   // host frames: H2D into buffer b on the copy stream once the frame that last
@@ -914,6 +940,7 @@ void Net::forward_u8(const uint8_t* frames, unsigned flags) {
   CK(cudaEventRecord(ev_copied_[b], copy_st_));
   CK(cudaStreamWaitEvent(st, ev_copied_[b], 0));
   run_frame(flags, key | (static_cast<unsigned>(b) << 28));
+  s8_after();
   CK(cudaEventRecord(ev_consumed_[b], st));
 }
 
@@ -928,10 +955,11 @@ void Net::run_frame(unsigned flags, unsigned graph_key) {
   const bool u8 = (graph_key >> 31) != 0;
   const bool bcast = ((graph_key >> 30) & 1u) != 0;
   const int slot8 = static_cast<int>((graph_key >> 28) & 3u);
+  const bool s8 = ((graph_key >> 27) & 1u) != 0;
   last_flags_ = flags;
   last_launches_ = launch_count(gflags);
   if (timing_) {
-    enqueue_frame(gflags, u8, bcast, slot8);
+    enqueue_frame(gflags, u8, bcast, slot8, s8);
     CK(cudaStreamSynchronize(st));
     size_t k = 0;
     for (auto& p : pending_) {
@@ -953,7 +981,7 @@ void Net::run_frame(unsigned flags, unsigned graph_key) {
     cudaGraph_t g;
     CK(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     try {
-      enqueue_frame(gflags, u8, bcast, slot8);
+      enqueue_frame(gflags, u8, bcast, slot8, s8);
     } catch (...) {
       cudaStreamEndCapture(st, &g);
       throw;
@@ -1062,6 +1090,7 @@ void Net::reset(int stream) {
   if (stream < -1 || stream >= S_) throw_invalid("reset: stream out of range");
   cudaStream_t st = ctx_->stream;
   const int s0 = stream < 0 ? 0 : stream, s1 = stream < 0 ? S_ : stream + 1;
+  for (int k = s0; k < s1; ++k) s8_pending_[k] = 1;
   for (NodeRT& r : nodes_) {
     if (r.d.kind == kExternal) continue;
     const size_t per_out = r.out.bytes / S_;

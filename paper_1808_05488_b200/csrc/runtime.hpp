@@ -98,6 +98,7 @@ struct NodeRT {
   bool state_chw = false;        // first-layer exact conv: input state as CHW planes (= the frame layout)
   DevBuf wimg, ktab, bias, wraw; // wraw: [Cout][Cin*kh*kw] fp32 for the exact path
   DevBuf state, inmap;           // Detect policy
+  DevBuf state8;                 // first layer, 8-bit ingest: byte shadow of the state (DetectFrameArgs::state8)
   // every node
   DevBuf out;                    // [S][H][W][Cs]
   DevBuf outmap_own, idx_own;
@@ -152,8 +153,9 @@ class Net {
 
  private:
   void build();
-  // kernels of one frame (graph body); slot8 = which 8-bit ingest pointer slot the first detect reads
-  void enqueue_frame(unsigned flags, bool u8 = false, bool bcast = false, int slot8 = 0);
+  // kernels of one frame (graph body); slot8 = which 8-bit ingest pointer slot the first detect reads;
+  // s8 = the first detect compares against the 8-bit state shadow
+  void enqueue_frame(unsigned flags, bool u8 = false, bool bcast = false, int slot8 = 0, bool s8 = false);
   int launch_count(unsigned flags) const;
   void clear_maps();
 
@@ -179,6 +181,9 @@ class Net {
   cudaStream_t copy_st_ = nullptr;
   cudaEvent_t ev_copied_[2] = {nullptr, nullptr}, ev_consumed_[2] = {nullptr, nullptr};
   int u8_buf_ = 0;
+  // host view of the 8-bit state shadow: valid per stream once a full update
+  // went through the 8-bit ingest; any fp32 frame invalidates it
+  std::vector<uint8_t> s8_valid_, s8_pending_;
   void upload_taus(const std::vector<uint8_t>& rescan);
   void run_frame(unsigned flags, unsigned graph_key);
   float* amax_entry(int node) const { return amax_.as<float>() + static_cast<size_t>(node + 1) * S_; }

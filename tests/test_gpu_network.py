@@ -8,7 +8,7 @@ maps within max_rel_err <= TOL_NET.
 import numpy as np
 import pytest
 
-from paper_1808_05488_b200 import cbi
+from paper_1808_05488_b200 import _lib, cbi
 from tests import oracle
 
 pytestmark = pytest.mark.gpu
@@ -179,6 +179,46 @@ def test_pnm8_ingest_matches_fp32_and_reference(gpu):
             assert np.array_equal(a.node_state(0, s), b.node_state(0, s))
             want = refs[s].forward(f32[t, s])
             assert np.array_equal(a.node_output(0, s), refs[s].output(0))  # first layer bit-exact
+            assert oracle.max_rel_err(a.output(s), want) <= TOL_NET
+
+
+def test_pnm8_state_shadow_mixed_ingest(gpu):
+    """The 8-bit ingest keeps a byte shadow of the first layer's state and
+    compares against it once every stream had a full update through the 8-bit
+    path. Mixed feeding (8-bit, fp32, 8-bit again, a per-stream reset, a forced
+    full update) must stay bit-identical to the fp32 API on the same values and
+    to the reference, whichever comparison source each frame used."""
+    S, H, W = 3, 48, 64
+    spec = cbi.make_seg_spec(5, H, W)
+    taus = [0.04] * 5
+    raw = np.stack([seq(H, W, n=12, seed=700 + s, noise=0.02) for s in range(S)], axis=1)
+    pnm = cbi.to_pnm8(raw)
+    f32 = cbi.from_pnm8(pnm)
+    a = cbi.convert_to_cb(spec, taus, n_streams=S)
+    b = cbi.convert_to_cb(spec, taus, n_streams=S)
+    refs = [oracle.RefNet(spec, taus) for _ in range(S)]
+    # frame -> how net a is fed: u8, f32, u8 + reset of stream 1 before, u8 + FORCE_FULL
+    plan = ["u8", "u8", "u8", "f32", "u8", "u8", "reset1", "u8", "u8", "full", "u8", "u8"]
+    for t, how in enumerate(plan):
+        if how == "reset1":
+            a.reset(1)
+            b.reset(1)
+            refs[1].reset()
+        if how == "f32":
+            a.enqueue(f32[t])
+        elif how == "full":
+            a.enqueue_u8(pnm[t], _lib.FWD_FORCE_FULL)
+        else:
+            a.enqueue_u8(pnm[t])
+        b.enqueue(f32[t], _lib.FWD_FORCE_FULL if how == "full" else 0)
+        assert np.array_equal(a.counts(), b.counts()), (t, how)
+        for s in range(S):
+            if how == "full":
+                refs[s].reset()
+            want = refs[s].forward(f32[t, s])
+            assert np.array_equal(a.node_state(0, s), b.node_state(0, s)), (t, s)
+            assert np.array_equal(a.node_output(0, s), refs[s].output(0)), (t, s)
+            assert np.array_equal(a.output(s), b.output(s)), (t, s)
             assert oracle.max_rel_err(a.output(s), want) <= TOL_NET
 
 
