@@ -137,6 +137,7 @@ int cbg_device_available(void);
 /* ---- context: one device + one CUDA stream -------------------------------- */
 int cbg_ctx_create(int device, cbg_ctx* out);
 void cbg_ctx_destroy(cbg_ctx ctx);
+/* Waits for the ctx stream and the copy-out stream (cbg_net_copy_output_detached). */
 int cbg_ctx_sync(cbg_ctx ctx);
 /* The context's cudaStream_t, for interop (returned as void*). */
 void* cbg_ctx_stream(cbg_ctx ctx);
@@ -307,6 +308,13 @@ int cbg_net_timing_report(cbg_net net, char* buf, int len);
 /* Asynchronous D2H copy of a node's retained output in the device layout
  * (NHWC fp32, channel stride round_up(C,4), all streams) on the ctx stream. */
 int cbg_net_copy_output_async(cbg_net net, int node, void* host_dst);
+/* The same bytes, pipelined for serving: a device-to-device copy into one of
+ * two staging buffers on the ctx stream, then the D2H on the context's
+ * copy-out stream (cbg_ctx_copy_stream), so the next frame's kernels do not
+ * wait for PCIe. Complete after cbg_ctx_sync (which waits for both streams)
+ * or after the copy-out stream. host_dst should be pinned. */
+int cbg_net_copy_output_detached(cbg_net net, int node, void* host_dst);
+void* cbg_ctx_copy_stream(cbg_ctx ctx);
 int cbg_net_output_bytes(cbg_net net, int node, int64_t* bytes);
 /* Asynchronous D2H copy of the per-frame change counts [slot][n_streams]
  * (int32) into host memory; node_slot (nullable) receives each node's slot. */

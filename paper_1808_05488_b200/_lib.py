@@ -111,6 +111,7 @@ SIGNATURES = {
     "cbg_ctx_destroy": (None, [_vp]),
     "cbg_ctx_sync": (C.c_int, [_vp]),
     "cbg_ctx_stream": (_vp, [_vp]),
+    "cbg_ctx_copy_stream": (_vp, [_vp]),
     "cbg_gen_synthetic": (C.c_int, [_P(SyntheticConfigC), _vp, _vp]),
     "cbg_fill_random_weights": (C.c_int, [_P(NetworkSpecC), C.c_uint32, _P(_vp), _P(_vp)]),
     "cbg_net_validate": (C.c_int, [_P(NetworkSpecC), _vp, C.c_int, _vp, C.c_int]),
@@ -157,6 +158,7 @@ SIGNATURES = {
     "cbg_net_set_kernel_timing": (C.c_int, [_vp, C.c_int]),
     "cbg_net_timing_report": (C.c_int, [_vp, C.c_char_p, C.c_int]),
     "cbg_net_copy_output_async": (C.c_int, [_vp, C.c_int, _vp]),
+    "cbg_net_copy_output_detached": (C.c_int, [_vp, C.c_int, _vp]),
     "cbg_net_output_bytes": (C.c_int, [_vp, C.c_int, _P(C.c_int64)]),
     "cbg_net_copy_counts_async": (C.c_int, [_vp, _vp, _vp]),
     "cbg_net_count_slots": (C.c_int, [_vp, _P(C.c_int)]),

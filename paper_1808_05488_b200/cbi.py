@@ -454,6 +454,11 @@ class Context:
     def stream(self) -> int:
         return lib.cbg_ctx_stream(self.handle) or 0
 
+    @property
+    def copy_stream(self) -> int:
+        """the copy-out stream of copy_output_detached (synchronize() waits for it too)"""
+        return lib.cbg_ctx_copy_stream(self.handle) or 0
+
     def __del__(self):
         if getattr(self, "handle", None) and lib is not None:
             lib.cbg_ctx_destroy(self.handle)
@@ -885,6 +890,11 @@ class CBNetwork:
         """Async D2H of a node's raw device output (NHWC, all streams) into pinned memory."""
         check(lib.cbg_net_copy_output_async(self.handle, node, C.c_void_p(host_ptr)))
 
+
+    def copy_output_detached(self, host_ptr: int, node: int = -1):
+        """copy_output_async through a device staging buffer, D2H on the context's
+        copy-out stream: the next frame does not wait for PCIe (Context.synchronize waits for it)"""
+        check(lib.cbg_net_copy_output_detached(self.handle, node, C.c_void_p(host_ptr)))
     def count_layout(self):
         """(n_slots, node->slot) of the device change-count array [slot][S]."""
         n = C.c_int()

@@ -95,6 +95,7 @@ int cbg_ctx_sync(cbg_ctx ctx) {
   return guard([&] {
     need(ctx, "cbg_ctx_sync");
     cbg::cuda_check(cudaStreamSynchronize(ctx->ctx.stream), "cudaStreamSynchronize");
+    cbg::cuda_check(cudaStreamSynchronize(ctx->ctx.d2h), "cudaStreamSynchronize");
   });
 }
 void* cbg_ctx_stream(cbg_ctx ctx) { return ctx ? static_cast<void*>(ctx->ctx.stream) : nullptr; }
@@ -386,6 +387,14 @@ int cbg_net_count_slots(cbg_net net, int* slots) {
     *slots = std::max(1, net->net->count_slots());
   });
 }
+int cbg_net_copy_output_detached(cbg_net net, int node, void* host_dst) {
+  return guard([&] {
+    need(net, "cbg_net_copy_output_detached");
+    need(host_dst, "cbg_net_copy_output_detached");
+    net->net->copy_output_detached(node, host_dst);
+  });
+}
+void* cbg_ctx_copy_stream(cbg_ctx ctx) { return ctx ? static_cast<void*>(ctx->ctx.d2h) : nullptr; }
 int cbg_net_output_bytes(cbg_net net, int node, int64_t* bytes) {
   return guard([&] {
     need(net, "cbg_net_output_bytes");

@@ -298,8 +298,10 @@ Ctx::Ctx(int dev) : device(dev) {
     throw Error(CBG_ERR_UNSUPPORTED, std::string("kernels are built for sm_100a; device is ") + prop.name);
   sm_count = prop.multiProcessorCount;
   CK(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&d2h, cudaStreamNonBlocking));
 }
 Ctx::~Ctx() {
+  if (d2h) cudaStreamDestroy(d2h);
   if (stream) cudaStreamDestroy(stream);
 }
 
@@ -477,6 +479,13 @@ Net::~Net() {
     cudaStreamDestroy(copy_st_);
   }
   for (auto& e : ev_map_) cudaEventDestroy(e);
+  for (int b = 0; b < 2; ++b) {
+    if (ev_staged_[b]) cudaEventDestroy(ev_staged_[b]);
+    if (ev_drained_[b]) {
+      cudaEventSynchronize(ev_drained_[b]);
+      cudaEventDestroy(ev_drained_[b]);
+    }
+  }
   if (side_st_) {
     cudaStreamSynchronize(side_st_);
     cudaStreamDestroy(side_st_);
@@ -1045,6 +1054,31 @@ void Net::copy_output_async(int node, void* host_dst) {
   if (node >= static_cast<int>(nodes_.size())) throw_invalid("copy_output_async: bad node");
   const NodeRT& r = nodes_[node];
   CK(cudaMemcpyAsync(host_dst, r.out.p, r.out.bytes, cudaMemcpyDeviceToHost, ctx_->stream));
+}
+
+void Net::copy_output_detached(int node, void* host_dst) {
+  if (node < 0) node = static_cast<int>(nodes_.size()) - 1;
+  if (node >= static_cast<int>(nodes_.size())) throw_invalid("copy_output_detached: bad node");
+  const NodeRT& r = nodes_[node];
+  cudaStream_t st = ctx_->stream;
+  if (!ev_staged_[0])
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaEventCreateWithFlags(&ev_staged_[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_drained_[b], cudaEventDisableTiming));
+    }
+  const int b = out_buf_;
+  out_buf_ ^= 1;
+  if (out_stage_[b].bytes < r.out.bytes) {
+    CK(cudaEventSynchronize(ev_drained_[b]));
+    out_stage_[b].alloc(r.out.bytes);
+  }
+  // staging b is free once its previous D2H (two calls ago) has drained
+  CK(cudaStreamWaitEvent(st, ev_drained_[b], 0));
+  CK(cudaMemcpyAsync(out_stage_[b].p, r.out.p, r.out.bytes, cudaMemcpyDeviceToDevice, st));
+  CK(cudaEventRecord(ev_staged_[b], st));
+  CK(cudaStreamWaitEvent(ctx_->d2h, ev_staged_[b], 0));
+  CK(cudaMemcpyAsync(host_dst, out_stage_[b].p, r.out.bytes, cudaMemcpyDeviceToHost, ctx_->d2h));
+  CK(cudaEventRecord(ev_drained_[b], ctx_->d2h));
 }
 
 void Net::set_external(const float* x_chw, const uint8_t* map, const int32_t* rowcol, int64_t n, bool full) {

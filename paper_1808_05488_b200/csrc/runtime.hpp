@@ -83,6 +83,7 @@ struct Ctx {
   int device = 0;
   int sm_count = 148;
   cudaStream_t stream = nullptr;
+  cudaStream_t d2h = nullptr;  // copy-out stream of the detached output copies (cbg_ctx_sync waits for both)
   explicit Ctx(int dev);
   ~Ctx();
 };
@@ -147,6 +148,9 @@ class Net {
   void set_timing(bool on);
   std::string timing_report() const;  // JSON object
   void copy_output_async(int node, void* host_dst);  // raw NHWC [S][H][W][Cs] on the ctx stream
+  // the same bytes through a device staging buffer: D2D on the ctx stream, D2H
+  // on the ctx's copy-out stream, so the next frame does not wait for PCIe
+  void copy_output_detached(int node, void* host_dst);
   void copy_counts_async(int32_t* host_dst);         // [slot][S] on the ctx stream
   int count_slots() const { return n_slots_; }
   int node_slot(int node) const { return nodes_[node].count_slot; }
@@ -184,6 +188,9 @@ class Net {
   // host view of the 8-bit state shadow: valid per stream once a full update
   // went through the 8-bit ingest; any fp32 frame invalidates it
   std::vector<uint8_t> s8_valid_, s8_pending_;
+  DevBuf out_stage_[2];
+  cudaEvent_t ev_staged_[2] = {nullptr, nullptr}, ev_drained_[2] = {nullptr, nullptr};
+  int out_buf_ = 0;
   void upload_taus(const std::vector<uint8_t>& rescan);
   void run_frame(unsigned flags, unsigned graph_key);
   float* amax_entry(int node) const { return amax_.as<float>() + static_cast<size_t>(node + 1) * S_; }

@@ -318,3 +318,29 @@ def test_a_operand_paths(gpu, monkeypatch, direct):
     monkeypatch.setenv("CBG_GEMM_DIRECT", direct)
     spec = cbi.make_seg_spec(9, 80, 112)
     run_pair(spec, [0.05] * 5, frames_for(80, 112, noise=0.003))
+
+
+def test_detached_output_copy_pipelines(gpu):
+    """cbg_net_copy_output_detached: frame k's output lands in its own host
+    buffer although frame k+1 (and k+2) were enqueued before anyone waited;
+    the bytes equal the synchronous readback of a twin network."""
+    S, H, W, T = 2, 40, 56, 5
+    spec = cbi.make_seg_spec(6, H, W)
+    frames = np.stack([cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, T, 2, 8, 2, 2, 0.01, 40 + s))
+                       for s in range(S)], axis=1)
+    a = cbi.convert_to_cb(spec, [0.03] * 5, n_streams=S)
+    b = cbi.convert_to_cb(spec, [0.03] * 5, n_streams=S)
+    nbytes = a.output_bytes(-1)
+    bufs = [np.zeros(nbytes // 4, np.float32) for _ in range(T)]
+    want = []
+    for t in range(T):
+        a.enqueue(frames[t])
+        a.copy_output_detached(bufs[t].ctypes.data)
+        b.enqueue(frames[t])
+        w = np.zeros(nbytes // 4, np.float32)
+        b.copy_output_async(w.ctypes.data)
+        b.synchronize()
+        want.append(w)
+    a.synchronize()
+    for t in range(T):
+        assert np.array_equal(bufs[t], want[t]), t
