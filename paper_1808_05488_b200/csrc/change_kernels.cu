@@ -240,8 +240,6 @@ __global__ void __launch_bounds__(kThreads) detect_frame_chw_scalar_kernel(Detec
 constexpr float kInv255 = 1.0f / 255.0f;  // fp32(1/255)
 // kC: channel count known at compile time (3 = RGB PNM, the common case; 0 =
 // runtime a.C <= 4). <= 64 registers: 8 CTAs per SM keep enough loads in flight.
-// kS8 (kChw, kC = 3): compare against the 8-bit state shadow (1 byte per
-// value read instead of 4; the fp32 state is only written).
 CBG_DEV float byte_to_unit(uint32_t word, int b) {
   // load_pnm's byte / 255.0f: float(byte) via the 2^23 magic, then
   // q = byte * fp32(1/255) and one FMA residual step, which is the
@@ -251,9 +249,8 @@ CBG_DEV float byte_to_unit(uint32_t word, int b) {
   const float q = __fmul_rn(fv, kInv255);
   return fmaf(fmaf(-q, 255.0f, fv), kInv255, q);
 }
-template <bool kChw, int kC, bool kS8 = false>
+template <bool kChw, int kC>
 __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(DetectFrameArgs a) {
-  static_assert(!kS8 || (kChw && kC == 3), "8-bit state shadow: CHW state, 3 channels");
   constexpr int CM = kC ? kC : 4;  // register arrays
   const int s = blockIdx.y;
   const int CC = kC ? kC : a.C;
@@ -272,14 +269,7 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(Detec
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
     const long long p0 = q << 2;
     // 4 pixels x C bytes = C words, 4-byte aligned (byte offset 4*C*q)
-    uint32_t wd[CM], sw[CM];
-    if constexpr (kS8) {
-      if (!boot) {
-        const uint32_t* ssrc = reinterpret_cast<const uint32_t*>(s8 + p0 * CC);
-#pragma unroll
-        for (int i = 0; i < CM; ++i) sw[i] = ssrc[i];
-      }
-    }
+    uint32_t wd[CM];
     const uint32_t* src = reinterpret_cast<const uint32_t*>(x8 + p0 * CC);
 #pragma unroll
     for (int i = 0; i < CM; ++i) wd[i] = i < CC ? __ldg(src + i) : 0u;
@@ -298,12 +288,7 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(Detec
     uint32_t ch = 0;
     float sv[4][CM];
     if (!boot) {
-      if constexpr (kS8) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-#pragma unroll
-          for (int c = 0; c < CM; ++c) sv[j][c] = byte_to_unit(sw[(j * CM + c) >> 2], j * CM + c);
-      } else if constexpr (kChw) {
+      if constexpr (kChw) {
 #pragma unroll
         for (int c = 0; c < CM; ++c)
           if (c < CC) {
@@ -348,28 +333,97 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(Detec
             *reinterpret_cast<float4*>(st + (p0 + j) * 4) = make_float4(px[j][0], CM > 1 ? px[j][1 % CM] : 0.f, CM > 2 ? px[j][2 % CM] : 0.f, CM > 3 ? px[j][3 % CM] : 0.f);
       }
     }
-    // the 8-bit shadow: the frame's words on a full update; the changed
-    // pixels' bytes merged into the old words otherwise (kS8 only: without it
-    // the shadow is stale until the stream's next full update)
-    if (s8 && (write_all || (kS8 && ch))) {
+    // the 8-bit shadow takes the frame's words on a full update; this kernel
+    // does not track it at changed pixels, so it is valid again only after the
+    // stream's next full update (detect_frame_s8_kernel keeps it current)
+    if (s8 && write_all) {
       uint32_t* sdst = reinterpret_cast<uint32_t*>(s8 + p0 * CC);
 #pragma unroll
-      for (int i = 0; i < CM; ++i) {
-        if (i >= CC) continue;
-        uint32_t v = wd[i];
-        if constexpr (kS8) {
-          if (!write_all) {
-            uint32_t keep = 0;  // bytes of unchanged pixels keep the old state
-#pragma unroll
-            for (int k = 0; k < 4; ++k)
-              if (!((ch >> ((4 * i + k) / CM)) & 1u)) keep |= 0xFFu << (8 * k);
-            v = (v & ~keep) | (sw[i] & keep);
-          }
-        }
-        sdst[i] = v;
-      }
+      for (int i = 0; i < CM; ++i)
+        if (i < CC) sdst[i] = wd[i];
     }
     if (ch) {
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        if ((ch >> j) & 1u) m[p0 + j] = e;
+    }
+  }
+  warp_amax(a.amax ? a.amax + s : nullptr, vmax);
+}
+
+// The 8-bit shadow path on its own (3 channels, CHW fp32 state): everything it
+// reads is bytes (12 B of frame + 12 B of shadow per 4 pixels), so each thread
+// batches kQ quads, a grid stride apart, with all their loads issued first.
+template <int kQ>
+__global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_s8_kernel(DetectFrameArgs a) {
+  const int s = blockIdx.y;
+  const uint8_t e = epoch8(*a.frame);
+  const bool boot = a.boot[s] != 0;
+  const long long HW = static_cast<long long>(a.H) * a.W;
+  const uint8_t* x8 = *a.x8_slot + static_cast<long long>(s) * 3 * HW;
+  uint8_t* s8 = a.state8 + static_cast<long long>(s) * 3 * HW;
+  float* st = a.state + static_cast<long long>(s) * 3 * HW;
+  uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  const bool write_all = boot || !a.closed_loop;
+  const float tau = a.tau[s];
+  const long long n4 = HW >> 2;
+  const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  float vmax = 0.0f;
+  for (long long q0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q0 < n4; q0 += kQ * stride) {
+    uint32_t wd[kQ][3], sw[kQ][3];
+#pragma unroll
+    for (int u = 0; u < kQ; ++u) {
+      const long long q = q0 + u * stride;
+      if (q < n4) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(x8 + 12 * q);
+        const uint32_t* ssrc = reinterpret_cast<const uint32_t*>(s8 + 12 * q);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          wd[u][i] = __ldg(src + i);
+          sw[u][i] = boot ? 0u : ssrc[i];
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kQ; ++u) {
+      const long long q = q0 + u * stride;
+      if (q >= n4) continue;
+      const long long p0 = q << 2;
+      uint32_t ch = 0;
+      if (!boot) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const int b = 3 * j + c;
+            if ((tau < 0.0f || wd[u][b >> 2] != sw[u][b >> 2]) &&  // equal words: |x - s| = 0 <= tau
+                fabsf(byte_to_unit(wd[u][b >> 2], b) - byte_to_unit(sw[u][b >> 2], b)) > tau)
+              ch |= 1u << j;
+          }
+      }
+      if (!(write_all || ch)) continue;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float v[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const int b = 3 * j + c;
+          const bool take = write_all || ((ch >> j) & 1u);
+          v[j] = byte_to_unit(take ? wd[u][b >> 2] : sw[u][b >> 2], b);
+          if (take) vmax = fmaxf(vmax, v[j]);
+        }
+        *reinterpret_cast<float4*>(st + c * HW + p0) = make_float4(v[0], v[1], v[2], v[3]);
+      }
+      uint32_t* sdst = reinterpret_cast<uint32_t*>(s8 + 12 * q);
+#pragma unroll
+      for (int i = 0; i < 3; ++i) {
+        uint32_t keep = 0;  // bytes of unchanged pixels keep the old state
+        if (!write_all)
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if (!((ch >> ((4 * i + k) / 3)) & 1u)) keep |= 0xFFu << (8 * k);
+        sdst[i] = (wd[u][i] & ~keep) | (sw[u][i] & keep);
+      }
 #pragma unroll
       for (int j = 0; j < 4; ++j)
         if ((ch >> j) & 1u) m[p0 + j] = e;
@@ -873,7 +927,7 @@ void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
     if (HW % 4 == 0 && (a.state_chw || a.Cs == 4)) {
       dim3 grid(2 * blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
       if (a.state_chw && a.C == 3 && a.use_state8 && a.state8)
-        detect_frame_u8_kernel<true, 3, true><<<grid, kFrameThreads, 0, st>>>(a);
+        detect_frame_s8_kernel<2><<<grid, kFrameThreads, 0, st>>>(a);
       else if (a.state_chw && a.C == 3) detect_frame_u8_kernel<true, 3><<<grid, kFrameThreads, 0, st>>>(a);
       else if (a.state_chw) detect_frame_u8_kernel<true, 0><<<grid, kFrameThreads, 0, st>>>(a);
       else detect_frame_u8_kernel<false, 0><<<grid, kFrameThreads, 0, st>>>(a);

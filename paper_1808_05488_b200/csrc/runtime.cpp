@@ -683,7 +683,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
   // those maps exist (their GEMMs may still run), then joined back
   auto map_compaction = [&](int k, const DilateCompactArgs& dc) {
     const NodeDesc& dk = nodes_[k].d;
-    bool side = side_dc_;
+    bool side = side_dc_ && !timing_;  // per-kernel timing keeps every kernel on the ctx stream (serial attribution)
     for (int in : dk.inputs) side = side && nodes_[map_owner(in)].d.kind != kExternal;
     if (!side) {
       timed(dk.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });

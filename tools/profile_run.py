@@ -22,6 +22,7 @@ ap.add_argument("--objects", type=int, default=6)
 ap.add_argument("--object-size", type=int, default=40)
 ap.add_argument("--velocity", type=int, default=4)
 ap.add_argument("--dense", action="store_true")
+ap.add_argument("--ingest", choices=["u8", "f32"], default="u8", help="frame format, as bench.py --ingest")
 a = ap.parse_args()
 S, H, W = a.streams, a.height, a.width
 spec = cbi.make_seg_spec(1, H, W)
@@ -30,7 +31,11 @@ frames = np.stack([cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, a.frames, a.ob
 net = cbi.convert_to_cb(spec, [0.05] * 5, n_streams=S)
 if a.dense:
     net.set_dense(True)
+pnm = cbi.to_pnm8(frames)  # [T, S, H, W, C]: what bench.py feeds (u8), or its byte/255 (f32)
 for t in range(a.frames):
-    net.enqueue(np.ascontiguousarray(frames[t]))
+    if a.ingest == "u8":
+        net.enqueue_u8(np.ascontiguousarray(pnm[t]))
+    else:
+        net.enqueue(np.ascontiguousarray(cbi.from_pnm8(pnm[t])))
 net.synchronize()
 print("counts L1..L7 (stream 0):", net.counts()[:, 0].tolist())
