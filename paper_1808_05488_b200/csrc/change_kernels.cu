@@ -472,9 +472,30 @@ __global__ void __launch_bounds__(kThreads) detect_frame_u8_scalar_kernel(Detect
 template <int kCache>
 __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListArgs a, int glog) {
   const int s = blockIdx.y;
-  const uint8_t e = epoch8(*a.frame);
+  const uint32_t fno = *a.frame;
+  const uint8_t e = epoch8(fno);
   const bool boot = a.boot[s] != 0;
-  const bool dense = boot || a.prod_idx == nullptr || (a.dense != nullptr && *a.dense != 0);
+  // pre-split copy: if the GEMM's exponent moved since the copy was split,
+  // this frame rewrites the whole copy (dense walk; dense detection gives the
+  // sparse walk's result)
+  const bool has_split = a.split != nullptr;
+  int e_now = 0;
+  bool resplit = false;
+  if (has_split) {
+    e_now = f16_scale_exp(__ldg(a.amax_in + s));
+    const uint32_t par = fno & 1u;
+    resplit = a.split_e[(par ^ 1u) * a.S + s] != e_now;
+    if (blockIdx.x == 0 && threadIdx.x == 0) a.split_e[par * a.S + s] = e_now;
+  }
+  const float xs = exp2i(-e_now);
+  const unsigned long long xs2 = pack_f32x2(xs, xs);
+  auto put_split = [&](long long off, float4 v) {  // off: element offset of the 4-channel chunk
+    uint4 w;
+    f16_split2(v.x, v.y, xs2, w.x, w.z);
+    f16_split2(v.z, v.w, xs2, w.y, w.w);
+    *reinterpret_cast<uint4*>(a.split + off) = w;
+  };
+  const bool dense = boot || resplit || a.prod_idx == nullptr || (a.dense != nullptr && *a.dense != 0);
   const long long HW = static_cast<long long>(a.H) * a.W;
   const long long n = dense ? HW : a.prod_count[s];
   const float* x = a.x + static_cast<long long>(s) * HW * a.Cs;
@@ -539,9 +560,18 @@ __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListAr
     if (active && (any || write_all)) {
 #pragma unroll
       for (int j = 0; j < kCache; ++j)
-        if (sub + j * g < nv) *reinterpret_cast<float4*>(sp + 4 * (sub + j * g)) = xc[j];
-      for (int v = sub + kCache * g; v < nv; v += g)
-        *reinterpret_cast<float4*>(sp + 4 * v) = ldg_nc_f4(xp + 4 * v);
+        if (sub + j * g < nv) {
+          *reinterpret_cast<float4*>(sp + 4 * (sub + j * g)) = xc[j];
+          if (has_split) put_split(static_cast<long long>(s) * HW * a.Cs + p * a.Cs + 4 * (sub + j * g), xc[j]);
+        }
+      for (int v = sub + kCache * g; v < nv; v += g) {
+        const float4 xv = ldg_nc_f4(xp + 4 * v);
+        *reinterpret_cast<float4*>(sp + 4 * v) = xv;
+        if (has_split) put_split(static_cast<long long>(s) * HW * a.Cs + p * a.Cs + 4 * v, xv);
+      }
+    } else if (active && resplit) {  // unchanged pixel, new exponent: split the kept state
+      for (int v = sub; v < nv; v += g)
+        put_split(static_cast<long long>(s) * HW * a.Cs + p * a.Cs + 4 * v, *reinterpret_cast<const float4*>(sp + 4 * v));
     }
     if (active && any && !boot && sub == 0) m[p] = e;
   }

@@ -4,6 +4,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #define CBG_DEV __device__ __forceinline__
@@ -374,5 +375,42 @@ __host__ __device__ constexpr uint32_t umma_idesc_f16(int M, int N) {
          | (static_cast<uint32_t>(N >> 3) << 17)     // n_dim
          | (static_cast<uint32_t>(M >> 4) << 24);    // m_dim
 }
+
+// ---- 3xFP16 operand split (shared by the GEMM and the detect kernels that
+// keep a pre-split copy of a GEMM's input state) ---------------------------------
+CBG_DEV unsigned long long pack_f32x2(float lo, float hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
+  return r;
+}
+// Two fp32 values -> packed fp16 hi and lo parts of (x * 2^-e), packed fp32x2
+// arithmetic: x*s exact (power of two), hi = fp16_rn, lo = fp16_rn(x*s - hi)
+// (ptxas may fuse the multiply into the subtraction: x*s is exact, so the
+// result is the same).
+CBG_DEV void f16_split2(float x0, float x1, unsigned long long s2, uint32_t& hi, uint32_t& lo) {
+  unsigned long long p;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(pack_f32x2(x0, x1)), "l"(s2));
+  float p0, p1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(p0), "=f"(p1) : "l"(p));
+  const __half2 hh = __floats2half2_rn(p0, p1);
+  const float2 hf = __half22float2(hh);
+  unsigned long long d;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(p), "l"(pack_f32x2(hf.x, hf.y)));
+  float d0, d1;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
+  const __half2 ll = __floats2half2_rn(d0, d1);
+  hi = *reinterpret_cast<const uint32_t*>(&hh);
+  lo = *reinterpret_cast<const uint32_t*>(&ll);
+}
+
+// Exponent e with bound * 2^-e < 2^15 (fp16 operands stay finite), clamped so
+// 2^-e and 2^e are normal floats.
+CBG_DEV int f16_scale_exp(float bound) {
+  const uint32_t E = (__float_as_uint(bound) >> 23) & 0xFFu;
+  if (!(bound > 0.0f) || E == 0xFFu) return 0;
+  int e = static_cast<int>(E) - 127 - 14;
+  return e < -126 ? -126 : e > 126 ? 126 : e;
+}
+CBG_DEV float exp2i(int e) { return __uint_as_float(static_cast<uint32_t>(e + 127) << 23); }
 
 }  // namespace cbg

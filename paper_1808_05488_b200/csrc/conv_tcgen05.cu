@@ -73,8 +73,9 @@ namespace {
 constexpr int kPrecTF32 = 0;
 constexpr int kPrecF16 = 1;        // fp16 split, A staged through shared memory by fetch warps
 constexpr int kPrecF16Direct = 2;  // fp16 split, A loaded by the convert warps straight from global
+constexpr int kPrecF16Presplit = 3;  // direct, A already split by the layer's detect (ConvGemmArgs::src_presplit)
 __host__ __device__ constexpr bool is_f16(int p) { return p != kPrecTF32; }
-__host__ __device__ constexpr bool is_direct(int p) { return p == kPrecF16Direct; }
+__host__ __device__ constexpr bool is_direct(int p) { return p == kPrecF16Direct || p == kPrecF16Presplit; }
 
 // Warp roles per N tile (21 warps = 672 threads either way):
 //   N <= 128: 4 epilogue, 8 fetch (2 groups), 8 convert (2 groups), 1 MMA
@@ -142,41 +143,6 @@ struct Cfg {
   static constexpr uint32_t kAColBase = kNAcc * NPAD;  // first A stage column
   static_assert(kNAcc * NPAD + kStages * kACols <= 512, "TMEM budget");
 };
-
-CBG_DEV unsigned long long pack_f32x2(float lo, float hi) {
-  unsigned long long r;
-  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(lo), "f"(hi));
-  return r;
-}
-// Two fp32 values -> packed fp16 hi and lo parts of (x * 2^-e), packed fp32x2
-// arithmetic: x*s exact (power of two), hi = fp16_rn, lo = fp16_rn(x*s - hi)
-// (ptxas may fuse the multiply into the subtraction: x*s is exact, so the
-// result is the same).
-CBG_DEV void f16_split2(float x0, float x1, unsigned long long s2, uint32_t& hi, uint32_t& lo) {
-  unsigned long long p;
-  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(p) : "l"(pack_f32x2(x0, x1)), "l"(s2));
-  float p0, p1;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(p0), "=f"(p1) : "l"(p));
-  const __half2 hh = __floats2half2_rn(p0, p1);
-  const float2 hf = __half22float2(hh);
-  unsigned long long d;
-  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(p), "l"(pack_f32x2(hf.x, hf.y)));
-  float d0, d1;
-  asm("mov.b64 {%0, %1}, %2;" : "=f"(d0), "=f"(d1) : "l"(d));
-  const __half2 ll = __floats2half2_rn(d0, d1);
-  hi = *reinterpret_cast<const uint32_t*>(&hh);
-  lo = *reinterpret_cast<const uint32_t*>(&ll);
-}
-
-// Exponent e with bound * 2^-e < 2^15 (fp16 operands stay finite), clamped so
-// 2^-e and 2^e are normal floats.
-CBG_DEV int f16_scale_exp(float bound) {
-  const uint32_t E = (__float_as_uint(bound) >> 23) & 0xFFu;
-  if (!(bound > 0.0f) || E == 0xFFu) return 0;
-  int e = static_cast<int>(E) - 127 - 14;
-  return e < -126 ? -126 : e > 126 ? 126 : e;
-}
-CBG_DEV float exp2i(int e) { return __uint_as_float(static_cast<uint32_t>(e + 127) << 23); }
 
 __host__ __device__ constexpr int tail_bytes(int stages, int KB, int S, int nbias, int npad, bool direct) {
   return 8 * (3 * stages + 4) + 16 + kBM * 8 + (S + 1) * 4 + 16 + 4 * epi_buf_floats(npad) + 4 * nbias +
@@ -406,8 +372,15 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
 #pragma unroll
             for (int b = 0; b < 2; ++b) {  // row a, a+8 -> registers 0-1 / 2-3 (+4 for chunk c+4)
               const float4 x = v[2 * h + b][j];
-              f16_split2(x.x, x.y, xs2, hi[4 * j + 2 * b], lo[4 * j + 2 * b]);
-              f16_split2(x.z, x.w, xs2, hi[4 * j + 2 * b + 1], lo[4 * j + 2 * b + 1]);
+              if constexpr (PREC == kPrecF16Presplit) {  // the detect split the chunk: {hi01, hi23, lo01, lo23}
+                hi[4 * j + 2 * b] = __float_as_uint(x.x);
+                hi[4 * j + 2 * b + 1] = __float_as_uint(x.y);
+                lo[4 * j + 2 * b] = __float_as_uint(x.z);
+                lo[4 * j + 2 * b + 1] = __float_as_uint(x.w);
+              } else {
+                f16_split2(x.x, x.y, xs2, hi[4 * j + 2 * b], lo[4 * j + 2 * b]);
+                f16_split2(x.z, x.w, xs2, hi[4 * j + 2 * b + 1], lo[4 * j + 2 * b + 1]);
+              }
             }
           tmem_st_16x256b_x2(ta + (static_cast<uint32_t>(16 * h) << 16), hi);
           tmem_st_16x256b_x2(ta + (static_cast<uint32_t>(16 * h) << 16) + C::kALo, lo);
@@ -720,7 +693,7 @@ int conv_gemm_read_trace(unsigned long long* host, int n) {
 }
 
 int conv_gemm_stages(int npad, int prec) {
-  return prec == kPrecF16Direct ? stages_prec<kPrecF16Direct>(npad)
+  return is_direct(prec) ? stages_prec<kPrecF16Direct>(npad)
          : prec == kPrecF16     ? stages_prec<kPrecF16>(npad)
                                 : stages_prec<kPrecTF32>(npad);
 }
@@ -732,7 +705,8 @@ int conv_gemm_smem_bytes(int npad, int KB, int S, int prec, int n_tiles) {
 }
 
 void launch_conv_gemm(const ConvGemmArgs& a, cudaStream_t st) {
-  if (a.prec == kPrecF16Direct) launch_prec<kPrecF16Direct>(a, st);
+  if (a.prec == kPrecF16Direct && a.src_presplit) launch_prec<kPrecF16Presplit>(a, st);
+  else if (a.prec == kPrecF16Direct) launch_prec<kPrecF16Direct>(a, st);
   else if (a.prec == kPrecF16) launch_prec<kPrecF16>(a, st);
   else launch_prec<kPrecTF32>(a, st);
 }

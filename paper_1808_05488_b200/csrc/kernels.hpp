@@ -56,6 +56,12 @@ struct DetectListArgs {
   int Cs, H, W, S;
   const float* tau;          // device [S]
   int closed_loop;
+  // pre-split copy of the state for a 3xFP16 GEMM that reads it (nullable):
+  // per 4 channels {hi01, hi23, lo01, lo23} fp16 pairs at the state's byte
+  // offsets, split with e = f16_scale_exp(amax_in[s]) exactly as the GEMM would.
+  uint32_t* split;
+  int32_t* split_e;          // [2][S] exponent of the whole copy, by frame parity
+  const float* amax_in;      // [S] the GEMM's operand bound
 };
 void launch_detect_list(const DetectListArgs& a, cudaStream_t st);
 
@@ -109,6 +115,7 @@ void launch_join(const JoinArgs& a, cudaStream_t st);
 // update_output: dense.cpp:44-112, layers.cpp:10-31).
 struct ConvGemmArgs {
   const float* src;        // [S][Hin][Win][Cs] column source (state or producer output)
+  int src_presplit;        // src is the detect's pre-split copy (DetectListArgs::split), not fp32
   float* out;              // [S][Hout][Wout][Co4]
   const int32_t* idx;      // [S][Hout*Wout]
   const int32_t* count;    // [S]

@@ -501,6 +501,10 @@ std::unique_ptr<Net> Net::clone() const {
     if (a.out.bytes) CK(cudaMemcpy(b.out.p, a.out.p, a.out.bytes, cudaMemcpyDeviceToDevice));
     if (a.state.bytes) CK(cudaMemcpy(b.state.p, a.state.p, a.state.bytes, cudaMemcpyDeviceToDevice));
     if (a.state8.bytes) CK(cudaMemcpy(b.state8.p, a.state8.p, a.state8.bytes, cudaMemcpyDeviceToDevice));
+    if (a.split.bytes) {
+      CK(cudaMemcpy(b.split.p, a.split.p, a.split.bytes, cudaMemcpyDeviceToDevice));
+      CK(cudaMemcpy(b.split_e.p, a.split_e.p, a.split_e.bytes, cudaMemcpyDeviceToDevice));
+    }
   }
   c->s8_valid_ = s8_valid_;
   c->s8_pending_ = s8_pending_;
@@ -582,6 +586,19 @@ void Net::build() {
         r.state.alloc(static_cast<size_t>(S_) * HWi * (r.state_chw ? d.Ci : r.Csi) * sizeof(float));
         if (r.state_chw && d.Ci == 3 && HWi % 4 == 0) r.state8.alloc(static_cast<size_t>(S_) * HWi * 3 + 16);
         r.inmap.alloc(static_cast<size_t>(S_) * HWi + 16);
+        // the direct 3xFP16 GEMM of a k x k layer (k > 1) gathers every input value
+        // k^2 times: its detect keeps the state pre-split, once per changed pixel
+        static const bool presplit = [] {
+          const char* e = std::getenv("CBG_PRESPLIT");
+          return !(e && std::atoi(e) == 0);
+        }();
+        if (presplit && !r.exact && r.prec == 2 && d.inputs[0] >= 0 && nodes_[d.inputs[0]].d.kind != kExternal &&
+            c.kernel_h * c.kernel_w > 1) {
+          r.split.alloc(r.state.bytes);
+          r.split_e.alloc(2 * static_cast<size_t>(S_) * sizeof(int32_t));
+          CK(cudaMemset(r.split_e.p, 0x7f, r.split_e.bytes));  // no exponent yet: the first frame splits all
+          CK(cudaStreamSynchronize(nullptr));
+        }
       }
       if (!reuse) {
         if (d.policy == CBG_POLICY_DETECT || d.policy == CBG_POLICY_PROPAGATE)
@@ -719,7 +736,9 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
                            ext ? nullptr : prod->idx, counts + prod->count_slot * S_, frame, boot,
                            rescan_now_.as<uint8_t>() + i, r.Csi, d.Hi, d.Wi, S_,
                            taus_.as<float>() + static_cast<size_t>(i) * S_,
-                           topo_.mode == CBG_MODE_CLOSEDLOOP};
+                           topo_.mode == CBG_MODE_CLOSEDLOOP,
+                           r.split.bytes ? r.split.as<uint32_t>() : nullptr, r.split_e.as<int32_t>(),
+                           amax_entry(amax_origin(src))};
           timed(d.name + ".detect", [&] { launch_detect_list(a, st); });
         }
         // ClosedLoop reads the state; FeedForward's state equals x after detection.
@@ -797,6 +816,10 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
       }
       ConvGemmArgs g{};
       g.src = column_src;
+      if (r.split.bytes) {  // the detect's pre-split copy of the same state
+        g.src = static_cast<const float*>(r.split.p);
+        g.src_presplit = 1;
+      }
       g.out = r.out.as<float>();
       g.idx = r.idx;
       g.count = counts + r.count_slot * S_;

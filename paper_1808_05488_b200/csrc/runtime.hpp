@@ -100,6 +100,7 @@ struct NodeRT {
   DevBuf wimg, ktab, bias, wraw; // wraw: [Cout][Cin*kh*kw] fp32 for the exact path
   DevBuf state, inmap;           // Detect policy
   DevBuf state8;                 // first layer, 8-bit ingest: byte shadow of the state (DetectFrameArgs::state8)
+  DevBuf split, split_e;         // 3xFP16 GEMM input: pre-split copy of the state (DetectListArgs::split)
   // every node
   DevBuf out;                    // [S][H][W][Cs]
   DevBuf outmap_own, idx_own;
