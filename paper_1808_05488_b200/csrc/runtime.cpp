@@ -588,10 +588,8 @@ void Net::build() {
         r.inmap.alloc(static_cast<size_t>(S_) * HWi + 16);
         // the direct 3xFP16 GEMM of a k x k layer (k > 1) gathers every input value
         // k^2 times: its detect keeps the state pre-split, once per changed pixel
-        static const bool presplit = [] {
-          const char* e = std::getenv("CBG_PRESPLIT");
-          return !(e && std::atoi(e) == 0);
-        }();
+        const char* ps_env = std::getenv("CBG_PRESPLIT");  // read per build: A/B in one process
+        const bool presplit = !(ps_env && std::atoi(ps_env) == 0);
         if (presplit && !r.exact && r.prec == 2 && d.inputs[0] >= 0 && nodes_[d.inputs[0]].d.kind != kExternal &&
             c.kernel_h * c.kernel_w > 1) {
           r.split.alloc(r.state.bytes);
