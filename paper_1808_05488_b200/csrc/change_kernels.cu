@@ -665,9 +665,12 @@ __global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompa
   const int in_lo = max(0, r0 * a.stride - a.pad);
   const int in_hi = min(a.Hin, (r1 - 1) * a.stride - a.pad + a.kh);
   const int nin = max(0, in_hi - in_lo);
-  uint32_t* s_in = smw;                 // [nin][nwi]
   uint32_t* s_h = smw + nin * nwi;      // [nin][nwo]
   uint32_t* s_out = s_h + nin * nwo;    // [nrows][nwo]
+  // identity window (1x1, stride 1, same size: joins, 1x1 convs): the staged
+  // rows are the output rows, no dilation phases
+  const bool ident = a.kh == 1 && a.kw == 1 && a.stride == 1 && a.pad == 0 && a.Hin == a.Hout && a.Win == a.Wout;
+  uint32_t* s_in = ident ? s_out : smw;  // [nin][nwi]
   const int nout = nrows * nwo;
 
   if (boot) {
@@ -712,6 +715,7 @@ __global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompa
       }
       s_in[i] = word;
     }
+    if (!ident) {
     __syncthreads();
   DCT(1);
     // 2. horizontal dilation (+ stride subsampling) per staged row
@@ -776,6 +780,7 @@ __global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompa
       for (int jj = ja; jj < jb; ++jj) v |= s_h[(jj - in_lo) * nwo + wo];
       s_out[i] = v;
     }
+    }  // !ident
   }
   __syncthreads();
   DCT(3);
