@@ -514,12 +514,21 @@ __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListAr
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
 
-  for (long long base = (static_cast<long long>(blockIdx.x) * wpb + warp) * gpw; base < n;
-       base += static_cast<long long>(gridDim.x) * wpb * gpw) {
+  const long long step = static_cast<long long>(gridDim.x) * wpb * gpw;
+  const long long base0 = (static_cast<long long>(blockIdx.x) * wpb + warp) * gpw;
+  // the next iteration's list entry is loaded one iteration ahead, so the
+  // list -> data dependency costs one memory latency per warp, not one per pixel
+  int p_next = (list && base0 + (lane >> glog) < n) ? __ldg(list + base0 + (lane >> glog)) : 0;
+  for (long long base = base0; base < n; base += step) {
     const long long k = base + (lane >> glog);
     const bool active = k < n;
     long long p = 0;
-    if (active) p = list ? list[k] : k;
+    if (list) {
+      p = p_next;
+      if (k + step < n) p_next = __ldg(list + k + step);
+    } else {
+      p = k;
+    }
     const float* xp = x + p * a.Cs;
     float* sp = st + p * a.Cs;
     // up to kCache float4 of x per lane stay in registers for the state write;
