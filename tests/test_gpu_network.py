@@ -284,3 +284,37 @@ def test_presplit_copy_follows_growing_magnitudes(gpu, monkeypatch):
                 assert np.array_equal(net.node_output(i, s), plain.node_output(i, s)), (t, s, i)
             for i in range(3):
                 assert counts[i, s] == refs[s].stats(i)["changed_px"], (t, s, i)
+
+
+def test_presplit_copy_under_control_operations(gpu, monkeypatch):
+    """Pre-split vs GEMM-side split, bit-identical on every node while the
+    sequence goes through the control paths that change which pixels the
+    detect walks: a threshold decrease (dense rescan), a per-stream reset, a
+    forced full update, dense mode on and off, and 8-bit frames."""
+    S, H, W, T = 3, 48, 64, 12
+    spec = cbi.make_seg_spec(9, H, W)
+    taus = [0.05] * 5
+    raw = np.stack([seq(H, W, n=T, seed=950 + s, noise=0.02) for s in range(S)], axis=1)
+    pnm = cbi.to_pnm8(raw)
+    f32 = cbi.from_pnm8(pnm)
+    net = cbi.convert_to_cb(spec, taus, n_streams=S)
+    monkeypatch.setenv("CBG_PRESPLIT", "0")
+    plain = cbi.convert_to_cb(spec, taus, n_streams=S)
+    for t in range(T):
+        for n_ in (net, plain):
+            if t == 3:
+                n_.set_thresholds([0.02] * 5)   # tau decreased: dense rescan next frame
+            if t == 5:
+                n_.reset(2)
+            if t == 7:
+                n_.set_dense(True)
+            if t == 9:
+                n_.set_dense(False)
+            if t % 2:
+                n_.enqueue_u8(pnm[t])
+            else:
+                n_.enqueue(f32[t], _lib.FWD_FORCE_FULL if t == 6 else 0)
+        assert np.array_equal(net.counts(), plain.counts()), t
+        for s in range(S):
+            for i in range(len(net.nodes())):
+                assert np.array_equal(net.node_output(i, s), plain.node_output(i, s)), (t, s, i)
