@@ -811,7 +811,7 @@ __global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompa
   __syncthreads();
   DCT(5);
 
-  // 6. scatter the row-major index list and tag the output map
+  // 6. scatter the tile's row-major run of the index list and tag the output map
   int pos = s_prefix + off;
   int32_t* idx = a.idx + s * HWout;
   uint8_t* om = a.out_map + s * HWout;

@@ -5,7 +5,7 @@
 // layer of the scene-labeling net), the partial im2col + gemm + update_output
 // of the reference (dense.cpp:44-112, layers.cpp:10-31):
 //
-//   for every changed output pixel p (row-major index list, count on device)
+//   for every changed output pixel p (index list and count on device)
 //     acc[o] = 0;  for r ascending: acc[o] = acc[o] + K[o][r] * X[r][p]
 //     prev_output[p][o] = act(acc[o] + b[o])
 //

@@ -3,7 +3,7 @@
 // Replaces, in one persistent kernel, the reference's partial im2col + GEMM +
 // output update (dense.cpp:44-112, layers.cpp:10-31, layers.cpp:112-114):
 //
-//   for every changed output pixel p (row-major index list, count on device)
+//   for every changed output pixel p (index list and count on device)
 //     Y[p, :] = act( sum_k X[p, k] * K[:, k] + bias )      scattered into
 //     prev_output[p, :]  (NHWC: one contiguous Cout vector per pixel)
 //

@@ -66,8 +66,9 @@ struct DetectListArgs {
 void launch_detect_list(const DetectListArgs& a, cudaStream_t st);
 
 // Window dilation (reference change.cpp:45-67, also CB pooling's map,
-// layers.cpp:163) fused with the ordered stream compaction of the output map
-// into the row-major index list (reference extract_indexes, change.cpp:77-84).
+// layers.cpp:163) fused with the stream compaction of the output map into the
+// index list (reference extract_indexes, change.cpp:77-84): row-major inside a
+// tile of output rows, tiles in completion order (Net::read_changes sorts).
 // Up to 4 input maps are OR-ed first (join nodes, network.cpp:366-373).
 struct DilateCompactArgs {
   const uint8_t* in_map[4];  // [S][Hin][Win] epoch-tagged
