@@ -390,16 +390,20 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_s8_kernel(Detec
       if (q >= n4) continue;
       const long long p0 = q << 2;
       uint32_t ch = 0;
-      if (!boot) {
+      // a quad whose 12 bytes equal the shadow cannot change (|x - s| = 0 <= tau):
+      // the common case skips the per-byte comparisons
+      const bool same = (wd[u][0] == sw[u][0]) & (wd[u][1] == sw[u][1]) & (wd[u][2] == sw[u][2]);
+      if (!boot && (!same || tau < 0.0f)) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < 4; ++j) {
+          bool cj = false;
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             const int b = 3 * j + c;
-            if ((tau < 0.0f || wd[u][b >> 2] != sw[u][b >> 2]) &&  // equal words: |x - s| = 0 <= tau
-                fabsf(byte_to_unit(wd[u][b >> 2], b) - byte_to_unit(sw[u][b >> 2], b)) > tau)
-              ch |= 1u << j;
+            cj |= fabsf(byte_to_unit(wd[u][b >> 2], b) - byte_to_unit(sw[u][b >> 2], b)) > tau;
           }
+          ch |= static_cast<uint32_t>(cj) << j;
+        }
       }
       if (!(write_all || ch)) continue;
 #pragma unroll
