@@ -66,9 +66,6 @@ CBG_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity), "n"(CBG_MBAR_SUSPEND_NS)
       : "memory");
 }
-// Make generic-proxy shared-memory writes visible to the async proxy (UMMA reads).
-CBG_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-
 // 1-D bulk copy global -> shared on the TMA engine, completing on an mbarrier.
 CBG_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -76,35 +73,6 @@ CBG_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar)
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
-}
-
-// Multicast 1-D bulk copy: the bytes land at the same CTA-relative offset in
-// every CTA of cta_mask and complete_tx is signalled on the mbarrier at the
-// same offset in each of them.
-CBG_DEV void bulk_g2s_multicast(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint16_t cta_mask) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1], %2, [%3], "
-      "%4;" ::"r"(smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "h"(cta_mask)
-      : "memory");
-}
-CBG_DEV uint32_t cluster_ctarank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %cluster_ctarank;" : "=r"(r));
-  return r;
-}
-CBG_DEV void cluster_sync_all() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-// Arrive on the mbarrier at the same smem offset in CTA `rank` of the cluster.
-CBG_DEV void mbar_arrive_remote(uint64_t* bar, uint32_t rank) {
-  uint32_t remote;
-  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(smem_u32(bar)), "r"(rank));
-  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
-}
-
-CBG_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
 }
 
 // ---- cp.async (LDGSTS): 16-B async copy with zero-fill (src_bytes = 0) -----------
@@ -129,29 +97,11 @@ CBG_DEV uint2 lds_u2(uint32_t addr) {
   return v;
 }
 CBG_DEV void warp_sync_mem() { asm volatile("bar.warp.sync 0xffffffff;" ::: "memory"); }
-CBG_DEV uint32_t lds_u32(uint32_t addr) {
-  uint32_t v;
-  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
-  return v;
-}
 // Arrive on an mbarrier once all prior cp.async of this thread complete (the
 // thread itself does not wait); the barrier's expected count covers it (.noinc).
 CBG_DEV void cp_async_mbar_arrive(uint64_t* bar) {
   asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
-CBG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-CBG_DEV void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-
-// ---- tf32 split (3xTF32: x = hi + lo, both representable in tf32) -------------------
-CBG_DEV uint32_t tf32_rna(float x) {
-  uint32_t r;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-  return r;
-}
-
 // ---- tcgen05 ------------------------------------------------------------------------
 CBG_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
@@ -165,56 +115,6 @@ CBG_DEV void tmem_dealloc(uint32_t taddr, uint32_t ncols) {
 CBG_DEV void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 CBG_DEV void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// D[tmem] (+)= A[smem] * B[smem]^T, kind::tf32, fp32 accumulate, cta_group::1.
-CBG_DEV void umma_tf32(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// Warp-converged variants: every lane executes the asm with warp-uniform
-// operands and elect.sync picks the issuing lane, so descriptors stay in
-// uniform registers (a lane-0-only branch forces per-MMA R2UR waterfall loops,
-// measured at ~95 cycles per tcgen05.mma).
-CBG_DEV void umma_tf32_elect(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred p, e;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.ne.b32 p, %4, 0;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
-      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
-// One K=32 block of the 3xTF32 product (K-major SW128 operands): 4 k-steps of
-// 8 tf32 (32 B) x 3 products, 12 tcgen05.mma under a single elect.sync.
-// Descriptor start addresses advance by 2 (16-B units) per k-step.
-CBG_DEV void umma_tf32x3_kblock(uint32_t d_tmem, uint64_t a_hi, uint64_t a_lo, uint64_t b_hi, uint64_t b_lo,
-                                uint32_t idesc, uint32_t accumulate) {
-  asm volatile(
-      "{\n\t.reg .pred e, p;\n\t.reg .b64 ah, al, bh, bl;\n\t"
-      "elect.sync _|e, 0xffffffff;\n\t"
-      "setp.ne.b32 p, %6, 0;\n\t"
-      "mov.b64 ah, %1;\n\tmov.b64 al, %2;\n\tmov.b64 bh, %3;\n\tmov.b64 bl, %4;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, p;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, 1;\n\t"
-      "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, 1;\n\t"
-      "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, 1;\n\t"
-      "add.s64 ah, ah, 2;\n\tadd.s64 al, al, 2;\n\tadd.s64 bh, bh, 2;\n\tadd.s64 bl, bl, 2;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], al, bh, %5, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bl, %5, 1;\n\t"
-      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], ah, bh, %5, 1;\n\t}" ::"r"(d_tmem),
-      "l"(a_hi), "l"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accumulate)
-      : "memory");
-}
 // Same K=32 block with A (hi and lo) in tensor memory ("ts" form): A_hi at
 // TMEM columns [a_hi, a_hi+32), A_lo at [a_lo, a_lo+32), lane = row; each
 // k-step of 8 tf32 advances A by 8 columns and B by 32 B (2 in 16-B units).
@@ -270,17 +170,6 @@ CBG_DEV void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
 }
-// 32 lanes x 32 bit, 32 consecutive columns per thread (this warp's lane quarter).
-CBG_DEV void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
-      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
-      "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]), "r"(r[9]),
-      "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15]), "r"(r[16]), "r"(r[17]), "r"(r[18]),
-      "r"(r[19]), "r"(r[20]), "r"(r[21]), "r"(r[22]), "r"(r[23]), "r"(r[24]), "r"(r[25]), "r"(r[26]), "r"(r[27]),
-      "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
-      : "memory");
-}
 // 32 lanes x 32 bit, 16 consecutive columns per thread.
 CBG_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
@@ -305,12 +194,6 @@ CBG_DEV void umma_commit_elect(uint64_t* bar) {
       "elect.sync _|e, 0xffffffff;\n\t"
       "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
       : "memory");
-}
-// Arrive on an mbarrier once all previously issued tcgen05 ops of this thread complete.
-CBG_DEV void umma_commit(uint64_t* bar) {
-  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                   smem_u32(bar))
-               : "memory");
 }
 // 32 lanes x 32 bit, 16 consecutive columns per thread.
 CBG_DEV void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {

@@ -629,7 +629,10 @@ void Net::build() {
   frame_ctr_.alloc(4);
   dc_ctr_.alloc(nodes_.size() * 2 * S_ * 2 * sizeof(int32_t));
   boot_req_.alloc(S_);
-  CK(cudaMemset(boot_req_.p, 1, S_));
+  // a network bootstraps on its first frame (network.cpp:318-321); a standalone
+  // layer does not: only force_full_update makes it a full update (layers.cpp:64-71)
+  if (n == 0 || nodes_[0].d.kind != kExternal) CK(cudaMemset(boot_req_.p, 1, S_));
+  CK(cudaStreamSynchronize(nullptr));
   s8_valid_.assign(S_, 0);
   s8_pending_.assign(S_, 1);
   boot_now_.alloc(S_);
@@ -656,6 +659,9 @@ int Net::amax_origin(int node) const {
 
 void Net::clear_maps() {
   for (NodeRT& r : nodes_) {
+    // an external node's map was uploaded for this call already (set_external
+    // tags it with the coming frame's epoch): clearing it would drop it
+    if (r.d.kind == kExternal) continue;
     if (r.inmap.bytes) CK(cudaMemsetAsync(r.inmap.p, 0, r.inmap.bytes, ctx_->stream));
     if (r.outmap_own.bytes) CK(cudaMemsetAsync(r.outmap_own.p, 0, r.outmap_own.bytes, ctx_->stream));
     if (r.wc_map.bytes) CK(cudaMemsetAsync(r.wc_map.p, 0, r.wc_map.bytes, ctx_->stream));
@@ -1126,19 +1132,21 @@ void Net::set_external(const float* x_chw, const uint8_t* map, const int32_t* ro
   std::vector<uint8_t> m(HW, full ? tag : 0);
   if (map && !full)
     for (size_t i = 0; i < HW; ++i) m[i] = map[i] ? tag : 0;
-  CK(cudaMemcpy(e.outmap, m.data(), HW, cudaMemcpyHostToDevice));
+  // ordered on the ctx stream after the previous frame's kernels, which may
+  // still read the map, list and count (pageable sources are staged at call time)
+  CK(cudaMemcpyAsync(e.outmap, m.data(), HW, cudaMemcpyHostToDevice, st));
   std::vector<int32_t> idx;
   if (full) {
     idx.resize(HW);
     for (size_t k = 0; k < HW; ++k) idx[k] = static_cast<int32_t>(k);
-    CK(cudaMemcpy(e.idx, idx.data(), HW * sizeof(int32_t), cudaMemcpyHostToDevice));
+    CK(cudaMemcpyAsync(e.idx, idx.data(), HW * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   } else if (rowcol) {
     idx.resize(static_cast<size_t>(n));
     for (int64_t k = 0; k < n; ++k) idx[k] = rowcol[2 * k] * d.W + rowcol[2 * k + 1];
-    if (n) CK(cudaMemcpy(e.idx, idx.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice));
+    if (n) CK(cudaMemcpyAsync(e.idx, idx.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   }
   const int32_t cnt = static_cast<int32_t>(full ? HW : rowcol ? n : 0);
-  CK(cudaMemcpy(counts_.as<int32_t>() + e.count_slot * S_, &cnt, sizeof(cnt), cudaMemcpyHostToDevice));
+  CK(cudaMemcpyAsync(counts_.as<int32_t>() + e.count_slot * S_, &cnt, sizeof(cnt), cudaMemcpyHostToDevice, st));
 }
 
 void Net::reset(int stream) {

@@ -248,3 +248,62 @@ def test_tensor_precisions_and_operand_scaling(gpu, monkeypatch, prec, scale):
         assert rel <= 5e-6, f"{prec} scale {scale}: relative error {rel}"
         x = x.copy()
         x[:, rng.integers(0, 40, 50), rng.integers(0, 36, 50)] *= -1.5
+
+
+def test_epoch_wrap_keeps_upstream_map(gpu):
+    """Maps are epoch-tagged and cleared once per 255 frames; the upstream map
+    a standalone layer receives on a wrap call must survive the clear. A
+    Propagate conv and a pool run 300 calls (past two wraps) against the
+    reference, each call changing a few upstream pixels."""
+    rng = np.random.default_rng(41)
+    s = rand_spec(rng, 3, kernels=(3,), stride=1, pad=1)
+    conv = cbi.CBConvLayer(s, 0.0, cbi.DetectionPolicy.Propagate, in_height=12, in_width=10)
+    rconv = oracle.RefConv(s, 0.0, cbi.DetectionPolicy.Propagate, in_h=12, in_w=10)
+    pool = cbi.CBPoolLayer(2, 2, 3, 12, 10, 6, 5)
+    rpool = oracle.RefPool(2, 2, 3, 12, 10, 6, 5)
+    x = rng.uniform(-1, 1, (3, 12, 10)).astype(np.float32)
+    conv.forward(x, force_full_update=True)
+    rconv.forward(x, None, None, force=True)
+    pool.forward(x, force_full_update=True)
+    rpool.forward(x, force=True)
+    for t in range(300):
+        m = np.zeros((12, 10), np.uint8)
+        m[rng.integers(0, 12, 3), rng.integers(0, 10, 3)] = 1
+        x = np.where(m[None], rng.uniform(-1, 1, x.shape), x).astype(np.float32)
+        idx = np.argwhere(m).astype(np.int32)
+        res = conv.forward(x, cbi.UpstreamChange(m, idx))
+        rconv.forward(x, m, idx)
+        pres = pool.forward(x, cbi.UpstreamChange(m, idx))
+        rpool.forward(x, m, idx)
+        if t % 25 == 0 or t in range(250, 260) or t in range(505, 515):
+            same_changes(res, rconv)
+            rm, ri = rpool.changes()
+            assert np.array_equal(pres.out_map, rm) and np.array_equal(pres.indexes, ri), t
+            assert np.array_equal(pool.prev_output, rpool.prev_output), t
+            assert oracle.max_rel_err(conv.prev_output, rconv.prev_output) <= TOL, t
+    assert np.array_equal(pool.prev_output, rpool.prev_output)
+
+
+@pytest.mark.parametrize("policy", [cbi.DetectionPolicy.Detect, cbi.DetectionPolicy.Propagate])
+def test_first_call_without_force_is_not_a_bootstrap(gpu, policy):
+    """A standalone layer has no bootstrap (layers.cpp:64-71 runs only under
+    force_full_update): the first unforced Detect call compares against the
+    zero state, a Propagate call updates only the upstream's dilated pixels."""
+    rng = np.random.default_rng(43)
+    s = rand_spec(rng, 2, kernels=(3,), stride=1, pad=1)
+    g, r = pair(s, 0.05, policy=policy, h=10, w=10)
+    x = rng.uniform(0, 1, (2, 10, 10)).astype(np.float32)
+    x[:, :5, :] = 0.0  # unchanged against the zero state
+    m = np.zeros((10, 10), np.uint8)
+    m[7, 3] = 1
+    idx = np.argwhere(m).astype(np.int32)
+    if policy == cbi.DetectionPolicy.Detect:
+        res = g.forward(x)
+        r.forward(x)
+    else:
+        res = g.forward(x, cbi.UpstreamChange(m, idx))
+        r.forward(x, m, idx)
+    same_changes(res, r)
+    assert len(res.indexes) < 100
+    assert oracle.max_rel_err(g.prev_output, r.prev_output) <= TOL
+    assert np.array_equal(g.prev_output == 0, r.prev_output == 0)
