@@ -455,9 +455,18 @@ def ref_seg_stats_csv(seed, height, width, taus, synth: "cbi.SyntheticConfig", w
     return subprocess.run(args, capture_output=True, text=True, check=True).stdout
 
 
+# observed max_rel_err per test (tests/conftest.py writes it to $CBG_PARITY_OUT:
+# the measured maxima behind every tolerance in the GPU tests)
+OBSERVED: dict = {}
+
+
 def max_rel_err(a, b) -> float:
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     if a.size == 0:
         return 0.0
-    return float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(b))))
+    e = float(np.max(np.abs(a - b) / np.maximum(1.0, np.abs(b))))
+    test = os.environ.get("PYTEST_CURRENT_TEST", "").split(" ")[0]
+    if test:
+        OBSERVED[test] = max(OBSERVED.get(test, 0.0), e)
+    return e

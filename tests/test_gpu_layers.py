@@ -3,9 +3,9 @@ reference build (oracle/_ref), on identical seeded inputs.
 
 Adapted from the reference's tests/test_layers.cpp and acceptance C1-C3.
 Bars: change maps, index lists, input states and pooled
-outputs are bit-exact; conv outputs (3xTF32 tensor-core GEMM, different sum
-order than the reference's sequential fp32 loop) within max_rel_err
-(tests/oracles.hpp:59-66) <= TOL.
+outputs are bit-exact; conv outputs (3xFP16 tcgen05 GEMM with a different sum
+order than the reference's sequential fp32 loop, or bit-exact on the CUDA-core
+path for Cout <= 16) within max_rel_err (tests/oracles.hpp:59-66) <= TOL.
 """
 import numpy as np
 import pytest
@@ -15,7 +15,7 @@ from tests import oracle
 
 pytestmark = pytest.mark.gpu
 
-TOL = 2e-5  # max_rel_err for conv outputs (fp32-accurate 3xTF32 GEMM)
+TOL = 4e-6  # max_rel_err for conv outputs: 2x the largest observed (1.97e-6; CBG_PARITY_OUT)
 
 
 def rand_spec(rng, cin, kernels=(1, 3, 5, 7), max_out=40, stride=None, pad=None):

@@ -13,7 +13,7 @@ from tests import oracle
 
 pytestmark = pytest.mark.gpu
 
-TOL_NET = 1e-4
+TOL_NET = 8e-5  # 2x the largest observed (4.0e-5, test_pnm8_state_shadow_mixed_ingest; CBG_PARITY_OUT)
 
 
 def seq(h, w, n=6, seed=7, objects=3, size=10, vel=3, noise=0.0, c=3):
