@@ -40,21 +40,36 @@ METRIC = "frames/s per B200 vs changed-pixel % (scene-labeling net); % HBM/TC ro
 REF_BENCH = os.path.join(ROOT, "oracle", "_ref", "ref_bench")
 
 
+# BASELINE.json configs this bench runs: configs[1] (the metric's workload, the
+# default; weak scaling, streams per GPU) and configs[4] (64 x 1080p streams
+# sharded over the ranks: strong scaling, the driver's SCALE run with --config cfg5)
+CONFIGS = {
+    "cfg2": dict(height=480, width=640, streams=64, groups=4, ring=16, objects=6, object_size=40, velocity=4,
+                 scaling="weak", sweep_steps=6),
+    "cfg5": dict(height=1080, width=1920, streams=64, groups=4, ring=4, objects=12, object_size=80, velocity=4,
+                 scaling="strong", sweep_steps=0),
+}
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--streams", type=int, default=64, help="camera streams per GPU")
-    ap.add_argument("--groups", type=int, default=4,
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS),
+                    help="cfg2: scene-labeling net 640x480, 64 streams per GPU (weak); cfg5: 64 x 1920x1080 "
+                         "streams in total, sharded over the GPUs (strong)")
+    ap.add_argument("--streams", type=int, default=None,
+                    help="camera streams per GPU (cfg2) / in total over all GPUs (cfg5)")
+    ap.add_argument("--groups", type=int, default=None,
                     help="stream groups per GPU, each its own stream set on its own CUDA stream (overlap)")
-    ap.add_argument("--ring", type=int, default=16, help="distinct frames per stream (ping-pong playback)")
-    ap.add_argument("--height", type=int, default=480)
-    ap.add_argument("--width", type=int, default=640)
-    ap.add_argument("--objects", type=int, default=6)
-    ap.add_argument("--object-size", type=int, default=40)
-    ap.add_argument("--velocity", type=int, default=4)
+    ap.add_argument("--ring", type=int, default=None, help="distinct frames per stream (ping-pong playback)")
+    ap.add_argument("--height", type=int, default=None)
+    ap.add_argument("--width", type=int, default=None)
+    ap.add_argument("--objects", type=int, default=None)
+    ap.add_argument("--object-size", type=int, default=None)
+    ap.add_argument("--velocity", type=int, default=None)
     ap.add_argument("--noise", type=float, default=0.0)
     ap.add_argument("--tau", type=float, default=0.05)
     ap.add_argument("--profile-steps", type=int, default=5, help="instrumented steps for the roofline")
@@ -65,9 +80,24 @@ def parse():
     ap.add_argument("--ingest", choices=["u8", "f32"], default="u8",
                     help="device-resident frame format of the value / roofline / dense / sweep passes: the 8-bit "
                          "PNM payload (cbg_net_forward_u8) or its fp32 conversion (cbg_net_forward)")
-    ap.add_argument("--sweep-steps", type=int, default=6,
+    ap.add_argument("--sweep-steps", type=int, default=None,
                     help="timed steps per point of the change-rate sweep (0 disables the sweep)")
-    return ap.parse_args()
+    ap.add_argument("--cpu-one-core-budget", type=float, default=8.0,
+                    help="seconds of the 1-thread, 1-stream CPU reference sample (0 disables)")
+    a = ap.parse_args()
+    for k, v in CONFIGS[a.config].items():
+        if getattr(a, k, None) is None:
+            setattr(a, k, v)
+    return a
+
+
+def local_streams(a, rank, world):
+    """(shard, stream count on this rank, stream groups) of the configured workload"""
+    from paper_1808_05488_b200.sharding import shard_streams, weak_shard
+    shard = weak_shard(a.streams, rank, world) if a.scaling == "weak" else shard_streams(a.streams, rank, world)
+    S = shard.count
+    G = max(g for g in range(1, a.groups + 1) if S % g == 0)
+    return shard, S, G
 
 
 def dist_env():
@@ -76,11 +106,14 @@ def dist_env():
 
 
 def config_dict(a, world):
-    return {"workload": f"scene-labeling net (seg7 layers, derived dims) {a.width}x{a.height}, "
-                        f"{a.streams} streams/GPU, gen_synthetic {a.objects}x{a.object_size}px objects "
+    total = a.streams * world if a.scaling == "weak" else a.streams
+    per = f"{a.streams} streams/GPU" if a.scaling == "weak" else f"{a.streams} streams sharded over {world} GPU(s)"
+    return {"workload": f"{a.config}: scene-labeling net (seg7 layers, derived dims) {a.width}x{a.height}, "
+                        f"{per}, gen_synthetic {a.objects}x{a.object_size}px objects "
                         f"v={a.velocity} noise={a.noise}, tau={a.tau}",
-            "height": a.height, "width": a.width, "streams_per_gpu": a.streams,
-            "total_streams": a.streams * world, "stream_groups": a.groups, "frame_ring": a.ring,
+            "baseline_config": a.config, "height": a.height, "width": a.width,
+            "streams_per_gpu": a.streams if a.scaling == "weak" else -(-a.streams // world),
+            "total_streams": total, "stream_groups": a.groups, "frame_ring": a.ring,
             "objects": a.objects, "object_size": a.object_size,
             "velocity": a.velocity, "noise_std": a.noise, "tau": a.tau,
             "frames": "gen_synthetic quantized to 8-bit PNM payloads; fp32 arms see load_pnm's byte/255.0f",
@@ -111,7 +144,7 @@ def reference_arm(a, rank, world):
         return
     threads = os.cpu_count() or 1
     base = {"metric": METRIC, "unit": "frames/s", "impl": "reference", "n_gpus": a.gpus, "steps": a.steps,
-            "warmup": a.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "warmup": a.warmup, "higher_is_better": True, "scaling": a.scaling, "vs_baseline": None, "dtype": "f32",
             "data": "synthetic (gen_synthetic, seeded)", "config": config_dict(a, world)}
     if not os.path.exists(REF_BENCH):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/ref_bench not built"}))
@@ -200,30 +233,65 @@ SWEEP = [(1, 8), (2, 16), (3, 32), (6, 40), (10, 48), (24, 64), (60, 96), "rando
 
 
 # ---------------------------------------------------------------------------
-# algorithmic work per kernel
+# algorithmic work per kernel launch
 # ---------------------------------------------------------------------------
-def kernel_work(node, kernel, n_out, n_up, S_counts):
-    """Algorithmic (bytes, flops) of one launch, summed over the streams.
-    n_out/n_up: per-stream lists of this node's / its producer's changed pixels."""
-    kind, name, cin, hin, win, cout, hout, wout, k, ops_pp = node
+def receptive_union(out_mask, hin, win, kh, kw, st, pad):
+    """U: input pixels inside the receptive field of any marked output pixel
+    (the distinct pixels a gather has to read once)."""
+    import numpy as np
+    ho, wo = out_mask.shape
+    m = np.zeros((hin, win), bool)
+
+    def rng(k, n_out, n_in):  # output range whose tap k lands inside the input
+        o0 = max(0, -(-(pad - k) // st))
+        o1 = min(n_out, (n_in - 1 + pad - k) // st + 1)
+        return o0, o1
+    for kj in range(kh):
+        j0, j1 = rng(kj, ho, hin)
+        if j0 >= j1:
+            continue
+        for ki in range(kw):
+            i0, i1 = rng(ki, wo, win)
+            if i0 >= i1:
+                continue
+            m[j0 * st - pad + kj:(j1 - 1) * st - pad + kj + 1:st,
+              i0 * st - pad + ki:(i1 - 1) * st - pad + ki + 1:st] |= out_mask[j0:j1, i0:i1]
+    return int(m.sum())
+
+
+def kernel_work(kn, nd, n_out, n_det, n_up, u_ratio, ingest, pool_of=None, n_pool=None):
+    """Algorithmic (bytes, flops) of one launch of kernel kn of node nd, summed
+    over the streams. n_out / n_det / n_up: per-stream changed output pixels,
+    detected input pixels (before dilation) and the producer's changed pixels;
+    u_ratio: U / n_out of the node's gather (receptive_union, sampled)."""
+    cin, hin, win = nd["in"]
+    cout, hout, wout = nd["out"]
+    k2 = nd["k"] ** 2
     b = f = 0.0
-    for s in range(S_counts):
-        no = int(n_out[s])
-        nu = int(n_up[s]) if n_up is not None else None
-        if kernel == "detect":
-            if nu is None:  # dense scan of the network input: read x and state
-                b += 8.0 * cin * hin * win
-            else:           # sparse: x and state at the producer's update set
-                b += 8.0 * cin * nu
-        elif kernel == "dilcomp":
-            b += hin * win / 8.0 + hout * wout / 8.0 + 4.0 * no + 4
-        elif kernel == "gemm":
-            f += ops_pp * no
-            # gather lower bound (each changed pixel's own receptive-field centre),
-            # weights once, scatter of the Cout vector
-            b += 4.0 * cin * no + 4.0 * cout * no + (4.0 * cout * cin * k * k if s == 0 else 0.0)
-        elif kernel == "pool":
+    for s in range(len(n_out)):
+        no, nd_ = float(n_out[s]), float(n_det[s]) if n_det is not None else 0.0
+        if kn == "detect":
+            if n_up is None:  # first layer, dense over the frame
+                if ingest == "u8":  # 8-bit frame + 8-bit state shadow read; fp32 state + shadow written
+                    b += 2.0 * cin * hin * win + 5.0 * cin * nd_
+                else:               # fp32 frame + fp32 state read, state written
+                    b += 8.0 * cin * hin * win + 4.0 * cin * nd_
+            else:             # x and state at the producer's update set, state (+ pre-split copy) written
+                b += 8.0 * cin * float(n_up[s]) + 4.0 * cin * nd_ * (2 if nd["presplit"] else 1)
+            b += hin * win / 8.0  # bitmap
+        elif kn == "dilcomp":
+            b += hin * win / 8.0 + hout * wout / 8.0 + 4.0 * no
+            if pool_of is not None:
+                b += pool_of["out"][1] * pool_of["out"][2] / 8.0 + 4.0 * float(n_pool[s])
+        elif kn == "gemm":
+            f += nd["ops_pp"] * no
+            b += 4.0 * cin * u_ratio * no + 4.0 * cout * no
+        elif kn == "pool":
             b += 4.0 * cin * 4 * no + 4.0 * cin * no
+        elif kn == "join":
+            b += 4.0 * cout * (nd["n_in"] + 1) * no
+    if kn == "gemm":
+        b += 4.0 * cout * cin * k2  # weights (fp16 hi + lo images, or fp32) once per launch
     return b, f
 
 
@@ -251,42 +319,44 @@ def main():
             dist.init_process_group(backend)
     from paper_1808_05488_b200 import cbi
     from paper_1808_05488_b200.sharding import max_over_ranks as _max_over_ranks
-    from paper_1808_05488_b200.sharding import weak_shard
 
-    peaks = {"hbm_gbs": 6538.6, "bf16_tflops": 1661.9, "bf16_tflops_sustained": 1399.9, "source": "fallback"}
+    peaks = {"hbm_gbs": 6538.6, "bf16_tflops": 1661.9, "bf16_tflops_sustained": 1399.9, "sm_max_mhz": 1965.0,
+             "source": "fallback (B200_PROFILING.md)"}
     pk_path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(pk_path):
         with open(pk_path) as fh:
             peaks.update(json.load(fh))
         peaks["source"] = "measured (MEASURED_PEAKS.json)"
+    n_sm = torch.cuda.get_device_properties(local).multi_processor_count
 
-    S, H, W, G = a.streams, a.height, a.width, a.groups
-    if S % G:
-        raise SystemExit("--streams must be a multiple of --groups")
+    shard, S, G = local_streams(a, rank, world)
+    H, W = a.height, a.width
     Sg = S // G
     ctxs = [cbi.Context(local) for _ in range(G)]
     ctx = ctxs[0]
     spec = cbi.make_seg_spec(1, H, W)
     taus = [a.tau] * 5
     L = max(3, a.ring)
-    # frame ring [L][S][C][H][W], pinned on the host and resident in HBM; played
-    # ping-pong (1..L-1, L-2..2, ...) so motion stays continuous for any step count
-    # The frames are what a PNM sequence delivers (cbi run -> load_pnm): 8-bit
-    # payloads ([H][W][C] bytes) of gen_synthetic frames; the fp32 arm sees
-    # load_pnm's byte / 255.0f of the same bytes, so every arm runs one workload.
-    host = torch.empty((L, S, 3, H, W), dtype=torch.float32, pin_memory=True)
+    # frame ring [L][S][H][W][C], 8-bit PNM payloads (what a camera or `cbi run`'s
+    # PNM sequence delivers: load_pnm, io.cpp:349-399), pinned on the host and
+    # resident in HBM; played ping-pong (1..L-1, L-2..2, ...) so motion stays
+    # continuous for any step count. The fp32 arms see load_pnm's byte / 255.0f
+    # of the same bytes (IEEE division), so every arm runs one workload.
     host8 = torch.empty((L, S, H, W, 3), dtype=torch.uint8, pin_memory=True)
-    hnp, h8np = host.numpy(), host8.numpy()
-    shard = weak_shard(S, rank, world)  # streams rank*S .. rank*S+S-1, seed 1000 + global id
-    for s in range(S):
-        raw = cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, L, a.objects, a.object_size, a.velocity,
-                                                    a.velocity, a.noise, shard.seed(s)))
-        h8np[:, s] = cbi.to_pnm8(raw)
-        hnp[:, s] = cbi.from_pnm8(h8np[:, s])
-    dev = host.to(f"cuda:{local}")
+    h8np = host8.numpy()
+    from concurrent.futures import ThreadPoolExecutor
+
+    def _gen(s_):
+        h8np[:, s_] = cbi.to_pnm8(cbi.gen_synthetic(cbi.SyntheticConfig(
+            H, W, 3, L, a.objects, a.object_size, a.velocity, a.velocity, a.noise, shard.seed(s_))))
+    with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as pool:
+        list(pool.map(_gen, range(S)))
     dev8 = host8.to(f"cuda:{local}")
-    torch.cuda.synchronize()
     u8_in = a.ingest == "u8"
+    dev = None
+    if not u8_in:  # [L][S][C][H][W] fp32 = byte / 255.0f
+        dev = (dev8.permute(0, 1, 4, 2, 3).float() / 255.0).contiguous()
+    torch.cuda.synchronize()
 
     def feed(net_, t, g=None):
         """one frame of the device-resident workload (all streams of group g, or of the whole set)"""
@@ -316,11 +386,9 @@ def main():
     nets = [cbi.convert_to_cb(spec, taus, n_streams=Sg, ctx=ctxs[g]) for g in range(G)]
     net = nets[0]
     n_slots, node_slot = net.count_layout()
+    det_slot = net.detect_slots()
     nodes = net.nodes()
-    counts_pinned = torch.empty((G, a.steps + 1, n_slots, Sg), dtype=torch.int32, pin_memory=True)
-
-    def dptr(t, g):
-        return dev[t, g * Sg].data_ptr()
+    counts_pinned = torch.empty((G, a.steps + 1, Sg, n_slots), dtype=torch.int32, pin_memory=True)
 
     def timed_region(step_fn, steps):
         """device time of `steps` calls of step_fn(k) across all groups (CUDA events)"""
@@ -342,6 +410,14 @@ def main():
         torch.cuda.synchronize()
         return t0.elapsed_time(t1)
 
+    def change_of(cnt):
+        """cnt [..., S, slot] -> (L1-output fraction, L1 detected-input fraction, per-layer fractions)"""
+        l1_px = nodes[0].out_shape[1] * nodes[0].out_shape[2]
+        in_px = nodes[0].in_shape[1] * nodes[0].in_shape[2]
+        per = {n.name: float(cnt[..., node_slot[i]].mean()) / (n.out_shape[1] * n.out_shape[2])
+               for i, n in enumerate(nodes)}
+        return (float(cnt[..., node_slot[0]].mean()) / l1_px, float(cnt[..., det_slot[0]].mean()) / in_px, per)
+
     # ---- value: frames resident in HBM ---------------------------------------
     for g in range(G):
         feed(nets[g], 0, g)  # bootstrap (untimed)
@@ -362,13 +438,12 @@ def main():
         ms = max_over_ranks(timed_region(value_step, a.steps))
     barrier()
     launches = net.last_launches() * G
-    cnt = np.concatenate([counts_pinned[g, :a.steps].numpy() for g in range(G)], axis=2)
-    l1_px = nodes[0].out_shape[1] * nodes[0].out_shape[2]
-    l1_frac = float(cnt[:, node_slot[0], :].mean()) / l1_px
-    per_layer = {n.name: float(cnt[:, node_slot[i], :].mean()) / (n.out_shape[1] * n.out_shape[2])
-                 for i, n in enumerate(nodes)}
-    value = S * world * a.steps / (ms / 1000.0)
+    cnt = np.concatenate([counts_pinned[g, :a.steps].numpy() for g in range(G)], axis=1)  # [step][S][slot]
+    l1_frac, l1_det_frac, per_layer = change_of(cnt)
+    total_streams = S * world if a.scaling == "weak" else a.streams
+    value = total_streams * a.steps / (ms / 1000.0)
     next_k = base_k + a.steps
+    labels = net.kernel_labels()
 
     # ---- roofline: instrumented pass (per-kernel CUDA events) -----------------
     # one stream set holding all S streams (the launch shape of the ncu capture
@@ -379,67 +454,107 @@ def main():
         feed(pnet, frame_at(next_k + k))
     ctx.synchronize()
     pnet.set_kernel_timing(True)
+    layer = {ld.name: ld for ld in spec.layers}
+    desc = []
+    for i, n in enumerate(nodes):
+        ld = layer.get(n.name)
+        k = ld.conv.kernel_h if (ld is not None and n.kind == cbi.LayerKind.Conv) else 1
+        desc.append({"in": tuple(n.in_shape), "out": tuple(n.out_shape), "k": k, "ops_pp": int(n.ops_per_pixel),
+                     "presplit": n.kind == cbi.LayerKind.Conv and k > 1 and n.out_shape[0] > 16
+                     and bool(n.inputs) and n.inputs[0] >= 0,
+                     "n_in": len(n.inputs), "conv": ld.conv if n.kind == cbi.LayerKind.Conv else None})
+    # pools whose map and list come from their producer's compaction (no own dilcomp launch)
+    fused_pool = {n.inputs[0]: i for i, n in enumerate(nodes)
+                  if n.kind == cbi.LayerKind.Pool and f"{n.name}.dilcomp" not in labels}
     work = {}
-    prof_counts = torch.empty((n_slots, S), dtype=torch.int32, pin_memory=True)
+    prof_counts = torch.empty((S, n_slots), dtype=torch.int32, pin_memory=True)
+    u_ratio = {}
     for k in range(a.profile_steps):
         feed(pnet, frame_at(next_k + 2 + k))
         pnet.copy_counts_async(prof_counts.data_ptr())
         ctx.synchronize()
-        c = prof_counts.numpy()
+        c = prof_counts.numpy().T  # [slot][S]
+        if k == a.profile_steps - 1 or not u_ratio:
+            # U / n_out of each conv's gather on a sample of streams of this frame
+            for i, n in enumerate(nodes):
+                cv = desc[i]["conv"]
+                if cv is None:
+                    continue
+                num = den = 0
+                for sidx in range(min(S, 8)):
+                    m, _ = pnet.node_changes(i, sidx)
+                    num += receptive_union(m.astype(bool), n.in_shape[1], n.in_shape[2], cv.kernel_h, cv.kernel_w,
+                                           cv.stride, cv.padding)
+                    den += int(m.sum())
+                u_ratio[i] = num / den if den else 1.0
         for i, n in enumerate(nodes):
             src = n.inputs[0] if n.inputs else -1
-            cin, hin, win = n.in_shape
-            cout, hout, wout = n.out_shape
-            kk = 0
-            if n.kind == cbi.LayerKind.Conv:
-                kk = int(round((n.ops_per_pixel / (2 * cout * max(1, cin))) ** 0.5))
-            desc = (n.kind, n.name, cin, hin, win, cout, hout, wout, kk, int(n.ops_per_pixel))
             n_out = c[node_slot[i]]
+            n_det = c[det_slot[i]] if det_slot[i] >= 0 else None
             n_up = c[node_slot[src]] if src >= 0 else None
-            for kern in ("detect", "dilcomp", "gemm", "pool"):
-                bb, ff = kernel_work(desc, kern, n_out, n_up, S)
-                wsum = work.setdefault(f"{n.name}.{kern}", [0.0, 0.0])
+            kinds = {cbi.LayerKind.Conv: ("detect", "dilcomp", "gemm"), cbi.LayerKind.Pool: ("dilcomp", "pool")}
+            for kern in kinds.get(n.kind, ("dilcomp", "join")):
+                pc = fused_pool.get(i)
+                bb, ff = kernel_work(kern, desc[i], n_out, n_det, n_up, u_ratio.get(i, 1.0), a.ingest,
+                                     desc[pc] if (kern == "dilcomp" and pc is not None) else None,
+                                     c[node_slot[pc]] if pc is not None else None)
+                wsum = work.setdefault(f"{n.name}.{kern}", [0.0, 0.0, 0])
                 wsum[0] += bb
                 wsum[1] += ff
+                wsum[2] += 1
     rep = pnet.timing_report()
     pnet.set_kernel_timing(False)
     del pnet
-    traffic = {}
+    traffic, ncu_us = {}, {}
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         with open(tpath) as fh:
             tj = json.load(fh)
         if tj.get("streams") == S and tj.get("height") == H and tj.get("width") == W:
             traffic = tj.get("dram_bytes_per_launch", {})
+            ncu_us = tj.get("duration_us", {})
     hbm = peaks["hbm_gbs"] * 1e9
     # the tcgen05 GEMMs run kind::f16 (3xFP16 split, default) or kind::tf32
     # (CBG_GEMM_PREC=tf32); the tensor peak is that kind's dense rate: the
     # measured bf16 (= fp16) rate, or half of it for tf32
     f16_gemm = os.environ.get("CBG_GEMM_PREC", "f16") != "tf32"
-    tf32 = peaks["bf16_tflops"] * 1e12 / (1 if f16_gemm else 2)
+    tc = peaks["bf16_tflops"] * 1e12 / (1 if f16_gemm else 2)
+    # the bit-exact CUDA-core convs (Cout <= 16) issue one non-fused fp32 mul
+    # and one add per MAC: 1 flop per lane per clock on 128 lanes per SM
+    fp32 = n_sm * 128 * peaks["sm_max_mhz"] * 1e6
+    exact = {n.name for n in nodes if n.kind == cbi.LayerKind.Conv and n.out_shape[0] <= 16}
     kernels = []
     for label, (tot_ms, nl) in rep["kernels"].items():
-        bb, ff = work.get(label, [0.0, 0.0])
-        t = tot_ms / 1000.0
-        t_roof = max(bb / hbm, ff / tf32)
-        kernels.append({"kernel": label, "ms_per_launch": tot_ms / max(1, nl), "share": 0.0,
-                        "bytes_per_launch": bb / max(1, nl), "flops_per_launch": ff / max(1, nl),
-                        "roofline_frac": (t_roof / t) if t > 0 else None,
-                        "bound": "tensor" if ff / tf32 > bb / hbm else "hbm"})
+        bb, ff, nw = work.get(label, [0.0, 0.0, 1])
+        bb, ff = bb / max(1, nw), ff / max(1, nw)  # per launch
+        t = tot_ms / 1000.0 / max(1, nl)
+        fpk = fp32 if label.split(".")[0] in exact else tc
+        t_roof = max(bb / hbm, ff / fpk)
+        bound = ("fp32" if fpk == fp32 else "tensor") if ff / fpk > bb / hbm else "hbm"
+        kk = {"kernel": label, "ms_per_launch": 1000.0 * t, "share": 0.0, "bytes_per_launch": bb,
+              "flops_per_launch": ff, "roofline_frac": (t_roof / t) if t > 0 else None, "bound": bound}
+        if label in traffic and ncu_us.get(label):
+            kk["ncu_dram_bytes"] = traffic[label]
+            kk["ncu_us"] = ncu_us[label]
+            kk["ncu_dram_frac"] = traffic[label] / (ncu_us[label] * 1e-6) / hbm
+        kernels.append(kk)
     tot = sum(k["ms_per_launch"] for k in kernels) or 1.0
     for k in kernels:
         k["share"] = k["ms_per_launch"] / tot
     kernels.sort(key=lambda k: -k["ms_per_launch"])
     dom = kernels[0]
-    if dom["bound"] == "tensor":
+    if dom["bound"] in ("tensor", "fp32"):
+        pk = tc if dom["bound"] == "tensor" else fp32
         achieved = dom["flops_per_launch"] / (dom["ms_per_launch"] / 1000.0) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": tf32 / 1e12, "unit": "TFLOP/s",
-                "frac": achieved / (tf32 / 1e12),
-                # the split-fp32 product issues 3 MMAs per useful MAC: the tensor
-                # pipe's share is 3x the useful fraction (attainable useful frac <= 1/3)
-                "tensor_issue_frac": 3 * achieved / (tf32 / 1e12),
-                "peak_note": ("fp16 dense = measured bf16 rate" if f16_gemm else "tf32 dense = measured bf16 / 2")
-                + "; useful fp32-accurate flops (2*Cout*Cin*k^2 per changed px), 3 MMAs per useful MAC"}
+        roof = {"bound": "tensor", "achieved": achieved, "peak": pk / 1e12, "unit": "TFLOP/s",
+                "frac": achieved / (pk / 1e12)}
+        if dom["bound"] == "tensor":
+            # the split-fp32 product issues 3 MMAs per useful MAC: the tensor
+            # pipe's share is 3x the useful fraction (attainable useful frac <= 1/3)
+            roof["tensor_issue_frac"] = 3 * achieved / (pk / 1e12)
+            roof["peak_note"] = (("fp16 dense = measured bf16 rate (burst)" if f16_gemm else "tf32 dense = measured "
+                                  "bf16 / 2") + "; useful fp32-accurate flops (2*Cout*Cin*k^2 per changed px), "
+                                 "3 MMAs per useful MAC")
     else:
         achieved = dom["bytes_per_launch"] / (dom["ms_per_launch"] / 1000.0) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
@@ -447,10 +562,23 @@ def main():
     roof.update({"kernel": dom["kernel"], "traffic": traffic.get(dom["kernel"]),
                  "traffic_note": "dram__bytes_read.sum + dram__bytes_write.sum per launch, profiles/ncu_traffic.json",
                  "launch_streams": S, "peak_source": peaks["source"],
-                 "step_roofline_frac": (sum(max(k["bytes_per_launch"] / hbm, k["flops_per_launch"] / tf32)
+                 "work_model": ("algorithmic bytes/flops per launch from the device counts (DESIGN.md §3): detect "
+                                "2*Cin B/px of 8-bit frame+shadow (u8) or 8*Cin (f32) + state writes at detected px; "
+                                "detect_list 8*Cin per producer-changed px + 4*Cin per detected px (x2 with the "
+                                "pre-split copy); dilcomp bitmaps in+out + 4 B per listed px (+ a fused pool's); "
+                                "gemm 4*Cin*U + 4*Cout*n_out + weights (U = receptive-field union, sampled on "
+                                "8 streams); pool 4*C*(4+1) per px"),
+                 "peaks": {"hbm_gbs": peaks["hbm_gbs"], "tensor_tflops": tc / 1e12, "fp32_tflops": fp32 / 1e12},
+                 "step_roofline_frac": (sum(max(k["bytes_per_launch"] / hbm, k["flops_per_launch"] /
+                                                (fp32 if k["kernel"].split(".")[0] in exact else tc))
                                             for k in kernels) / (tot / 1000.0)),
-                 "top_kernels": kernels[:6],
-                 "all_kernels_us": {k["kernel"]: round(1000 * k["ms_per_launch"], 1) for k in kernels}})
+                 "top_kernels": kernels[:8],
+                 "all_kernels": {k["kernel"]: {"us": round(1000 * k["ms_per_launch"], 1),
+                                               "frac": round(k["roofline_frac"] or 0.0, 3), "bound": k["bound"],
+                                               **({"ncu_us": k["ncu_us"], "ncu_dram_frac": round(k["ncu_dram_frac"], 3)}
+                                                  if "ncu_us" in k else {})}
+                                 for k in kernels},
+                 "u_ratio": {nodes[i].name: round(v, 3) for i, v in u_ratio.items()}})
 
     # ---- dense path (same kernels, every frame a full update) -------------------
     dense_fps = None
@@ -468,80 +596,74 @@ def main():
                 feed(dnets[g], frame_at(k), g)
 
         dms = max_over_ranks(timed_region(dense_step, a.dense_steps))
-        dense_fps = S * world * a.dense_steps / (dms / 1000.0)
+        dense_fps = total_streams * a.dense_steps / (dms / 1000.0)
         del dnets
 
     # ---- change-rate sweep: frames/s vs changed-pixel % (the metric's x-axis) ---
     sweep = []
     if a.sweep_steps > 0:
-        from concurrent.futures import ThreadPoolExecutor
         R = 6
         sorder = list(range(1, R)) + list(range(R - 2, 1, -1))
-        sw_counts = torch.empty((G, n_slots, Sg), dtype=torch.int32, pin_memory=True)
+        sw_counts = torch.empty((G, Sg, n_slots), dtype=torch.int32, pin_memory=True)
         for pt in SWEEP:
             if pt == "random":
                 gen = torch.Generator(device=f"cuda:{local}").manual_seed(4242 + rank)
-                if u8_in:
-                    sdev = torch.randint(0, 256, (R, S, H, W, 3), generator=gen, device=f"cuda:{local}",
-                                         dtype=torch.uint8)
-                else:
-                    sdev = torch.rand((R, S, 3, H, W), generator=gen, device=f"cuda:{local}")
+                sdev8 = torch.randint(0, 256, (R, S, H, W, 3), generator=gen, device=f"cuda:{local}",
+                                      dtype=torch.uint8)
             else:
                 ob, sz = pt
-                sh = torch.empty((R, S, H, W, 3) if u8_in else (R, S, 3, H, W),
-                                 dtype=torch.uint8 if u8_in else torch.float32, pin_memory=True)
+                sh = torch.empty((R, S, H, W, 3), dtype=torch.uint8, pin_memory=True)
                 shn = sh.numpy()
 
-                def _gen(s_, ob=ob, sz=sz, shn=shn):
-                    p8 = cbi.to_pnm8(cbi.gen_synthetic(cbi.SyntheticConfig(
+                def _gen_s(s_, ob=ob, sz=sz, shn=shn):
+                    shn[:, s_] = cbi.to_pnm8(cbi.gen_synthetic(cbi.SyntheticConfig(
                         H, W, 3, R, ob, sz, a.velocity, a.velocity, a.noise, shard.seed(s_))))
-                    shn[:, s_] = p8 if u8_in else cbi.from_pnm8(p8)
                 with ThreadPoolExecutor(max_workers=min(16, os.cpu_count() or 1)) as pool:
-                    list(pool.map(_gen, range(S)))
-                sdev = sh.to(f"cuda:{local}")
+                    list(pool.map(_gen_s, range(S)))
+                sdev8 = sh.to(f"cuda:{local}")
+            sdev = sdev8 if u8_in else (sdev8.permute(0, 1, 4, 2, 3).float() / 255.0).contiguous()
 
-            def sfeed(net_, t, g, sdev=None):
+            def sfeed(net_, t, g, sdev=sdev):
                 if u8_in:
                     net_.enqueue_device_u8(sdev[t, g * Sg].data_ptr())
                 else:
                     net_.enqueue_device(sdev[t, g * Sg].data_ptr())
             snets = [cbi.convert_to_cb(spec, taus, n_streams=Sg, ctx=ctxs[g]) for g in range(G)]
             for g in range(G):
-                sfeed(snets[g], 0, g, sdev)
+                sfeed(snets[g], 0, g)
             for k in range(3):
                 for g in range(G):
-                    sfeed(snets[g], sorder[k % len(sorder)], g, sdev)
+                    sfeed(snets[g], sorder[k % len(sorder)], g)
             for c in ctxs:
                 c.synchronize()
             barrier()
 
-            def sweep_step(k, snets=snets, sdev=sdev):
+            def sweep_step(k, snets=snets, sfeed=sfeed):
                 for g in range(G):
-                    sfeed(snets[g], sorder[(3 + k) % len(sorder)], g, sdev)
+                    sfeed(snets[g], sorder[(3 + k) % len(sorder)], g)
 
             sms = max_over_ranks(timed_region(sweep_step, a.sweep_steps))
             for g in range(G):
                 snets[g].copy_counts_async(sw_counts[g].data_ptr())
             for c in ctxs:
                 c.synchronize()
-            sc = np.concatenate([sw_counts[g].numpy() for g in range(G)], axis=1)
-            fps = S * world * a.sweep_steps / (sms / 1000.0)
+            sc = np.concatenate([sw_counts[g].numpy() for g in range(G)], axis=0)  # [S][slot]
+            fr, dfr, per = change_of(sc)
+            fps = total_streams * a.sweep_steps / (sms / 1000.0)
             sweep.append({"synthetic": ("uniform noise every frame" if pt == "random"
                                         else f"{pt[0]} objects x {pt[1]} px"),
-                          "l1_changed_pct": 100.0 * float(sc[node_slot[0]].mean()) / l1_px,
-                          "per_layer_changed_pct": {n.name: round(100.0 * float(sc[node_slot[i]].mean())
-                                                                  / (n.out_shape[1] * n.out_shape[2]), 3)
-                                                    for i, n in enumerate(nodes)},
+                          "l1_changed_pct": 100.0 * fr, "input_detected_pct": 100.0 * dfr,
+                          "per_layer_changed_pct": {k_: round(100.0 * v_, 3) for k_, v_ in per.items()},
                           "frames_per_s": fps,
                           "speedup_vs_dense": (fps / dense_fps) if dense_fps else None})
-            del snets, sdev
+            del snets, sdev, sdev8
         torch.cuda.empty_cache()
     crossover = None
     if dense_fps and sweep:
+        import math
         pts = sorted((p["l1_changed_pct"], p["frames_per_s"] / dense_fps) for p in sweep)
         for (x0, r0), (x1, r1) in zip(pts, pts[1:]):
             if r0 >= 1.0 > r1:  # linear in log(change) between the bracketing points
-                import math
                 f = (r0 - 1.0) / (r0 - r1)
                 crossover = math.exp(math.log(max(x0, 1e-6)) + f * (math.log(x1) - math.log(max(x0, 1e-6))))
                 break
@@ -551,6 +673,12 @@ def main():
     # the device); also the fp32 Tensor3 API (cbg_net_forward) with host frames
     e2e = e2e_f32 = None
     if not a.no_e2e:
+        hnp = None
+        if a.config == "cfg2":  # host fp32 frames (4x the bytes) for the Tensor3 arm
+            hnp = torch.empty((L, S, 3, H, W), dtype=torch.float32, pin_memory=True).numpy()
+            for t in range(L):
+                hnp[t] = cbi.from_pnm8(h8np[t])
+
         def run_e2e(u8):
             enets = [cbi.convert_to_cb(spec, taus, n_streams=Sg, ctx=ctxs[g]) for g in range(G)]
             out_bytes = enets[0].output_bytes(-1)
@@ -578,16 +706,18 @@ def main():
 
             ems = max_over_ranks(timed_region(e2e_step, a.steps))
             del enets
-            return {"value": S * world * a.steps / (ems / 1000.0), "unit": "frames/s",
+            return {"value": total_streams * a.steps / (ems / 1000.0), "unit": "frames/s",
                     "h2d_bytes_per_step": frame8_bytes if u8 else frame_bytes, "d2h_bytes_per_step": out_bytes * G,
                     "ms_per_step": ems / a.steps}
         e2e = run_e2e(True)
         e2e["api"] = ("cbg_net_forward_u8: pinned host 8-bit PNM payloads [S][H][W][3], load_pnm conversion "
-                      "(byte/255.0f) fused into the first layer's detect; D2H of the last node's output (cbg_net_copy_output_detached: "
-                      "staged on the device, copied out on the context's copy-out stream)")
-        e2e_f32 = run_e2e(False)
-        e2e_f32["api"] = ("cbg_net_forward: pinned host fp32 CHW frames (Tensor3); D2H of the last node's output "
-                          "(cbg_net_copy_output_detached)")
+                      "(byte/255.0f) fused into the first layer's detect; D2H of the last node's output "
+                      "(cbg_net_copy_output_detached: staged on the device, copied out on the context's "
+                      "copy-out stream)")
+        if hnp is not None:
+            e2e_f32 = run_e2e(False)
+            e2e_f32["api"] = ("cbg_net_forward: pinned host fp32 CHW frames (Tensor3); D2H of the last node's "
+                              "output (cbg_net_copy_output_detached)")
 
     # ---- CPU baseline (rank 0, N=1) ---------------------------------------------
     cpu = None
@@ -599,10 +729,30 @@ def main():
                    "sample": f"oracle/_ref/ref_bench: {r['frames']} post-bootstrap frames of {r['streams']} "
                              f"streams, one cbi::CBNetwork per thread, L1 change "
                              f"{100 * r['l1_change_frac']:.2f}%"}
+            if a.cpu_one_core_budget > 0:
+                r1 = run_ref_bench(a, 1, frames=3, budget=a.cpu_one_core_budget, streams=1)
+                cpu["one_core"] = {"value": r1["fps"], "unit": "frames/s", "cores": 1,
+                                   "sample": f"{r1['frames']} post-bootstrap frames of 1 stream, 1 thread"}
+            dpath = os.path.join(ROOT, "profiles", f"r02_cpu_dense_{a.config}.json")
+            if os.path.exists(dpath):
+                with open(dpath) as fh:
+                    cpu["dense_oracle"] = json.load(fh)
+
+    parity = None
+    ppath = os.path.join(ROOT, "profiles", "r02_parity.json")
+    if os.path.exists(ppath):
+        with open(ppath) as fh:
+            pj = json.load(fh).get(a.config)
+        if pj:
+            sm = pj["summary"]
+            parity = {"source": "profiles/r02_parity.json (tests/test_gpu_fullsize.py vs oracle/_ref, "
+                                "tools/parity_report.py)", "workload": pj.get("workload"),
+                      "l1_bit_exact": sm.get("l1_bit_exact"), "min_mask_agreement": sm.get("min_agree"),
+                      "max_rel_err": sm.get("max_rel_err"), "final_max_rel_err": sm.get("final_max_rel_err")}
 
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": "frames/s", "n_gpus": world, "steps": a.steps,
-               "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": "weak",
+               "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True, "scaling": a.scaling,
                "vs_baseline": None, "dtype": "f32",
                "gemm_precision": ("3xFP16 tcgen05 kind::f16, fp32 operands split hi+lo with power-of-two scaling, "
                                   "fp32 accumulate (fp32-accurate); Cout<=16 layers bit-exact on CUDA cores"
@@ -610,10 +760,14 @@ def main():
                                   "3xTF32 tcgen05 (fp32-accurate); Cout<=16 layers bit-exact on CUDA cores"),
                "data": "synthetic (gen_synthetic, seeded; random-init He-uniform weights)",
                "config": config_dict(a, world),
-               "change": {"l1_changed_frac": l1_frac, "per_layer_changed_frac": per_layer},
+               "change": {"l1_changed_frac": l1_frac, "input_detected_frac": l1_det_frac,
+                          "x_axis_note": "l1_changed = the first layer's dilated output update set (its index "
+                                         "list); input_detected = pixels of the frame whose |x - s| > tau "
+                                         "before dilation (the paper's changed pixels, PAPER.md:213-214)",
+                          "per_layer_changed_frac": per_layer},
                "dense_path_fps": dense_fps, "speedup_vs_dense": (value / dense_fps) if dense_fps else None,
                "sweep": sweep, "crossover_l1_changed_pct": crossover,
-               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_f32": e2e_f32,
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_f32": e2e_f32, "parity": parity,
                "gpu_launches": launches * a.steps,
                "clocks": clocks.summary()}
         print(json.dumps(out))

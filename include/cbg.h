@@ -316,10 +316,21 @@ int cbg_net_copy_output_async(cbg_net net, int node, void* host_dst);
 int cbg_net_copy_output_detached(cbg_net net, int node, void* host_dst);
 void* cbg_ctx_copy_stream(cbg_ctx ctx);
 int cbg_net_output_bytes(cbg_net net, int node, int64_t* bytes);
-/* Asynchronous D2H copy of the per-frame change counts [slot][n_streams]
- * (int32) into host memory; node_slot (nullable) receives each node's slot. */
+/* Asynchronous D2H copy of the per-frame change counts [n_streams][slots]
+ * (int32, slots = cbg_net_count_slots) into host memory; node_slot (nullable)
+ * receives each node's slot. */
 int cbg_net_copy_counts_async(cbg_net net, int32_t* host_dst, int32_t* node_slot);
 int cbg_net_count_slots(cbg_net net, int* slots);
+/* Slot (in the same count array) of each node's detected input pixels before
+ * dilation (the detect map of a detect-policy conv, change.cpp:20-43), -1 for
+ * other nodes. Not a reference interface: the reference keeps this map
+ * internal to CBConvLayer::forward (layers.cpp:74-86); it is the paper's
+ * "changed pixels" of the input. */
+int cbg_net_detect_slots(cbg_net net, int32_t* det_slot);
+/* Labels ("<node>.<kernel>") of the kernels one frame launches with these
+ * forward flags, in launch order, as a JSON list (instrumentation: matches
+ * the timing report and ncu launch lists). */
+int cbg_net_kernel_labels(cbg_net net, unsigned flags, char* buf, int len);
 /* Debug builds only (-DCBG_TRACE, libcbg_trace.so): per-K-block clock64 timeline
  * of CTA 0 of the last GEMM launch, [6][4096]; returns entries copied (0 when
  * tracing is compiled out). */

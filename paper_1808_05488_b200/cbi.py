@@ -15,6 +15,7 @@ Data conventions (reference tensor.hpp / change.hpp):
 from __future__ import annotations
 
 import ctypes as C
+import json
 import enum
 from dataclasses import dataclass, field
 from typing import List, Optional, Sequence
@@ -896,12 +897,25 @@ class CBNetwork:
         copy-out stream: the next frame does not wait for PCIe (Context.synchronize waits for it)"""
         check(lib.cbg_net_copy_output_detached(self.handle, node, C.c_void_p(host_ptr)))
     def count_layout(self):
-        """(n_slots, node->slot) of the device change-count array [slot][S]."""
+        """(slots, node->slot) of the device change-count array [S][slots]."""
         n = C.c_int()
         check(lib.cbg_net_count_slots(self.handle, C.byref(n)))
         slots = np.zeros(len(self._nodes), np.int32)
         check(lib.cbg_net_copy_counts_async(self.handle, None, fptr(slots)))
         return n.value, slots
+
+    def kernel_labels(self, flags: int = 0):
+        """labels of the kernels one frame launches, in launch order"""
+        buf = C.create_string_buffer(1 << 16)
+        check(lib.cbg_net_kernel_labels(self.handle, flags, buf, len(buf)))
+        return json.loads(buf.value.decode())
+
+    def detect_slots(self):
+        """node -> slot of its detected (pre-dilation) input-pixel count in the
+        count array (-1: not a detect-policy conv)."""
+        slots = np.zeros(len(self._nodes), np.int32)
+        check(lib.cbg_net_detect_slots(self.handle, fptr(slots)))
+        return slots
 
     def copy_counts_async(self, host_ptr: int):
         check(lib.cbg_net_copy_counts_async(self.handle, C.c_void_p(host_ptr), None))

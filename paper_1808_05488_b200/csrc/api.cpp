@@ -380,6 +380,24 @@ int cbg_net_copy_counts_async(cbg_net net, int32_t* host_dst, int32_t* node_slot
     if (host_dst) net->net->copy_counts_async(host_dst);
   });
 }
+int cbg_net_kernel_labels(cbg_net net, unsigned flags, char* buf, int len) {
+  return guard([&] {
+    need(net, "cbg_net_kernel_labels");
+    need(buf, "cbg_net_kernel_labels");
+    std::string js = "[";
+    for (const std::string& l : net->net->kernel_labels(flags)) js += (js.size() > 1 ? ", \"" : "\"") + l + "\"";
+    js += "]";
+    if (static_cast<int>(js.size()) >= len) cbg::throw_invalid("cbg_net_kernel_labels: buffer too small");
+    std::memcpy(buf, js.c_str(), js.size() + 1);
+  });
+}
+int cbg_net_detect_slots(cbg_net net, int32_t* det_slot) {
+  return guard([&] {
+    need(net, "cbg_net_detect_slots");
+    need(det_slot, "cbg_net_detect_slots");
+    for (size_t i = 0; i < net->net->nodes().size(); ++i) det_slot[i] = net->net->det_slot(static_cast<int>(i));
+  });
+}
 int cbg_debug_gemm_trace(unsigned long long* buf, int n) { return cbg::conv_gemm_read_trace(buf, n); }
 int cbg_net_count_slots(cbg_net net, int* slots) {
   return guard([&] {

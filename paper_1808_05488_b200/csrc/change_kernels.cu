@@ -4,15 +4,17 @@
 //                   closed-loop state update        ref change.cpp:20-43
 //   detect_list     the same on NHWC inputs, walking only the producer's
 //                   update set                      ref change.cpp:20-43
-//   dilate_compact  window dilation of (OR-ed) change maps fused with the
-//                   stream compaction into the index list (row-major runs
-//                   per tile, one atomic offset per tile)
+//   dilate_compact  window dilation of (OR-ed) change bitmaps fused with the
+//                   stream compaction into the index list (one warp per
+//                   band of rows, row-major runs placed by one atomicAdd
+//                   each), optionally with a following 2x2 pool's map/list
 //                                                   ref change.cpp:45-84
 //   pool            change-based max pooling       ref layers.cpp:148-179
 //   join            Add / Concat at changed pixels  ref network.cpp:364-398
 //
 // Arithmetic is exact IEEE fp32 (no fast-math): |x - s| > tau and the max
 // comparisons are bit-identical to the reference.
+#include <algorithm>
 #include <cstdio>
 
 #include "common.cuh"
@@ -47,92 +49,136 @@ int sm_count() {
 }
 
 // ---------------------------------------------------------------------------
+// Change-map output of the detect kernels (bitmaps, common.cuh).
+// ---------------------------------------------------------------------------
+// One 4-pixel group q (pixels 4q..4q+3), bit j of ch = pixel 4q+j changed,
+// into a map begin_frame cleared. plain (W % 32 == 0): the 8 groups of a word
+// are 8 consecutive lanes (group ids are lane-aligned), so a warp with any
+// change OR-s each word over its 8 lanes with shuffles and stores it whole
+// (the word belongs to those lanes alone); the common all-unchanged warp pays
+// one vote. Otherwise (a group may straddle rows) changed pixels are OR-ed in
+// one by one. Every lane of the warp must call it (warp-uniform loop trips).
+CBG_DEV void put_quad(uint32_t* m, long long q, bool valid, uint32_t ch, int W, int plain) {
+  if (!__any_sync(0xffffffffu, ch != 0u)) return;
+  if (plain) {
+    uint32_t v = ch << (4 * (threadIdx.x & 7));
+    v |= __shfl_xor_sync(0xffffffffu, v, 1);
+    v |= __shfl_xor_sync(0xffffffffu, v, 2);
+    v |= __shfl_xor_sync(0xffffffffu, v, 4);
+    if (valid && v && (threadIdx.x & 7) == 0) m[q >> 3] = v;
+  } else if (valid && ch) {
+    for (int j = 0; j < 4; ++j)
+      if ((ch >> j) & 1u) map_set(m, (q << 2) + j, W);
+  }
+}
+
+// detected-pixel count of a stream (dc: its counter): one atomicAdd per CTA
+// (warp sums combined in shared memory), plus every pixel on a full update.
+// Every thread of the CTA must call it.
+CBG_DEV void detect_count(int32_t* dc, int nch, bool boot, long long HW) {
+  __shared__ int s_cnt;
+  if (threadIdx.x == 0) s_cnt = 0;
+  __syncthreads();
+  nch = __reduce_add_sync(0xffffffffu, nch);
+  if ((threadIdx.x & 31) == 0 && nch) atomicAdd(&s_cnt, nch);
+  __syncthreads();
+  if (threadIdx.x == 0 && dc) {
+    const int v = s_cnt + ((boot && blockIdx.x == 0) ? static_cast<int>(HW) : 0);
+    if (v) atomicAdd(dc, v);
+  }
+}
+
+// ---------------------------------------------------------------------------
 // detect on the network-input frame. One thread per pixel: the C channel
 // planes are read coalesced, the NHWC state as one 16-B vector per 4 channels.
 // ---------------------------------------------------------------------------
 template <bool kVec4>
 __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs a) {
   const int s = blockIdx.y;
-  const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
   const float* x = *a.x_slot + static_cast<long long>(s) * a.x_sstride;
   float* st = a.state + static_cast<long long>(s) * HW * a.Cs;
-  uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  uint32_t* m = a.map + static_cast<long long>(s) * a.H * map_words(a.W);
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
+  const int lane = threadIdx.x & 31;
   float vmax = 0.0f;
+  int nch = 0;
   if constexpr (kVec4) {
     // C <= 4 (Cs == 4), HW % 4 == 0: one thread = 4 consecutive pixels; the C
     // planes are read as float4, the 4 NHWC state vectors as 4 float4.
     const long long n4 = HW >> 2;
-    for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
+    for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q - lane < n4;
          q += static_cast<long long>(gridDim.x) * blockDim.x) {
-      const long long p0 = q << 2;
-      float4 xv[4];
+      const bool valid = q < n4;
+      uint32_t ch = 0;
+      if (valid) {
+        const long long p0 = q << 2;
+        float4 xv[4];
 #pragma unroll
-      for (int c = 0; c < 4; ++c)
-        xv[c] = c < a.C ? ldg_nc_f4(x + c * HW + p0) : make_float4(0.f, 0.f, 0.f, 0.f);
-      float4 sv[4];
-      if (!boot) {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) sv[j] = *reinterpret_cast<const float4*>(st + (p0 + j) * 4);
-      }
-      uint32_t mark = 0;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const float px[4] = {(&xv[0].x)[j], (&xv[1].x)[j], (&xv[2].x)[j], (&xv[3].x)[j]};
-        bool changed = false;
+        for (int c = 0; c < 4; ++c)
+          xv[c] = c < a.C ? ldg_nc_f4(x + c * HW + p0) : make_float4(0.f, 0.f, 0.f, 0.f);
+        float4 sv[4];
         if (!boot) {
-          const float sp[4] = {sv[j].x, sv[j].y, sv[j].z, sv[j].w};
 #pragma unroll
-          for (int c = 0; c < 4; ++c)
-            if (c < a.C) changed |= fabsf(px[c] - sp[c]) > tau;
+          for (int j = 0; j < 4; ++j) sv[j] = *reinterpret_cast<const float4*>(st + (p0 + j) * 4);
         }
-        if (changed || write_all) {
-          *reinterpret_cast<float4*>(st + (p0 + j) * 4) = make_float4(px[0], px[1], px[2], px[3]);
-          vmax = fmaxf(vmax, fmaxf(fmaxf(fabsf(px[0]), fabsf(px[1])), fmaxf(fabsf(px[2]), fabsf(px[3]))));
-        }
-        if (changed) mark |= static_cast<uint32_t>(e) << (8 * j);
-      }
-      if (mark) {  // only changed pixels get the epoch tag; others keep stale tags
-#pragma unroll
-        for (int j = 0; j < 4; ++j)
-          if ((mark >> (8 * j)) & 0xffu) m[p0 + j] = e;
-      }
-    }
-    warp_amax(a.amax ? a.amax + s : nullptr, vmax);
-    return;
-  }
-  for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < HW;
-       p += static_cast<long long>(gridDim.x) * blockDim.x) {
-    float* sp = st + p * a.Cs;
-    bool changed = false;
-    if (!boot) {
-      for (int c0 = 0; c0 < a.Cs; c0 += 4) {
-        const float4 sv = *reinterpret_cast<const float4*>(sp + c0);
-        const float s4[4] = {sv.x, sv.y, sv.z, sv.w};
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
-          const int c = c0 + j;
-          if (c < a.C) changed |= fabsf(__ldg(x + c * HW + p) - s4[j]) > tau;
+          const float px[4] = {(&xv[0].x)[j], (&xv[1].x)[j], (&xv[2].x)[j], (&xv[3].x)[j]};
+          bool changed = false;
+          if (!boot) {
+            const float sp[4] = {sv[j].x, sv[j].y, sv[j].z, sv[j].w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+              if (c < a.C) changed |= fabsf(px[c] - sp[c]) > tau;
+          }
+          if (changed || write_all) {
+            *reinterpret_cast<float4*>(st + (p0 + j) * 4) = make_float4(px[0], px[1], px[2], px[3]);
+            vmax = fmaxf(vmax, fmaxf(fmaxf(fabsf(px[0]), fabsf(px[1])), fmaxf(fabsf(px[2]), fabsf(px[3]))));
+          }
+          ch |= static_cast<uint32_t>(changed) << j;
         }
       }
-      if (changed) m[p] = e;
+      put_quad(m, q, valid, ch, a.W, a.map_plain);
+      nch += __popc(ch);
     }
-    if (changed || write_all) {
-      for (int c0 = 0; c0 < a.Cs; c0 += 4) {
-        float v[4];
+  } else {
+    for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < HW;
+         p += static_cast<long long>(gridDim.x) * blockDim.x) {
+      float* sp = st + p * a.Cs;
+      bool changed = false;
+      if (!boot) {
+        for (int c0 = 0; c0 < a.Cs; c0 += 4) {
+          const float4 sv = *reinterpret_cast<const float4*>(sp + c0);
+          const float s4[4] = {sv.x, sv.y, sv.z, sv.w};
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          v[j] = (c0 + j < a.C) ? __ldg(x + (c0 + j) * HW + p) : 0.0f;
-          vmax = fmaxf(vmax, fabsf(v[j]));
+          for (int j = 0; j < 4; ++j) {
+            const int c = c0 + j;
+            if (c < a.C) changed |= fabsf(__ldg(x + c * HW + p) - s4[j]) > tau;
+          }
         }
-        *reinterpret_cast<float4*>(sp + c0) = make_float4(v[0], v[1], v[2], v[3]);
+        if (changed) {
+          map_set(m, p, a.W);
+          ++nch;
+        }
+      }
+      if (changed || write_all) {
+        for (int c0 = 0; c0 < a.Cs; c0 += 4) {
+          float v[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            v[j] = (c0 + j < a.C) ? __ldg(x + (c0 + j) * HW + p) : 0.0f;
+            vmax = fmaxf(vmax, fabsf(v[j]));
+          }
+          *reinterpret_cast<float4*>(sp + c0) = make_float4(v[0], v[1], v[2], v[3]);
+        }
       }
     }
   }
   warp_amax(a.amax ? a.amax + s : nullptr, vmax);
+  detect_count(a.det_count ? a.det_count + s * a.cnt_stride : nullptr, nch, boot, HW);
 }
 
 // ---------------------------------------------------------------------------
@@ -145,76 +191,78 @@ __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs 
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kFrameThreads) detect_frame_chw_kernel(DetectFrameArgs a) {
   const int s = blockIdx.y;
-  const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
   const float* x = *a.x_slot + static_cast<long long>(s) * a.x_sstride;
   float* st = a.state + static_cast<long long>(s) * a.C * HW;
-  uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  uint32_t* m = a.map + static_cast<long long>(s) * a.H * map_words(a.W);
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
   const long long n4 = HW >> 2;
+  const int lane = threadIdx.x & 31;
   float vmax = 0.0f;
-  for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
+  int nch = 0;
+  for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q - lane < n4;
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long p0 = q << 2;
-    float4 xv[4], sv[4];
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      if (c < a.C) {
-        xv[c] = ldg_nc_f4(x + c * HW + p0);
-        if (!boot) sv[c] = *reinterpret_cast<const float4*>(st + c * HW + p0);
-      }
-    }
+    const bool valid = q < n4;
     uint32_t ch = 0;  // bit j: pixel p0+j changed
-    if (!boot) {
+    if (valid) {
+      const long long p0 = q << 2;
+      float4 xv[4], sv[4];
 #pragma unroll
       for (int c = 0; c < 4; ++c) {
         if (c < a.C) {
-          ch |= static_cast<uint32_t>(fabsf(xv[c].x - sv[c].x) > tau) << 0;
-          ch |= static_cast<uint32_t>(fabsf(xv[c].y - sv[c].y) > tau) << 1;
-          ch |= static_cast<uint32_t>(fabsf(xv[c].z - sv[c].z) > tau) << 2;
-          ch |= static_cast<uint32_t>(fabsf(xv[c].w - sv[c].w) > tau) << 3;
+          xv[c] = ldg_nc_f4(x + c * HW + p0);
+          if (!boot) sv[c] = *reinterpret_cast<const float4*>(st + c * HW + p0);
         }
       }
-    }
-    if (write_all || ch) {
+      if (!boot) {
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if (c < a.C) {
-          float4 v = xv[c];
-          if (!write_all) {  // keep unchanged pixels' state (same bits written back)
-            if (!(ch & 1u)) v.x = sv[c].x;
-            if (!(ch & 2u)) v.y = sv[c].y;
-            if (!(ch & 4u)) v.z = sv[c].z;
-            if (!(ch & 8u)) v.w = sv[c].w;
+        for (int c = 0; c < 4; ++c) {
+          if (c < a.C) {
+            ch |= static_cast<uint32_t>(fabsf(xv[c].x - sv[c].x) > tau) << 0;
+            ch |= static_cast<uint32_t>(fabsf(xv[c].y - sv[c].y) > tau) << 1;
+            ch |= static_cast<uint32_t>(fabsf(xv[c].z - sv[c].z) > tau) << 2;
+            ch |= static_cast<uint32_t>(fabsf(xv[c].w - sv[c].w) > tau) << 3;
           }
-          *reinterpret_cast<float4*>(st + c * HW + p0) = v;
-          vmax = fmaxf(vmax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+        }
+      }
+      if (write_all || ch) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if (c < a.C) {
+            float4 v = xv[c];
+            if (!write_all) {  // keep unchanged pixels' state (same bits written back)
+              if (!(ch & 1u)) v.x = sv[c].x;
+              if (!(ch & 2u)) v.y = sv[c].y;
+              if (!(ch & 4u)) v.z = sv[c].z;
+              if (!(ch & 8u)) v.w = sv[c].w;
+            }
+            *reinterpret_cast<float4*>(st + c * HW + p0) = v;
+            vmax = fmaxf(vmax, fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w))));
+          }
         }
       }
     }
-    if (ch) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if ((ch >> j) & 1u) m[p0 + j] = e;
-    }
+    put_quad(m, q, valid, ch, a.W, a.map_plain);
+    nch += __popc(ch);
   }
   warp_amax(a.amax ? a.amax + s : nullptr, vmax);
+  detect_count(a.det_count ? a.det_count + s * a.cnt_stride : nullptr, nch, boot, HW);
 }
 
 // scalar fallback (any C, any HW): CHW state, one thread per pixel
 __global__ void __launch_bounds__(kThreads) detect_frame_chw_scalar_kernel(DetectFrameArgs a) {
   const int s = blockIdx.y;
-  const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
   const float* x = *a.x_slot + static_cast<long long>(s) * a.x_sstride;
   float* st = a.state + static_cast<long long>(s) * a.C * HW;
-  uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  uint32_t* m = a.map + static_cast<long long>(s) * a.H * map_words(a.W);
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
   float vmax = 0.0f;
+  int nch = 0;
   for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < HW;
        p += static_cast<long long>(gridDim.x) * blockDim.x) {
     bool changed = false;
@@ -226,9 +274,13 @@ __global__ void __launch_bounds__(kThreads) detect_frame_chw_scalar_kernel(Detec
         st[c * HW + p] = v;
         vmax = fmaxf(vmax, fabsf(v));
       }
-    if (changed) m[p] = e;
+    if (changed) {
+      map_set(m, p, a.W);
+      ++nch;
+    }
   }
   warp_amax(a.amax ? a.amax + s : nullptr, vmax);
+  detect_count(a.det_count ? a.det_count + s * a.cnt_stride : nullptr, nch, boot, HW);
 }
 
 // ---------------------------------------------------------------------------
@@ -254,122 +306,126 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(Detec
   constexpr int CM = kC ? kC : 4;  // register arrays
   const int s = blockIdx.y;
   const int CC = kC ? kC : a.C;
-  const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
   const uint8_t* x8 = *a.x8_slot + static_cast<long long>(s) * CC * HW;
   float* st = a.state + static_cast<long long>(s) * (kChw ? CC : a.Cs) * HW;
-  uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  uint32_t* m = a.map + static_cast<long long>(s) * a.H * map_words(a.W);
   uint8_t* s8 = a.state8 ? a.state8 + static_cast<long long>(s) * CC * HW : nullptr;
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
   const long long n4 = HW >> 2;
+  const int lane = threadIdx.x & 31;
   float vmax = 0.0f;
-  for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q < n4;
+  int nch = 0;
+  for (long long q = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q - lane < n4;
        q += static_cast<long long>(gridDim.x) * blockDim.x) {
-    const long long p0 = q << 2;
-    // 4 pixels x C bytes = C words, 4-byte aligned (byte offset 4*C*q)
-    uint32_t wd[CM];
-    const uint32_t* src = reinterpret_cast<const uint32_t*>(x8 + p0 * CC);
-#pragma unroll
-    for (int i = 0; i < CM; ++i) wd[i] = i < CC ? __ldg(src + i) : 0u;
-    float px[4][CM];  // [pixel][channel]
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int c = 0; c < CM; ++c) {
-        if (c < CC) {
-          const int b = j * CC + c;  // byte index within the 4-pixel group
-          px[j][c] = byte_to_unit(wd[b >> 2], b);
-        } else {
-          px[j][c] = 0.0f;
-        }
-      }
+    const bool valid = q < n4;
     uint32_t ch = 0;
-    float sv[4][CM];
-    if (!boot) {
-      if constexpr (kChw) {
+    if (valid) {
+      const long long p0 = q << 2;
+      // 4 pixels x C bytes = C words, 4-byte aligned (byte offset 4*C*q)
+      uint32_t wd[CM];
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(x8 + p0 * CC);
 #pragma unroll
-        for (int c = 0; c < CM; ++c)
-          if (c < CC) {
-            const float4 v = *reinterpret_cast<const float4*>(st + c * HW + p0);
-            sv[0][c] = v.x, sv[1][c] = v.y, sv[2][c] = v.z, sv[3][c] = v.w;
-          }
-      } else {
-#pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const float4 v = *reinterpret_cast<const float4*>(st + (p0 + j) * 4);
-          const float vv[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-          for (int c = 0; c < CM; ++c) sv[j][c] = vv[c];
-        }
-      }
+      for (int i = 0; i < CM; ++i) wd[i] = i < CC ? __ldg(src + i) : 0u;
+      float px[4][CM];  // [pixel][channel]
 #pragma unroll
       for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int c = 0; c < CM; ++c)
-          if (c < CC && fabsf(px[j][c] - sv[j][c]) > tau) ch |= 1u << j;
-    }
-    if (write_all || ch) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (write_all || ((ch >> j) & 1u))
-#pragma unroll
-          for (int c = 0; c < CM; ++c) vmax = fmaxf(vmax, px[j][c]);
-      if constexpr (kChw) {
 #pragma unroll
         for (int c = 0; c < CM; ++c) {
           if (c < CC) {
-            float v[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) v[j] = (write_all || ((ch >> j) & 1u)) ? px[j][c] : sv[j][c];
-            *reinterpret_cast<float4*>(st + c * HW + p0) = make_float4(v[0], v[1], v[2], v[3]);
+            const int b = j * CC + c;  // byte index within the 4-pixel group
+            px[j][c] = byte_to_unit(wd[b >> 2], b);
+          } else {
+            px[j][c] = 0.0f;
           }
         }
-      } else {
+      float sv[4][CM];
+      if (!boot) {
+        if constexpr (kChw) {
+#pragma unroll
+          for (int c = 0; c < CM; ++c)
+            if (c < CC) {
+              const float4 v = *reinterpret_cast<const float4*>(st + c * HW + p0);
+              sv[0][c] = v.x, sv[1][c] = v.y, sv[2][c] = v.z, sv[3][c] = v.w;
+            }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const float4 v = *reinterpret_cast<const float4*>(st + (p0 + j) * 4);
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int c = 0; c < CM; ++c) sv[j][c] = vv[c];
+          }
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int c = 0; c < CM; ++c)
+            if (c < CC && fabsf(px[j][c] - sv[j][c]) > tau) ch |= 1u << j;
+      }
+      if (write_all || ch) {
 #pragma unroll
         for (int j = 0; j < 4; ++j)
           if (write_all || ((ch >> j) & 1u))
-            *reinterpret_cast<float4*>(st + (p0 + j) * 4) = make_float4(px[j][0], CM > 1 ? px[j][1 % CM] : 0.f, CM > 2 ? px[j][2 % CM] : 0.f, CM > 3 ? px[j][3 % CM] : 0.f);
+#pragma unroll
+            for (int c = 0; c < CM; ++c) vmax = fmaxf(vmax, px[j][c]);
+        if constexpr (kChw) {
+#pragma unroll
+          for (int c = 0; c < CM; ++c) {
+            if (c < CC) {
+              float v[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) v[j] = (write_all || ((ch >> j) & 1u)) ? px[j][c] : sv[j][c];
+              *reinterpret_cast<float4*>(st + c * HW + p0) = make_float4(v[0], v[1], v[2], v[3]);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if (write_all || ((ch >> j) & 1u))
+              *reinterpret_cast<float4*>(st + (p0 + j) * 4) = make_float4(px[j][0], CM > 1 ? px[j][1 % CM] : 0.f, CM > 2 ? px[j][2 % CM] : 0.f, CM > 3 ? px[j][3 % CM] : 0.f);
+        }
+      }
+      // the 8-bit shadow takes the frame's words on a full update; this kernel
+      // does not track it at changed pixels, so it is valid again only after the
+      // stream's next full update (detect_frame_s8_kernel keeps it current)
+      if (s8 && write_all) {
+        uint32_t* sdst = reinterpret_cast<uint32_t*>(s8 + p0 * CC);
+#pragma unroll
+        for (int i = 0; i < CM; ++i)
+          if (i < CC) sdst[i] = wd[i];
       }
     }
-    // the 8-bit shadow takes the frame's words on a full update; this kernel
-    // does not track it at changed pixels, so it is valid again only after the
-    // stream's next full update (detect_frame_s8_kernel keeps it current)
-    if (s8 && write_all) {
-      uint32_t* sdst = reinterpret_cast<uint32_t*>(s8 + p0 * CC);
-#pragma unroll
-      for (int i = 0; i < CM; ++i)
-        if (i < CC) sdst[i] = wd[i];
-    }
-    if (ch) {
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if ((ch >> j) & 1u) m[p0 + j] = e;
-    }
+    put_quad(m, q, valid, ch, a.W, a.map_plain);
+    nch += __popc(ch);
   }
   warp_amax(a.amax ? a.amax + s : nullptr, vmax);
+  detect_count(a.det_count ? a.det_count + s * a.cnt_stride : nullptr, nch, boot, HW);
 }
 
 // The 8-bit shadow path on its own (3 channels, CHW fp32 state): everything it
 // reads is bytes (12 B of frame + 12 B of shadow per 4 pixels), so each thread
 // batches kQ quads, a grid stride apart, with all their loads issued first.
-template <int kQ>
+template <int kQ, bool kPlain>
 __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_s8_kernel(DetectFrameArgs a) {
   const int s = blockIdx.y;
-  const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
   const uint8_t* x8 = *a.x8_slot + static_cast<long long>(s) * 3 * HW;
   uint8_t* s8 = a.state8 + static_cast<long long>(s) * 3 * HW;
   float* st = a.state + static_cast<long long>(s) * 3 * HW;
-  uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  uint32_t* m = a.map + static_cast<long long>(s) * a.H * map_words(a.W);
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
   const long long n4 = HW >> 2;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
+  const int lane = threadIdx.x & 31;
   float vmax = 0.0f;
-  for (long long q0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q0 < n4; q0 += kQ * stride) {
+  int nch = 0;
+  for (long long q0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q0 - lane < n4;
+       q0 += kQ * stride) {
     uint32_t wd[kQ][3], sw[kQ][3];
 #pragma unroll
     for (int u = 0; u < kQ; ++u) {
@@ -384,71 +440,95 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_s8_kernel(Detec
         }
       }
     }
+    uint32_t chq[kQ];
 #pragma unroll
     for (int u = 0; u < kQ; ++u) {
       const long long q = q0 + u * stride;
-      if (q >= n4) continue;
-      const long long p0 = q << 2;
+      const bool valid = q < n4;
       uint32_t ch = 0;
       // a quad whose 12 bytes equal the shadow cannot change (|x - s| = 0 <= tau):
       // the common case skips the per-byte comparisons
-      const bool same = (wd[u][0] == sw[u][0]) & (wd[u][1] == sw[u][1]) & (wd[u][2] == sw[u][2]);
-      if (!boot && (!same || tau < 0.0f)) {
+      if (valid && !boot) {
+        const bool same = (wd[u][0] == sw[u][0]) & (wd[u][1] == sw[u][1]) & (wd[u][2] == sw[u][2]);
+        if (!same || tau < 0.0f) {
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          bool cj = false;
+          for (int j = 0; j < 4; ++j) {
+            bool cj = false;
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            const int b = 3 * j + c;
-            cj |= fabsf(byte_to_unit(wd[u][b >> 2], b) - byte_to_unit(sw[u][b >> 2], b)) > tau;
+            for (int c = 0; c < 3; ++c) {
+              const int b = 3 * j + c;
+              cj |= fabsf(byte_to_unit(wd[u][b >> 2], b) - byte_to_unit(sw[u][b >> 2], b)) > tau;
+            }
+            ch |= static_cast<uint32_t>(cj) << j;
           }
-          ch |= static_cast<uint32_t>(cj) << j;
         }
       }
-      if (!(write_all || ch)) continue;
+      if (valid && (write_all || ch)) {
+        const long long p0 = q << 2;
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        float v[4];
+        for (int c = 0; c < 3; ++c) {
+          float v[4];
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          const int b = 3 * j + c;
-          const bool take = write_all || ((ch >> j) & 1u);
-          v[j] = byte_to_unit(take ? wd[u][b >> 2] : sw[u][b >> 2], b);
-          if (take) vmax = fmaxf(vmax, v[j]);
+          for (int j = 0; j < 4; ++j) {
+            const int b = 3 * j + c;
+            const bool take = write_all || ((ch >> j) & 1u);
+            v[j] = byte_to_unit(take ? wd[u][b >> 2] : sw[u][b >> 2], b);
+            if (take) vmax = fmaxf(vmax, v[j]);
+          }
+          *reinterpret_cast<float4*>(st + c * HW + p0) = make_float4(v[0], v[1], v[2], v[3]);
         }
-        *reinterpret_cast<float4*>(st + c * HW + p0) = make_float4(v[0], v[1], v[2], v[3]);
+        uint32_t* sdst = reinterpret_cast<uint32_t*>(s8 + 12 * q);
+#pragma unroll
+        for (int i = 0; i < 3; ++i) {
+          uint32_t keep = 0;  // bytes of unchanged pixels keep the old state
+          if (!write_all)
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (!((ch >> ((4 * i + k) / 3)) & 1u)) keep |= 0xFFu << (8 * k);
+          sdst[i] = (wd[u][i] & ~keep) | (sw[u][i] & keep);
+        }
       }
-      uint32_t* sdst = reinterpret_cast<uint32_t*>(s8 + 12 * q);
+      chq[u] = valid ? ch : 0u;
+      nch += __popc(ch);
+    }
+    // map bits of the kQ groups: one vote for all of them (put_quad)
+    uint32_t any = 0;
 #pragma unroll
-      for (int i = 0; i < 3; ++i) {
-        uint32_t keep = 0;  // bytes of unchanged pixels keep the old state
-        if (!write_all)
+    for (int u = 0; u < kQ; ++u) any |= chq[u];
+    if (__any_sync(0xffffffffu, any != 0u)) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            if (!((ch >> ((4 * i + k) / 3)) & 1u)) keep |= 0xFFu << (8 * k);
-        sdst[i] = (wd[u][i] & ~keep) | (sw[u][i] & keep);
+      for (int u = 0; u < kQ; ++u) {
+        const long long q = q0 + u * stride;
+        if constexpr (kPlain) {
+          uint32_t v = chq[u] << (4 * (threadIdx.x & 7));
+          v |= __shfl_xor_sync(0xffffffffu, v, 1);
+          v |= __shfl_xor_sync(0xffffffffu, v, 2);
+          v |= __shfl_xor_sync(0xffffffffu, v, 4);
+          if (v && (threadIdx.x & 7) == 0) m[q >> 3] = v;  // (v != 0 only for valid groups)
+        } else {
+          for (int j = 0; j < 4; ++j)
+            if ((chq[u] >> j) & 1u) map_set(m, (q << 2) + j, a.W);
+        }
       }
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if ((ch >> j) & 1u) m[p0 + j] = e;
     }
   }
   warp_amax(a.amax ? a.amax + s : nullptr, vmax);
+  detect_count(a.det_count ? a.det_count + s * a.cnt_stride : nullptr, nch, boot, HW);
 }
 
 // scalar fallback for 8-bit frames (HW % 4 != 0)
 __global__ void __launch_bounds__(kThreads) detect_frame_u8_scalar_kernel(DetectFrameArgs a) {
   const int s = blockIdx.y;
-  const uint8_t e = epoch8(*a.frame);
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
   const uint8_t* x8 = *a.x8_slot + static_cast<long long>(s) * a.C * HW;
   const bool chw = a.state_chw != 0;
   float* st = a.state + static_cast<long long>(s) * (chw ? a.C : a.Cs) * HW;
-  uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  uint32_t* m = a.map + static_cast<long long>(s) * a.H * map_words(a.W);
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
   float vmax = 0.0f;
+  int nch = 0;
   for (long long p = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; p < HW;
        p += static_cast<long long>(gridDim.x) * blockDim.x) {
     auto sidx = [&](int c) { return chw ? c * HW + p : p * a.Cs + c; };
@@ -462,9 +542,13 @@ __global__ void __launch_bounds__(kThreads) detect_frame_u8_scalar_kernel(Detect
         st[sidx(c)] = v;
         vmax = fmaxf(vmax, v);
       }
-    if (changed) m[p] = e;
+    if (changed) {
+      map_set(m, p, a.W);
+      ++nch;
+    }
   }
   warp_amax(a.amax ? a.amax + s : nullptr, vmax);
+  detect_count(a.det_count ? a.det_count + s * a.cnt_stride : nullptr, nch, boot, HW);
 }
 
 // ---------------------------------------------------------------------------
@@ -477,7 +561,6 @@ template <int kCache>
 __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListArgs a, int glog) {
   const int s = blockIdx.y;
   const uint32_t fno = *a.frame;
-  const uint8_t e = epoch8(fno);
   const bool boot = a.boot[s] != 0;
   // pre-split copy: if the GEMM's exponent moved since the copy was split,
   // this frame rewrites the whole copy (dense walk; dense detection gives the
@@ -501,10 +584,10 @@ __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListAr
   };
   const bool dense = boot || resplit || a.prod_idx == nullptr || (a.dense != nullptr && *a.dense != 0);
   const long long HW = static_cast<long long>(a.H) * a.W;
-  const long long n = dense ? HW : a.prod_count[s];
+  const long long n = dense ? HW : a.prod_count[s * a.cnt_stride];
   const float* x = a.x + static_cast<long long>(s) * HW * a.Cs;
   float* st = a.state + static_cast<long long>(s) * HW * a.Cs;
-  uint8_t* m = a.map + static_cast<long long>(s) * HW;
+  uint32_t* m = a.map + static_cast<long long>(s) * a.H * map_words(a.W);
   const int32_t* list = dense ? nullptr : a.prod_idx + static_cast<long long>(s) * HW;
 
   const int g = 1 << glog;
@@ -517,6 +600,7 @@ __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListAr
   const unsigned gmask = (g == 32 ? 0xffffffffu : ((1u << g) - 1u)) << ((lane >> glog) * g);
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
+  int nch = 0;
 
   const long long step = static_cast<long long>(gridDim.x) * wpb * gpw;
   const long long base0 = (static_cast<long long>(blockIdx.x) * wpb + warp) * gpw;
@@ -586,45 +670,23 @@ __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListAr
       for (int v = sub; v < nv; v += g)
         put_split(static_cast<long long>(s) * HW * a.Cs + p * a.Cs + 4 * v, *reinterpret_cast<const float4*>(sp + 4 * v));
     }
-    if (active && any && !boot && sub == 0) m[p] = e;
-  }
-}
-
-// ---------------------------------------------------------------------------
-// dilate + compact. Tile = rows_per_tile output rows (<= 32 pixels/thread).
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ int block_exclusive_scan(int v, int* s_warp, int& total) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int inc = v;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int u = __shfl_up_sync(0xffffffffu, inc, o);
-    if (lane >= o) inc += u;
-  }
-  if (lane == 31) s_warp[warp] = inc;
-  __syncthreads();
-  if (warp == 0) {
-    int w = lane < nw ? s_warp[lane] : 0;
-    int wi = w;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int u = __shfl_up_sync(0xffffffffu, wi, o);
-      if (lane >= o) wi += u;
+    if (active && any && !boot && sub == 0) {
+      map_set(m, p, a.W);
+      ++nch;
     }
-    if (lane < nw) s_warp[lane] = wi - w;  // exclusive warp offsets
-    if (lane == nw - 1) s_warp[32] = wi;   // block total
   }
-  __syncthreads();
-  total = s_warp[32];
-  return s_warp[warp] + inc - v;
+  detect_count(a.det_count ? a.det_count + s * a.cnt_stride : nullptr, nch, boot, HW);
 }
 
+// ---------------------------------------------------------------------------
+// dilate + compact on bitmaps: one warp per band of output rows.
+// ---------------------------------------------------------------------------
 // 32 bits of a bit-row starting at bit position B (bits outside [0, 32*nw) are 0).
 CBG_DEV uint32_t bits_at(const uint32_t* row, int nw, int B) {
   const int w = B >> 5, o = B & 31;  // arithmetic shift: floor for negative B
-  const uint32_t lo = (w >= 0 && w < nw) ? row[w] : 0u;
+  const uint32_t lo = (w >= 0 && w < nw) ? __ldg(row + w) : 0u;
   if (o == 0) return lo;
-  const uint32_t hi = (w + 1 >= 0 && w + 1 < nw) ? row[w + 1] : 0u;
+  const uint32_t hi = (w + 1 >= 0 && w + 1 < nw) ? __ldg(row + w + 1) : 0u;
   return __funnelshift_r(lo, hi, o);
 }
 
@@ -641,202 +703,158 @@ CBG_DEV uint32_t even_bits(uint32_t lo, uint32_t hi) {
   return squeeze(lo) | (squeeze(hi) << 16);
 }
 
-#ifdef CBG_DCTRACE
-#define DCT_DECL long long dct_t[8] = {0}; const long long dct_s = clock64()
-#define DCT(i) dct_t[i] = clock64() - dct_s
-#define DCT_PRINT if (threadIdx.x == 0 && (blockIdx.x == 5 || blockIdx.x == 15) && blockIdx.y < 2) \
-  printf("DCT %d %d n_tiles %d: %lld %lld %lld %lld %lld %lld %lld\n", blockIdx.x, blockIdx.y, a.n_tiles, dct_t[0], \
-         dct_t[1], dct_t[2], dct_t[3], dct_t[4], dct_t[5], dct_t[6])
-#else
-#define DCT_DECL do { } while (0)
-#define DCT(i) do { } while (0)
-#define DCT_PRINT do { } while (0)
-#endif
+CBG_DEV uint32_t row_mask(int W, int wo) {  // valid bits of word wo of a W-pixel row
+  const int v = W - wo * 32;
+  return v >= 32 ? 0xffffffffu : (v <= 0 ? 0u : ((1u << v) - 1u));
+}
 
-// Tile = rows_per_tile output rows. Maps are staged as bit-rows (32 pixels per
-// word, built with warp ballots), dilated separably in the bit domain
-// (horizontal: funnel-shift ORs, vertical: word ORs), counted with popc and
-// compacted: row-major inside the tile, tiles placed by one atomicAdd each.
-// <= 40 registers: a 256-thread CTA fits beside a persistent GEMM CTA (672 x 80)
-__global__ void __launch_bounds__(kThreads, 6) dilate_compact_kernel(DilateCompactArgs a) {
-  extern __shared__ __align__(16) uint32_t smw[];
-  __shared__ int s_warp[33];
-  __shared__ int s_prefix;
-  const int s = blockIdx.y, t = blockIdx.x;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  DCT_DECL;
-  const uint32_t f = *a.frame;
-  const uint8_t e = epoch8(f);
-  const bool boot = a.boot[s] != 0;
-  DCT(0);
-  const int r0 = t * a.rows_per_tile;
-  const int r1 = min(r0 + a.rows_per_tile, a.Hout);
-  const int nrows = r1 - r0;
-  const long long HWin = static_cast<long long>(a.Hin) * a.Win;
-  const long long HWout = static_cast<long long>(a.Hout) * a.Wout;
+// Store the words of one warp (word i of a band of nw-word rows starting at
+// row r0; the band's rows are contiguous in the map) and append their marked
+// pixels to the list: one atomicAdd on the stream's count per warp places the
+// warp's run (row-major); a nonzero word's pixels are written by the lanes of
+// its bits (coalesced). Every lane of the warp must call it (v = 0 for lanes
+// without a word).
+CBG_DEV void emit_words(uint32_t v, bool valid, int i, int r0, int nw, int W, uint32_t* gmap, int32_t* list,
+                        int32_t* ctr) {
+  const int lane = threadIdx.x & 31;
+  if (valid) gmap[i] = v;
+  const int cnt = __reduce_add_sync(0xffffffffu, __popc(v));
+  if (cnt == 0) return;
+  int base = 0;
+  if (lane == 0) base = atomicAdd(ctr, cnt);
+  base = __shfl_sync(0xffffffffu, base, 0);
+  const uint32_t below = (1u << lane) - 1u;
+  const int i0 = i - lane;
+  uint32_t nz = __ballot_sync(0xffffffffu, v != 0u);
+  while (nz) {
+    const int k = __ffs(nz) - 1;
+    nz &= nz - 1;
+    const uint32_t wk = __shfl_sync(0xffffffffu, v, k);
+    const int rr = (i0 + k) / nw, wo = (i0 + k) - rr * nw;
+    if ((wk >> lane) & 1u) list[base + __popc(wk & below)] = (r0 + rr) * W + wo * 32 + lane;
+    base += __popc(wk);
+  }
+}
+
+// CTA = band of `rows` output rows of one stream, one thread per output word:
+// OR the window's source words over its input rows (vertical), then dilate
+// the OR-ed row horizontally with funnel shifts (stride 2 compacts the even
+// bits); the loads are independent and mostly L1 hits (neighbouring words and
+// rows share them). Pinned (cropped) output dims and border clipping follow
+// dilate_window's bounds (change.cpp:45-61). With a fused pool, the band's
+// words go to shared memory and the pool's rows inside the band (ORs of row
+// pairs and bit pairs) are emitted after one barrier.
+__global__ void __launch_bounds__(512) dilate_compact_kernel(DilateCompactArgs a) {
+  extern __shared__ __align__(16) uint32_t s_out[];  // [rows][nwo], fused pool only
+  const int s = blockIdx.y, band = blockIdx.x;
   const int nwi = (a.Win + 31) >> 5, nwo = (a.Wout + 31) >> 5;
-  const int in_lo = max(0, r0 * a.stride - a.pad);
-  const int in_hi = min(a.Hin, (r1 - 1) * a.stride - a.pad + a.kh);
-  const int nin = max(0, in_hi - in_lo);
-  uint32_t* s_h = smw + nin * nwi;      // [nin][nwo]
-  uint32_t* s_out = s_h + nin * nwo;    // [nrows][nwo]
-  // identity window (1x1, stride 1, same size: joins, 1x1 convs): the staged
-  // rows are the output rows, no dilation phases
+  const bool boot = a.boot[s] != 0;
+  const int r0 = band * a.rows;
+  const int r1 = min(r0 + a.rows, a.Hout);
+  const int nout = (r1 - r0) * nwo;
+  // identity window (1x1, stride 1, same size: joins, 1x1 convs): OR of the input words
   const bool ident = a.kh == 1 && a.kw == 1 && a.stride == 1 && a.pad == 0 && a.Hin == a.Hout && a.Win == a.Wout;
-  uint32_t* s_in = ident ? s_out : smw;  // [nin][nwi]
-  const int nout = nrows * nwo;
-
-  if (boot) {
-    for (int i = threadIdx.x; i < nout; i += blockDim.x) {
-      const int wo = i % nwo;
-      const int valid = min(32, a.Wout - wo * 32);
-      s_out[i] = valid >= 32 ? 0xffffffffu : ((1u << valid) - 1u);
-    }
-  } else {
-    // 1. stage input rows as bits: one thread per 32-pixel word
-    for (int i = threadIdx.x; i < nin * nwi; i += blockDim.x) {
-      const int r = i / nwi, w = i - r * nwi;
-      const long long rowoff = static_cast<long long>(s) * HWin + static_cast<long long>(in_lo + r) * a.Win;
-      const int c0 = w * 32, n = min(32, a.Win - c0);
-      uint32_t word = 0;
-      for (int q = 0; q < a.n_in; ++q) {
-        const uint8_t* src = a.in_map[q] + rowoff + c0;
-        if (n == 32) {
-          // 9 aligned 32-bit loads cover the 32 bytes at any alignment (map
-          // buffers carry 16 B of slack); funnel shifts realign them, and a
-          // byte-exact zero test of (bytes ^ epoch) gives 4 flags per word
-          const uintptr_t ad = reinterpret_cast<uintptr_t>(src);
-          const uint32_t* base = reinterpret_cast<const uint32_t*>(ad & ~uintptr_t(3));
-          const uint32_t sh = 8u * static_cast<uint32_t>(ad & 3);
-          uint32_t wd[9];
-#pragma unroll
-          for (int k = 0; k < 9; ++k) wd[k] = __ldg(base + k);
-          const uint32_t e4 = 0x01010101u * e;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const uint32_t x = __funnelshift_r(wd[j], wd[j + 1], sh) ^ e4;
-            const uint32_t z = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);  // 0x80 where byte == 0
-            word |= (((z >> 7) * 0x10204080u) >> 28) << (4 * j);
-          }
-        } else {
-          uint8_t v[32];
-#pragma unroll
-          for (int b = 0; b < 32; ++b) v[b] = b < n ? src[b] : 0;
-#pragma unroll
-          for (int b = 0; b < 32; ++b) word |= static_cast<uint32_t>(v[b] == e) << b;
-        }
-      }
-      s_in[i] = word;
-    }
-    if (!ident) {
-    __syncthreads();
-  DCT(1);
-    // 2. horizontal dilation (+ stride subsampling) per staged row
-    for (int i = threadIdx.x; i < nin * nwo; i += blockDim.x) {
-      const int r = i / nwo, wo = i - r * nwo;
-      const uint32_t* row = s_in + r * nwi;
-      uint32_t v = 0;
-      if (a.stride <= 2 && a.kw <= 33) {
-        // the window's source bits lie in 3 (stride 1) or 4 (stride 2)
-        // consecutive words: read them once, then funnel shifts in registers
-        const int B0 = wo * 32 * a.stride - a.pad, w0 = B0 >> 5, o0 = B0 & 31;
-        uint32_t x[4];
-#pragma unroll
-        for (int k = 0; k < 4; ++k) x[k] = (w0 + k >= 0 && w0 + k < nwi && (k < 3 || a.stride == 2)) ? row[w0 + k] : 0u;
-        auto win = [&](int b) -> uint32_t {  // 32 bits from bit b of x[0..3]
-          return b < 32 ? __funnelshift_r(x[0], x[1], b)
-                        : (b < 64 ? __funnelshift_r(x[1], x[2], b - 32) : __funnelshift_r(x[2], x[3], b - 64));
-        };
-        if (a.stride == 1) {
-          for (int ki = 0; ki < a.kw; ++ki) v |= win(o0 + ki);
-        } else {
-          uint32_t lo = 0, hi = 0;
-          for (int ki = 0; ki < a.kw; ++ki) {
-            lo |= win(o0 + ki);
-            hi |= win(o0 + 32 + ki);
-          }
-          v = even_bits(lo, hi);
-        }
-      } else if (a.stride == 1) {
-        for (int ki = 0; ki < a.kw; ++ki) v |= bits_at(row, nwi, wo * 32 - a.pad + ki);
-      } else if (a.stride == 2) {
-        uint32_t lo = 0, hi = 0;
-        const int B0 = wo * 64 - a.pad;
-        for (int ki = 0; ki < a.kw; ++ki) {
-          lo |= bits_at(row, nwi, B0 + ki);
-          hi |= bits_at(row, nwi, B0 + 32 + ki);
-        }
-        v = even_bits(lo, hi);
-      } else {
-        for (int b = 0; b < 32; ++b) {
-          const int io = wo * 32 + b;
-          bool hit = false;
-          for (int ki = 0; ki < a.kw && !hit; ++ki) {
-            const int c = io * a.stride - a.pad + ki;
-            hit = c >= 0 && c < a.Win && ((row[c >> 5] >> (c & 31)) & 1u);
-          }
-          v |= static_cast<uint32_t>(hit) << b;
-        }
-      }
-      const int valid = a.Wout - wo * 32;  // clear bits past the row end
-      if (valid < 32) v &= (1u << max(valid, 0)) - 1u;
-      s_h[i] = v;
-    }
-    __syncthreads();
-  DCT(2);
-    // 3. vertical dilation
-    for (int i = threadIdx.x; i < nout; i += blockDim.x) {
+  const long long in_off = static_cast<long long>(s) * a.Hin * nwi;
+  const uint32_t* in_s = a.in_map[0] + in_off;
+  const long long HWo = static_cast<long long>(a.Hout) * a.Wout;
+  uint32_t* gmap = a.out_map + (static_cast<long long>(s) * a.Hout + r0) * nwo;
+  for (int i0 = 0; i0 < nout; i0 += blockDim.x) {  // block-uniform
+    const int i = i0 + threadIdx.x;
+    const bool mine = i < nout;
+    uint32_t v = 0;
+    if (mine) {
       const int rr = i / nwo, wo = i - rr * nwo;
-      const int jo = r0 + rr;
-      const int ja = max(jo * a.stride - a.pad, 0), jb = min(jo * a.stride - a.pad + a.kh, a.Hin);
-      uint32_t v = 0;
-      for (int jj = ja; jj < jb; ++jj) v |= s_h[(jj - in_lo) * nwo + wo];
-      s_out[i] = v;
+      if (boot) {
+        v = row_mask(a.Wout, wo);
+      } else if (ident) {
+        const long long off = in_off + static_cast<long long>(r0 + rr) * nwi + wo;
+        for (int q = 0; q < a.n_in; ++q) v |= __ldg(a.in_map[q] + off);
+      } else {
+        const int jo = r0 + rr;
+        const int ja = max(jo * a.stride - a.pad, 0), jb = min(jo * a.stride - a.pad + a.kh, a.Hin);
+        if (a.stride <= 2 && a.kw <= 33) {
+          // the window's source bits lie in 3 (stride 1) or 4 (stride 2) consecutive words
+          const int B0 = wo * 32 * a.stride - a.pad, w0 = B0 >> 5, o0 = B0 & 31;
+          uint32_t x[4] = {0u, 0u, 0u, 0u};
+          bool ok[4];
+#pragma unroll
+          for (int k = 0; k < 4; ++k) ok[k] = w0 + k >= 0 && w0 + k < nwi && (k < 3 || a.stride == 2);
+          for (int jj = ja; jj < jb; ++jj) {
+            const uint32_t* row = in_s + static_cast<long long>(jj) * nwi + w0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+              if (ok[k]) x[k] |= __ldg(row + k);
+          }
+          auto win = [&](int b) -> uint32_t {  // 32 bits from bit b of x[0..3]
+            return b < 32 ? __funnelshift_r(x[0], x[1], b)
+                          : (b < 64 ? __funnelshift_r(x[1], x[2], b - 32) : __funnelshift_r(x[2], x[3], b - 64));
+          };
+          if (a.stride == 1) {
+            for (int ki = 0; ki < a.kw; ++ki) v |= win(o0 + ki);
+          } else {
+            uint32_t lo = 0, hi = 0;
+            for (int ki = 0; ki < a.kw; ++ki) {
+              lo |= win(o0 + ki);
+              hi |= win(o0 + 32 + ki);
+            }
+            v = even_bits(lo, hi);
+          }
+        } else {
+          for (int jj = ja; jj < jb; ++jj) {
+            const uint32_t* row = in_s + static_cast<long long>(jj) * nwi;
+            if (a.stride == 1) {
+              for (int ki = 0; ki < a.kw; ++ki) v |= bits_at(row, nwi, wo * 32 - a.pad + ki);
+            } else if (a.stride == 2) {
+              uint32_t lo = 0, hi = 0;
+              const int B0 = wo * 64 - a.pad;
+              for (int ki = 0; ki < a.kw; ++ki) {
+                lo |= bits_at(row, nwi, B0 + ki);
+                hi |= bits_at(row, nwi, B0 + 32 + ki);
+              }
+              v |= even_bits(lo, hi);
+            } else {
+              for (int b = 0; b < 32; ++b) {
+                const int io = wo * 32 + b;
+                bool hit = false;
+                for (int ki = 0; ki < a.kw && !hit; ++ki) {
+                  const int c = io * a.stride - a.pad + ki;
+                  hit = c >= 0 && c < a.Win && ((__ldg(row + (c >> 5)) >> (c & 31)) & 1u);
+                }
+                v |= static_cast<uint32_t>(hit) << b;
+              }
+            }
+          }
+        }
+        v &= row_mask(a.Wout, wo);
+      }
+      if (a.pool_map) s_out[i] = v;
     }
-    }  // !ident
+    emit_words(v, mine, i, r0, nwo, a.Wout, gmap, a.idx + s * HWo, a.count + s * a.cnt_stride);
   }
+  if (a.pool_map == nullptr) return;
   __syncthreads();
-  DCT(3);
-
-  // 4. count (contiguous run of words per thread) + block scan
-  const int per = (nout + blockDim.x - 1) / blockDim.x;
-  const int w0 = min(static_cast<int>(threadIdx.x) * per, nout), w1 = min(w0 + per, nout);
-  int mine = 0;
-  for (int i = w0; i < w1; ++i) mine += __popc(s_out[i]);
-  int agg = 0;
-  const int off = block_exclusive_scan(mine, s_warp, agg);
-  DCT(4);
-
-  // 5. the tile's place in the list: one atomicAdd per tile. Tiles land in
-  //    completion order, each one a row-major run (readers that expose the
-  //    list sort it, Net::read_changes); no tile waits for its predecessors.
-  int32_t* ctr = a.tile_ctr + 2 * s;
-  if (threadIdx.x == 0) s_prefix = agg ? atomicAdd(ctr, agg) : 0;
-  __syncthreads();
-  DCT(5);
-
-  // 6. scatter the tile's row-major run of the index list and tag the output map
-  int pos = s_prefix + off;
-  int32_t* idx = a.idx + s * HWout;
-  uint8_t* om = a.out_map + s * HWout;
-  for (int i = w0; i < w1; ++i) {
-    uint32_t bits = s_out[i];
-    const int rr = i / nwo, wo = i - rr * nwo;
-    const int base = (r0 + rr) * a.Wout + wo * 32;
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      idx[pos++] = base + b;
-      om[base + b] = e;
+  // fused 2x2 / stride-2 pool: pooled row pr covers band rows 2pr, 2pr+1 (the
+  // second clipped at Hout), pooled bit j covers bits 2j, 2j+1
+  const int nwp = (a.Wp + 31) >> 5;
+  const int pr0 = r0 >> 1, pr1 = min((r1 + 1) >> 1, a.Hp);
+  const int np = max(0, pr1 - pr0) * nwp;
+  const int nrows = r1 - r0;
+  uint32_t* pmap = a.pool_map + (static_cast<long long>(s) * a.Hp + pr0) * nwp;
+  int32_t* plist = a.pool_idx + static_cast<long long>(s) * a.Hp * a.Wp;
+  for (int i0 = 0; i0 < np; i0 += blockDim.x) {
+    const int i = i0 + threadIdx.x;
+    const bool mine = i < np;
+    uint32_t v = 0;
+    if (mine) {
+      const int pr = i / nwp, pw = i - pr * nwp;
+      const int ra = 2 * (pr0 + pr) - r0, rb = ra + 1;
+      auto word = [&](int r, int w) { return (r < nrows && w < nwo) ? s_out[r * nwo + w] : 0u; };
+      const uint32_t lo = word(ra, 2 * pw) | word(rb, 2 * pw);
+      const uint32_t hi = word(ra, 2 * pw + 1) | word(rb, 2 * pw + 1);
+      v = even_bits(lo | (lo >> 1), hi | (hi >> 1)) & row_mask(a.Wp, pw);
     }
+    emit_words(v, mine, i, pr0, nwp, a.Wp, pmap, plist, a.pool_count + s * a.cnt_stride);
   }
-  // the last tile of the stream publishes the count (consumers are later kernels)
-  if (threadIdx.x == 0) {
-    __threadfence();
-    if (atomicAdd(ctr + 1, 1) == a.n_tiles - 1) a.count[s] = atomicAdd(ctr, 0);
-  }
-  DCT(6);
-  DCT_PRINT;
 }
 
 // ---------------------------------------------------------------------------
@@ -846,7 +864,7 @@ __device__ __forceinline__ float ref_max(float m, float v) { return (m < v) ? v 
 
 __global__ void __launch_bounds__(kFrameThreads) pool_kernel(PoolArgs a, int glog) {
   const int s = blockIdx.y;
-  const long long n = a.count[s];
+  const long long n = a.count[s * a.cnt_stride];
   const long long HWi = static_cast<long long>(a.Hin) * a.Win;
   const long long HWo = static_cast<long long>(a.Hout) * a.Wout;
   const float* x = a.x + s * HWi * a.Cs;
@@ -901,7 +919,7 @@ __global__ void __launch_bounds__(kFrameThreads) pool_kernel(PoolArgs a, int glo
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) join_kernel(JoinArgs a) {
   const int s = blockIdx.y;
-  const long long n = a.count[s];
+  const long long n = a.count[s * a.cnt_stride];
   const int32_t* list = a.idx + static_cast<long long>(s) * a.HW;
   const long long total = n * a.Cs_out;
   float vmax = 0.0f;
@@ -931,17 +949,23 @@ __global__ void __launch_bounds__(kThreads) join_kernel(JoinArgs a) {
 }
 
 __global__ void begin_frame_kernel(BeginFrameArgs a) {
-  const bool dense = a.dense != nullptr && *a.dense != 0;
-  for (int s = threadIdx.x; s < a.S; s += blockDim.x) {
-    a.boot_now[s] = static_cast<uint8_t>(a.boot_req[s] != 0 || dense);
-    a.boot_req[s] = 0;
+  if (blockIdx.x == 0) {
+    const bool dense = a.dense != nullptr && *a.dense != 0;
+    for (int s = threadIdx.x; s < a.S; s += blockDim.x) {
+      a.boot_now[s] = static_cast<uint8_t>(a.boot_req[s] != 0 || dense);
+      a.boot_req[s] = 0;
+    }
+    for (int i = threadIdx.x; i < a.n_nodes; i += blockDim.x) {
+      a.rescan_now[i] = a.rescan_req[i];
+      a.rescan_req[i] = 0;
+    }
+    for (int i = threadIdx.x; i < a.n_counts; i += blockDim.x)
+      if (i % a.cnt_stride >= a.keep) a.counts[i] = 0;
+    if (threadIdx.x == 0) *a.frame += 1u;
   }
-  for (int i = threadIdx.x; i < a.n_nodes; i += blockDim.x) {
-    a.rescan_now[i] = a.rescan_req[i];
-    a.rescan_req[i] = 0;
-  }
-  for (int i = threadIdx.x; i < a.n_dc_ctr; i += blockDim.x) a.dc_ctr[i] = 0;
-  if (threadIdx.x == 0) *a.frame += 1u;
+  for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n_clear;
+       i += static_cast<long long>(gridDim.x) * blockDim.x)
+    a.clear[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
 __global__ void nhwc_to_chw_kernel(const float* src, float* dst, int C, int Cs, long long HW) {
@@ -969,13 +993,20 @@ int group_log2(int Cs) {
 
 }  // namespace
 
+// The first detect merges map words in registers (no atomics) when it runs one
+// of the 4-pixel kernels on rows of whole words: the same condition for both ingests.
+bool detect_frame_plain_map(int C, int Cs, int W, int state_chw) {
+  return W % 32 == 0 && (state_chw ? C <= 4 : Cs == 4);
+}
+
 void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
   const long long HW = static_cast<long long>(a.H) * a.W;
   if (a.x8_slot) {
     if (HW % 4 == 0 && (a.state_chw || a.Cs == 4)) {
       dim3 grid(2 * blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
       if (a.state_chw && a.C == 3 && a.use_state8 && a.state8)
-        detect_frame_s8_kernel<2><<<grid, kFrameThreads, 0, st>>>(a);
+        a.map_plain ? detect_frame_s8_kernel<2, true><<<grid, kFrameThreads, 0, st>>>(a)
+                    : detect_frame_s8_kernel<2, false><<<grid, kFrameThreads, 0, st>>>(a);
       else if (a.state_chw && a.C == 3) detect_frame_u8_kernel<true, 3><<<grid, kFrameThreads, 0, st>>>(a);
       else if (a.state_chw) detect_frame_u8_kernel<true, 0><<<grid, kFrameThreads, 0, st>>>(a);
       else detect_frame_u8_kernel<false, 0><<<grid, kFrameThreads, 0, st>>>(a);
@@ -1013,15 +1044,22 @@ void launch_detect_list(const DetectListArgs& a, cudaStream_t st) {
   else detect_list_kernel<4><<<grid, kFrameThreads, 0, st>>>(a, glog);
 }
 
-int dilate_compact_smem(int Win, int Wout, int rows_per_tile, int kh, int stride) {
-  const int nin = (rows_per_tile - 1) * stride + kh;
-  const int nwi = (Win + 31) / 32, nwo = (Wout + 31) / 32;
-  return 4 * (nin * nwi + nin * nwo + rows_per_tile * nwo);
+bool dilate_compact_tiling(int Hin, int Win, int Hout, int Wout, int kh, int stride, int Wp, int* rows, int* bands,
+                           int* threads, int* smem_bytes) {
+  (void)Hin, (void)Win, (void)kh, (void)stride;
+  const int nwo = (Wout + 31) / 32;
+  // ~256 output words (threads) per band, an even number of rows (a fused pool's rows stay inside a band)
+  int r = std::max(2, std::min(64, 256 / std::max(1, nwo))) & ~1;
+  r = std::min(r, Hout + (Hout & 1));
+  *rows = r;
+  *bands = (Hout + r - 1) / r;
+  *threads = std::min(512, ((r * nwo + 31) / 32) * 32);
+  *smem_bytes = Wp > 0 ? r * nwo * 4 : 0;
+  return *smem_bytes <= 48 * 1024;
 }
 
 void launch_dilate_compact(const DilateCompactArgs& a, cudaStream_t st) {
-  dim3 grid(a.n_tiles, a.S);
-  dilate_compact_kernel<<<grid, kThreads, a.smem_bytes, st>>>(a);
+  dilate_compact_kernel<<<dim3(a.n_bands, a.S), a.threads, a.pool_map ? a.smem_bytes : 0, st>>>(a);
 }
 
 void launch_pool(const PoolArgs& a, cudaStream_t st) {
@@ -1037,7 +1075,8 @@ void launch_join(const JoinArgs& a, cudaStream_t st) {
 }
 
 void launch_begin_frame(const BeginFrameArgs& a, cudaStream_t st) {
-  begin_frame_kernel<<<1, 256, 0, st>>>(a);
+  const long long g = std::min<long long>(2 * sm_count(), (a.n_clear + 255) / 256);
+  begin_frame_kernel<<<static_cast<int>(std::max<long long>(1, g)), 256, 0, st>>>(a);
 }
 
 void launch_nhwc_to_chw(const float* src, float* dst, int C, int Cs, int HW, cudaStream_t st) {

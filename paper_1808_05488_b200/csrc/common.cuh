@@ -14,11 +14,21 @@
 
 namespace cbg {
 
-// ---- epochs ------------------------------------------------------------------
-// Change maps hold a per-frame tag instead of 0/1 so they never need clearing:
-// a pixel is marked in the current frame iff map[p] == epoch8(frame). The host
-// clears every map once per 255 frames (runtime.cpp, Net::forward).
-CBG_DEV uint8_t epoch8(uint32_t frame) { return static_cast<uint8_t>((frame - 1u) % 255u + 1u); }
+// ---- change bitmaps --------------------------------------------------------------
+// A change map is [H][nw] 32-bit words per stream, nw = ceil(W/32): pixel
+// (row, col) is bit (col & 31) of word row*nw + (col >> 5); bits past W are 0.
+CBG_DEV int map_words(int W) { return (W + 31) >> 5; }
+// OR one pixel's bit into a map (maps written this way are cleared by begin_frame)
+CBG_DEV void map_set(uint32_t* m, long long p, int W) {
+  const uint32_t pi = static_cast<uint32_t>(p), w = static_cast<uint32_t>(W);  // p < H*W < 2^31
+  const uint32_t row = pi / w, col = pi - row * w;
+  atomicOr(m + row * static_cast<uint32_t>(map_words(W)) + (col >> 5), 1u << (col & 31));
+}
+// Warp sum of v, one atomicAdd per warp (nullable dst). Every lane must call it.
+CBG_DEV void warp_count(int32_t* dst, int v) {
+  v = __reduce_add_sync(0xffffffffu, v);
+  if ((threadIdx.x & 31) == 0 && dst != nullptr && v) atomicAdd(dst, v);
+}
 
 // ---- running magnitude bounds (fp16 GEMM operand scales) -----------------------
 // Warp max of v >= 0, one atomicMax per warp (non-negative floats order as ints).

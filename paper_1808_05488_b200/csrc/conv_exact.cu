@@ -108,7 +108,7 @@ __global__ void __maxnreg__(88) conv_exact_kernel(ConvExactArgs a) {  // launche
     if (lane == 0) s_prefix[0] = 0;
     for (int s0 = 0; s0 < a.S; s0 += 32) {
       const int s = s0 + lane;
-      const int v = s < a.S ? (a.count[s] + kThreads * kPix - 1) / (kThreads * kPix) : 0;
+      const int v = s < a.S ? (a.count[s * a.cnt_stride] + kThreads * kPix - 1) / (kThreads * kPix) : 0;
       int inc = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -134,7 +134,7 @@ __global__ void __maxnreg__(88) conv_exact_kernel(ConvExactArgs a) {  // launche
       else hi = mid;
     }
     const int s = lo;
-    const int n = a.count[s];
+    const int n = a.count[s * a.cnt_stride];
     const int kb = (wb - s_prefix[s]) * (kThreads * kPix) + threadIdx.x;
     const float* src = a.src + static_cast<long long>(s) * a.src_sstride;
     const int32_t* list = a.idx + static_cast<long long>(s) * HWo;

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     if (lane == 0) tprefix[0] = 0;
     for (int s0 = 0; s0 < a.S; s0 += 32) {
       const int s = s0 + lane;
-      const int v = s < a.S ? ((a.count[s] + kBM - 1) / kBM) * a.n_tiles : 0;
+      const int v = s < a.S ? ((a.count[s * a.cnt_stride] + kBM - 1) / kBM) * a.n_tiles : 0;
       int inc = v;
 #pragma unroll
       for (int o = 1; o < 32; o <<= 1) {
@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int s, mt, nt;
       decode(w, s, mt, nt);
-      const int cnt = a.count[s];
+      const int cnt = a.count[s * a.cnt_stride];
       // this thread's rows of the tile -> receptive-field origins, in registers
       int jb[kFetchChunks], ib[kFetchChunks], roff[kFetchChunks];
 #pragma unroll
@@ -302,7 +302,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int s, mt, nt;
       decode(w, s, mt, nt);
-      const int cnt = a.count[s];
+      const int cnt = a.count[s * a.cnt_stride];
       const float xs = exp2i(-f16_scale_exp(__ldg(a.amax_in + s)));
       const unsigned long long xs2 = pack_f32x2(xs, xs);
       // rows (h, b) = 32*quarter + 16*h + 8*b + arow
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       int s, mt, nt;
       decode(w, s, mt, nt);
-      const int cnt = a.count[s];
+      const int cnt = a.count[s * a.cnt_stride];
       const int k = mt * kBM + quarter * 32 + lane;
       const bool valid = k < cnt;
       const int p = valid ? a.idx[s * HWout + k] : -1;

@@ -7,9 +7,16 @@
 //                           padded channels hold 0 forever.
 //   network input frame   : CHW fp32 (the reference Tensor3 layout), read only
 //                           by the first layer's fused ingest+detect kernel.
-//   change maps           : uint8 [H][W], epoch-tagged (see common.cuh).
-//   index lists           : int32 pixel ids p = row*W + col, row-major
-//                           ascending; count in a device int32 per stream.
+//   change maps           : bitmaps [H][nw] uint32, nw = ceil(W/32) words per
+//                           row; bit (col & 31) of word (row, col >> 5); bits
+//                           past W are 0 (common.cuh).
+//   index lists           : int32 pixel ids p = row*W + col, a concatenation
+//                           of row-major runs (one per compaction band); the
+//                           count is a device int32 per stream, accumulated
+//                           with atomics and zeroed by begin_frame. Counts
+//                           are [S][cnt_stride] (each stream's counters in their
+//                           own cache lines: the atomics of different streams
+//                           do not contend).
 #pragma once
 
 #include <cstdint>
@@ -22,8 +29,10 @@ namespace cbg {
 struct DetectFrameArgs {
   const float* const* x_slot;  // device slot holding the frame pointer [S][C][H][W]
   float* state;        // [S][H][W][Cs]
-  uint8_t* map;        // [S][H][W] epoch-tagged input-frame map
-  const uint32_t* frame;     // device frame counter
+  uint32_t* map;       // [S][H][nw] bitmap of the input frame's detected pixels, cleared by begin_frame
+  int map_plain;       // W % 32 == 0 (4-pixel kernels): words merged in registers, else bits OR-ed in
+  int32_t* det_count;  // detected (pre-dilation) pixels of stream s at [s * cnt_stride], atomic (nullable)
+  int cnt_stride;      // ints between consecutive streams' counters (one cache line or more each)
   const uint8_t* boot;       // [S] full-update flags for this frame
   int C, Cs, H, W, S;
   const float* tau;    // device [S] per-stream thresholds of this node (set_thresholds needs no re-capture)
@@ -40,6 +49,7 @@ struct DetectFrameArgs {
   int use_state8;
 };
 void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st);
+bool detect_frame_plain_map(int C, int Cs, int W, int state_chw);
 
 // Change detection on an NHWC input produced by a change-based node. Only the
 // producer's update set can differ from the state (exact), so
@@ -47,15 +57,17 @@ void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st);
 struct DetectListArgs {
   const float* x;            // [S][H][W][Cs]
   float* state;              // [S][H][W][Cs]
-  uint8_t* map;              // [S][H][W]
+  uint32_t* map;             // [S][H][nw] bitmap, cleared by begin_frame, bits OR-ed in
+  int32_t* det_count;        // detected pixels, [s * cnt_stride], atomic (nullable)
   const int32_t* prod_idx;   // [S][H*W]  (nullable when dense)
-  const int32_t* prod_count; // [S]
+  const int32_t* prod_count; // [s * cnt_stride]
   const uint32_t* frame;
   const uint8_t* boot;
   const uint8_t* dense;      // device flag (nullable = 0): rescan every pixel
   int Cs, H, W, S;
   const float* tau;          // device [S]
   int closed_loop;
+  int cnt_stride;
   // pre-split copy of the state for a 3xFP16 GEMM that reads it (nullable):
   // per 4 channels {hi01, hi23, lo01, lo23} fp16 pairs at the state's byte
   // offsets, split with e = f16_scale_exp(amax_in[s]) exactly as the GEMM would.
@@ -67,32 +79,47 @@ void launch_detect_list(const DetectListArgs& a, cudaStream_t st);
 
 // Window dilation (reference change.cpp:45-67, also CB pooling's map,
 // layers.cpp:163) fused with the stream compaction of the output map into the
-// index list (reference extract_indexes, change.cpp:77-84): row-major inside a
-// tile of output rows, tiles in completion order (Net::read_changes sorts).
+// index list (reference extract_indexes, change.cpp:77-84). One CTA per band
+// of `rows` output rows of one stream, one thread per output word, no block
+// barriers: each warp's run of the list (row-major) is placed with one
+// atomicAdd on the stream's count.
 // Up to 4 input maps are OR-ed first (join nodes, network.cpp:366-373).
+// Optionally the map and list of a 2x2 / stride-2 max-pool reading this
+// node's output map are derived in the same pass (bands are even-aligned, so
+// every pooled row lies inside one band).
 struct DilateCompactArgs {
-  const uint8_t* in_map[4];  // [S][Hin][Win] epoch-tagged
+  const uint32_t* in_map[4];  // [S][Hin][nwi] bitmaps
   int n_in;
-  uint8_t* out_map;          // [S][Hout][Wout] epoch-tagged
-  int32_t* idx;              // [S][Hout*Wout]
-  int32_t* count;            // [S]
-  int32_t* tile_ctr;         // [S][2] (list offset, tiles done), zeroed by begin_frame
-  const uint32_t* frame;
+  uint32_t* out_map;          // [S][Hout][nwo] bitmap (every word written)
+  int32_t* idx;               // [S][Hout*Wout]
+  int32_t* count;             // list length of stream s at [s * cnt_stride], atomic, zeroed by begin_frame
+  int cnt_stride;
   const uint8_t* boot;
   int Hin, Win, Hout, Wout, kh, kw, stride, pad;
-  int rows_per_tile, n_tiles, S;
-  int smem_bytes;
+  int rows;                   // output rows per band (even): one CTA
+  int n_bands;                // bands per stream
+  int S;
+  int threads;                // per CTA (one per output word of the band, <= 512)
+  int smem_bytes;             // fused pool: the band's words
+  uint32_t* pool_map;         // fused pool (nullable): [S][Hp][nwp]
+  int32_t* pool_idx;          // [S][Hp*Wp]
+  int32_t* pool_count;        // [s * cnt_stride]
+  int Hp, Wp;
 };
 void launch_dilate_compact(const DilateCompactArgs& a, cudaStream_t st);
-int dilate_compact_smem(int Win, int Wout, int rows_per_tile, int kh, int stride);
+// band geometry: rows per band, bands, threads per CTA, shared memory of a
+// fused pool (false: the band does not fit in shared memory)
+bool dilate_compact_tiling(int Hin, int Win, int Hout, int Wout, int kh, int stride, int Wp, int* rows, int* bands,
+                           int* threads, int* smem_bytes);
 
 // Change-based max pooling at the pool's index list (reference layers.cpp:148-179).
 struct PoolArgs {
   const float* x;        // [S][Hin][Win][Cs]
   float* out;            // [S][Hout][Wout][Cs]
   const int32_t* idx;    // [S][Hout*Wout]
-  const int32_t* count;  // [S]
+  const int32_t* count;  // [s * cnt_stride]
   int Cs, Hin, Win, Hout, Wout, size, stride, S;
+  int cnt_stride;
 };
 void launch_pool(const PoolArgs& a, cudaStream_t st);
 
@@ -106,8 +133,9 @@ struct JoinArgs {
   float* out;            // [S][H][W][Cs_out]
   int Cs_out;
   const int32_t* idx;
-  const int32_t* count;
+  const int32_t* count;  // [s * cnt_stride]
   int HW, S;
+  int cnt_stride;
   float* amax_out;       // [S] running max |written value|
 };
 void launch_join(const JoinArgs& a, cudaStream_t st);
@@ -119,7 +147,8 @@ struct ConvGemmArgs {
   int src_presplit;        // src is the detect's pre-split copy (DetectListArgs::split), not fp32
   float* out;              // [S][Hout][Wout][Co4]
   const int32_t* idx;      // [S][Hout*Wout]
-  const int32_t* count;    // [S]
+  const int32_t* count;    // [s * cnt_stride]
+  int cnt_stride;
   const uint8_t* wimg;     // pre-swizzled tf32 hi/lo weight images [n_tiles][KB][2][NPAD][128B]
   const uint32_t* ktab;    // [KB*8][2] per 16-B chunk: (kj | ki<<8 | c0<<16 | invalid<<31, (kj*Win + ki)*Cs + c0)
   const float* bias;       // [n_tiles*NPAD]
@@ -150,7 +179,8 @@ struct ConvExactArgs {
   int pstride;
   float* out;              // [S][Hout][Wout][Co4]
   const int32_t* idx;      // [S][Hout*Wout]
-  const int32_t* count;    // [S]
+  const int32_t* count;    // [s * cnt_stride]
+  int cnt_stride;
   const float* w;          // [Cout][Cin*kh*kw] (reference weights layout, tensor.hpp:47)
   const float* bias;       // [Cout]
   int Cin, Cout, Co4, kh, kw, stride, pad;
@@ -174,8 +204,10 @@ struct BeginFrameArgs {
   const uint8_t* dense;  // device flag: every frame is a full update
   uint8_t* rescan_now;   // [n_nodes] out: dense re-detection after a tau change
   uint8_t* rescan_req;   // [n_nodes] in, cleared
-  int32_t* dc_ctr;       // compaction counters of every node, zeroed
-  int n_dc_ctr;
+  int32_t* counts;       // per-frame atomic counters [S][cnt_stride] (list lengths, detected pixels):
+  int n_counts, cnt_stride, keep;  // entries [s][0, keep) (uploaded by the host) stay, the rest are zeroed
+  uint4* clear;          // bitmaps written by OR (sparse detections), zeroed
+  long long n_clear;     // 16-B units
   int S, n_nodes;
 };
 void launch_begin_frame(const BeginFrameArgs& a, cudaStream_t st);

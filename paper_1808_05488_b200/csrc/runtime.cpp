@@ -446,20 +446,20 @@ int exact_max_cout() {
   return e ? std::atoi(e) : 16;
 }
 
-void dc_tiling(int Hin, int Win, int Hout, int Wout, int kh, int stride, int S, int* rows, int* tiles,
-               int* smem) {
+// Compaction geometry of a node (kernels.hpp dilate_compact_tiling); Wp > 0: a fused pool's width.
+DilateCompactArgs dc_geometry(int Hin, int Win, int Hout, int Wout, int kh, int kw, int stride, int pad, int S,
+                              int Wp = 0) {
   if (Wout > 65536 || Win > 65536) throw Error(CBG_ERR_UNSUPPORTED, "map width > 65536 not supported");
-  // ~16K output pixels per tile (<= 64 bit-words per thread of a 256-thread
-  // block), but enough tiles to spread the stream set over the SMs
-  int r = std::max(1, std::min(Hout, 16384 / std::max(1, Wout)));
-  while (r > 1 && static_cast<long long>((Hout + r - 1) / r) * S < 148) r = (r + 1) / 2;
-  while (r > 1 && dilate_compact_smem(Win, Wout, r, kh, stride) > 48 * 1024) --r;
-  *rows = r;
-  *tiles = (Hout + r - 1) / r;
-  *smem = dilate_compact_smem(Win, Wout, r, kh, stride);
-  (void)Hin;
-  if (*smem > 48 * 1024) throw Error(CBG_ERR_UNSUPPORTED, "compaction tile exceeds 48 KB of shared memory");
+  DilateCompactArgs g{};
+  if (!dilate_compact_tiling(Hin, Win, Hout, Wout, kh, stride, Wp, &g.rows, &g.n_bands, &g.threads, &g.smem_bytes))
+    throw Error(CBG_ERR_UNSUPPORTED, "compaction band exceeds 48 KB of shared memory");
+  g.Hin = Hin, g.Win = Win, g.Hout = Hout, g.Wout = Wout;
+  g.kh = kh, g.kw = kw, g.stride = stride, g.pad = pad;
+  g.S = S;
+  g.n_in = 1;
+  return g;
 }
+size_t map_words_of(int H, int W) { return static_cast<size_t>(H) * ((W + 31) / 32); }
 }  // namespace
 
 Net::Net(Ctx* ctx, Topology topo, int n_streams) : ctx_(ctx), topo_(std::move(topo)), S_(n_streams) {
@@ -524,6 +524,13 @@ void Net::build() {
   const int n = static_cast<int>(topo_.nodes.size());
   nodes_.resize(n);
   n_slots_ = 0;
+  // count slots: external nodes' (uploaded by set_external) first, then the
+  // per-frame atomic counters begin_frame zeroes
+  for (int i = 0; i < n; ++i)
+    if (topo_.nodes[i].kind == kExternal) nodes_[i].count_slot = n_slots_++;
+  n_ext_slots_ = n_slots_;
+  size_t clear_words = 0;  // arena of OR-written bitmaps
+  std::vector<std::pair<int, size_t>> clear_off;
   for (int i = 0; i < n; ++i) {
     NodeRT& r = nodes_[i];
     r.d = topo_.nodes[i];
@@ -540,11 +547,11 @@ void Net::build() {
       r.idx = prod.idx;
       r.count_slot = prod.count_slot;
     } else {
-      r.outmap_own.alloc(static_cast<size_t>(S_) * HWo + 16);  // +16: dilate_compact's aligned word loads
+      r.outmap_own.alloc(static_cast<size_t>(S_) * map_words_of(d.H, d.W) * 4);
       r.idx_own.alloc(static_cast<size_t>(S_) * HWo * sizeof(int32_t));
-      r.outmap = r.outmap_own.as<uint8_t>();
+      r.outmap = r.outmap_own.as<uint32_t>();
       r.idx = r.idx_own.as<int32_t>();
-      r.count_slot = n_slots_++;
+      if (d.kind != kExternal) r.count_slot = n_slots_++;
     }
     if (d.kind == kExternal) continue;
     if (d.kind == CBG_LAYER_CONV) {
@@ -585,7 +592,11 @@ void Net::build() {
         r.state_chw = r.exact && d.inputs[0] < 0;
         r.state.alloc(static_cast<size_t>(S_) * HWi * (r.state_chw ? d.Ci : r.Csi) * sizeof(float));
         if (r.state_chw && d.Ci == 3 && HWi % 4 == 0) r.state8.alloc(static_cast<size_t>(S_) * HWi * 3 + 16);
-        r.inmap.alloc(static_cast<size_t>(S_) * HWi + 16);
+        r.det_slot = n_slots_++;
+        r.inmap_words = static_cast<size_t>(S_) * map_words_of(d.Hi, d.Wi);
+        r.inmap_plain = d.inputs[0] < 0 && detect_frame_plain_map(d.Ci, r.Csi, d.Wi, r.state_chw ? 1 : 0);
+        clear_off.push_back({i, clear_words});
+        clear_words += (r.inmap_words + 3) & ~static_cast<size_t>(3);  // 16-B aligned
         // the direct 3xFP16 GEMM of a k x k layer (k > 1) gathers every input value
         // k^2 times: its detect keeps the state pre-split, once per changed pixel
         const char* ps_env = std::getenv("CBG_PRESPLIT");  // read per build: A/B in one process
@@ -598,22 +609,38 @@ void Net::build() {
           CK(cudaStreamSynchronize(nullptr));
         }
       }
-      if (!reuse) {
-        if (d.policy == CBG_POLICY_DETECT || d.policy == CBG_POLICY_PROPAGATE)
-          dc_tiling(d.Hi, d.Wi, d.H, d.W, c.kernel_h, c.stride, S_, &r.dc_rows, &r.dc_tiles, &r.dc_smem);
-      }
+      if (!reuse && (d.policy == CBG_POLICY_DETECT || d.policy == CBG_POLICY_PROPAGATE))
+        r.dc = dc_geometry(d.Hi, d.Wi, d.H, d.W, c.kernel_h, c.kernel_w, c.stride, c.padding, S_);
       // worst-case map buffers (record_worst_case, layers.cpp:108-117)
       if (d.inputs[0] >= 0) {
-        dc_tiling(d.Hi, d.Wi, d.H, d.W, c.kernel_h, c.stride, S_, &r.dc_wc_rows, &r.dc_wc_tiles, &r.dc_wc_smem);
-        r.wc_map.alloc(static_cast<size_t>(S_) * HWo + 16);
+        r.dc_wc = dc_geometry(d.Hi, d.Wi, d.H, d.W, c.kernel_h, c.kernel_w, c.stride, c.padding, S_);
+        r.wc_map.alloc(static_cast<size_t>(S_) * map_words_of(d.H, d.W) * 4);
         r.wc_idx.alloc(static_cast<size_t>(S_) * HWo * sizeof(int32_t));
       }
       r.wc_slot = n_slots_++;
     } else if (d.kind == CBG_LAYER_POOL) {
-      dc_tiling(d.Hi, d.Wi, d.H, d.W, d.pool_size, d.pool_stride, S_, &r.dc_rows, &r.dc_tiles, &r.dc_smem);
+      // a 2x2 / stride-2 pool over a node that runs its own compaction gets its
+      // map and list from that compaction (one launch fewer, no map re-read)
+      NodeRT& p = nodes_[d.inputs[0]];
+      const bool host = p.d.kind != kExternal && p.dc.n_bands > 0 && p.pool_child < 0 && p.fused_into < 0 &&
+                        !(p.d.kind == CBG_LAYER_CONV && p.d.policy == CBG_POLICY_REUSE1X1);
+      const char* fe = std::getenv("CBG_FUSE_POOL");
+      if (host && d.pool_size == 2 && d.pool_stride == 2 && !(fe && std::atoi(fe) == 0)) {
+        DilateCompactArgs g = p.dc;
+        DilateCompactArgs f = dc_geometry(g.Hin, g.Win, g.Hout, g.Wout, g.kh, g.kw, g.stride, g.pad, S_, d.W);
+        p.dc = f;
+        p.pool_child = i;
+        r.fused_into = d.inputs[0];
+      } else {
+        r.dc = dc_geometry(d.Hi, d.Wi, d.H, d.W, d.pool_size, d.pool_size, d.pool_stride, 0, S_);
+      }
     } else {  // joins: OR of the parents' maps, 1x1 identity window
-      dc_tiling(d.H, d.W, d.H, d.W, 1, 1, S_, &r.dc_rows, &r.dc_tiles, &r.dc_smem);
+      r.dc = dc_geometry(d.H, d.W, d.H, d.W, 1, 1, 1, 0, S_);
     }
+  }
+  if (clear_words) {
+    clear_.alloc(clear_words * 4);
+    for (auto& [i, off] : clear_off) nodes_[i].inmap = clear_.as<uint32_t>() + off;
   }
   frame_.alloc(static_cast<size_t>(S_) * topo_.C * topo_.H * topo_.W * sizeof(float));
   frame_slot_.alloc(sizeof(void*));
@@ -627,7 +654,6 @@ void Net::build() {
   ev_map_.resize(nodes_.size());
   for (auto& e : ev_map_) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   frame_ctr_.alloc(4);
-  dc_ctr_.alloc(nodes_.size() * 2 * S_ * 2 * sizeof(int32_t));
   boot_req_.alloc(S_);
   // a network bootstraps on its first frame (network.cpp:318-321); a standalone
   // layer does not: only force_full_update makes it a full update (layers.cpp:64-71)
@@ -647,7 +673,10 @@ void Net::build() {
     for (int k = 0; k < S_; ++k) stream_taus_[static_cast<size_t>(i) * S_ + k] = nodes_[i].d.tau;
   }
   if (n) CK(cudaMemcpy(taus_.p, stream_taus_.data(), stream_taus_.size() * sizeof(float), cudaMemcpyHostToDevice));
-  counts_.alloc(static_cast<size_t>(std::max(1, n_slots_)) * S_ * sizeof(int32_t));
+  // [S][cnt_stride_]: each stream's counters in their own cache lines, so the
+  // per-warp / per-CTA atomics of different streams never share a line
+  cnt_stride_ = (std::max(1, n_slots_) + 31) / 32 * 32;
+  counts_.alloc(static_cast<size_t>(cnt_stride_) * S_ * sizeof(int32_t));
   amax_.alloc(static_cast<size_t>(n + 1) * S_ * sizeof(float));
   ext_amax_.assign(S_, 0.0f);
 }
@@ -655,17 +684,6 @@ void Net::build() {
 int Net::amax_origin(int node) const {
   while (node >= 0 && nodes_[node].d.kind == CBG_LAYER_POOL) node = nodes_[node].d.inputs[0];
   return node;  // -1 = network input
-}
-
-void Net::clear_maps() {
-  for (NodeRT& r : nodes_) {
-    // an external node's map was uploaded for this call already (set_external
-    // tags it with the coming frame's epoch): clearing it would drop it
-    if (r.d.kind == kExternal) continue;
-    if (r.inmap.bytes) CK(cudaMemsetAsync(r.inmap.p, 0, r.inmap.bytes, ctx_->stream));
-    if (r.outmap_own.bytes) CK(cudaMemsetAsync(r.outmap_own.p, 0, r.outmap_own.bytes, ctx_->stream));
-    if (r.wc_map.bytes) CK(cudaMemsetAsync(r.wc_map.p, 0, r.wc_map.bytes, ctx_->stream));
-  }
 }
 
 int Net::launch_count(unsigned flags) const {
@@ -677,7 +695,7 @@ int Net::launch_count(unsigned flags) const {
       k += (d.policy == CBG_POLICY_DETECT) + (d.policy != CBG_POLICY_REUSE1X1) + 1;
       if ((flags & CBG_FWD_RECORD_WORST_CASE) && d.inputs[0] >= 0) k += 1;
     } else {
-      k += 2;
+      k += r.fused_into >= 0 ? 1 : 2;
     }
   }
   return k;
@@ -692,13 +710,38 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
   {
     BeginFrameArgs b{frame_ctr_.as<uint32_t>(), boot_now_.as<uint8_t>(), boot_req_.as<uint8_t>(),
                      dense_flag_.as<uint8_t>(), rescan_now_.as<uint8_t>(), rescan_req_.as<uint8_t>(),
-                     dc_ctr_.as<int32_t>(), static_cast<int>(dc_ctr_.bytes / sizeof(int32_t)), S_, n};
+                     counts, cnt_stride_ * S_, cnt_stride_, n_ext_slots_,
+                     clear_.as<uint4>(), static_cast<long long>(clear_.bytes / 16), S_, n};
     timed("frame.begin", [&] { launch_begin_frame(b, st); });
   }
   // node whose compaction wrote node k's map (Reuse1x1 nodes alias their producer's)
   auto map_owner = [&](int k) {
     while (nodes_[k].d.kind == CBG_LAYER_CONV && nodes_[k].d.policy == CBG_POLICY_REUSE1X1) k = nodes_[k].d.inputs[0];
     return k;
+  };
+  // the compaction of node k (its geometry, maps and list), with its fused pool's outputs
+  auto compaction = [&](int k, const uint32_t* const* in, int n_in) {
+    const NodeRT& r = nodes_[k];
+    DilateCompactArgs dc = r.dc;
+    for (int q = 0; q < n_in; ++q) dc.in_map[q] = in[q];
+    dc.n_in = n_in;
+    dc.out_map = r.outmap;
+    dc.idx = r.idx;
+    dc.count = counts + r.count_slot;
+    dc.cnt_stride = cnt_stride_;
+    dc.boot = boot;
+    if (r.pool_child >= 0) {
+      const NodeRT& p = nodes_[r.pool_child];
+      dc.pool_map = p.outmap;
+      dc.pool_idx = p.idx;
+      dc.pool_count = counts + p.count_slot;
+      dc.Hp = p.d.H, dc.Wp = p.d.W;
+    }
+    return dc;
+  };
+  auto done_map = [&](int k, cudaStream_t on) {
+    CK(cudaEventRecord(ev_map_[k], on));
+    if (nodes_[k].pool_child >= 0) CK(cudaEventRecord(ev_map_[nodes_[k].pool_child], on));
   };
   // compaction of node k from its producers' maps: on the side stream once
   // those maps exist (their GEMMs may still run), then joined back
@@ -708,12 +751,12 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
     for (int in : dk.inputs) side = side && nodes_[map_owner(in)].d.kind != kExternal;
     if (!side) {
       timed(dk.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
-      CK(cudaEventRecord(ev_map_[k], st));
+      done_map(k, st);
       return;
     }
     for (int in : dk.inputs) CK(cudaStreamWaitEvent(side_st_, ev_map_[map_owner(in)], 0));
     timed(dk.name + ".dilcomp", [&] { launch_dilate_compact(dc, side_st_); }, side_st_);
-    CK(cudaEventRecord(ev_map_[k], side_st_));
+    done_map(k, side_st_);
     CK(cudaStreamWaitEvent(st, ev_map_[k], 0));
   };
   for (int i = 0; i < n; ++i) {
@@ -726,69 +769,56 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
       const ConvDesc& c = d.conv;
       const float* column_src = prod ? prod->out.as<float>() : nullptr;
       if (d.policy == CBG_POLICY_DETECT) {
+        int32_t* det = counts + r.det_slot;
         if (!prod) {
-          DetectFrameArgs a{frame_slot_.as<const float*>(), r.state.as<float>(), r.inmap.as<uint8_t>(), frame, boot,
-                            d.Ci, r.Csi, d.Hi, d.Wi, S_, taus_.as<float>() + static_cast<size_t>(i) * S_,
-                            topo_.mode == CBG_MODE_CLOSEDLOOP, r.state_chw, amax_entry(-1),
-                            u8 ? frame8_slot_.as<const uint8_t*>() + slot8 : nullptr,
-                            bcast ? 0LL : static_cast<long long>(d.Ci) * d.Hi * d.Wi,
-                            u8 ? r.state8.as<uint8_t>() : nullptr, (u8 && s8) ? 1 : 0};
+          DetectFrameArgs a{};
+          a.x_slot = frame_slot_.as<const float*>();
+          a.state = r.state.as<float>();
+          a.map = r.inmap;
+          a.map_plain = r.inmap_plain ? 1 : 0;
+          a.det_count = det;
+          a.cnt_stride = cnt_stride_;
+          a.boot = boot;
+          a.C = d.Ci, a.Cs = r.Csi, a.H = d.Hi, a.W = d.Wi, a.S = S_;
+          a.tau = taus_.as<float>() + static_cast<size_t>(i) * S_;
+          a.closed_loop = topo_.mode == CBG_MODE_CLOSEDLOOP;
+          a.state_chw = r.state_chw;
+          a.amax = amax_entry(-1);
+          a.x8_slot = u8 ? frame8_slot_.as<const uint8_t*>() + slot8 : nullptr;
+          a.x_sstride = bcast ? 0LL : static_cast<long long>(d.Ci) * d.Hi * d.Wi;
+          a.state8 = u8 ? r.state8.as<uint8_t>() : nullptr;
+          a.use_state8 = (u8 && s8) ? 1 : 0;
           timed(d.name + ".detect", [&] { launch_detect_frame(a, st); });
         } else {
           const bool ext = prod->d.kind == kExternal;  // standalone layer: arbitrary x, dense detect
-          DetectListArgs a{prod->out.as<float>(), r.state.as<float>(), r.inmap.as<uint8_t>(),
-                           ext ? nullptr : prod->idx, counts + prod->count_slot * S_, frame, boot,
+          DetectListArgs a{prod->out.as<float>(), r.state.as<float>(), r.inmap, det,
+                           ext ? nullptr : prod->idx, counts + prod->count_slot, frame, boot,
                            rescan_now_.as<uint8_t>() + i, r.Csi, d.Hi, d.Wi, S_,
                            taus_.as<float>() + static_cast<size_t>(i) * S_,
-                           topo_.mode == CBG_MODE_CLOSEDLOOP,
+                           topo_.mode == CBG_MODE_CLOSEDLOOP, cnt_stride_,
                            r.split.bytes ? r.split.as<uint32_t>() : nullptr, r.split_e.as<int32_t>(),
                            amax_entry(amax_origin(src))};
           timed(d.name + ".detect", [&] { launch_detect_list(a, st); });
         }
         // ClosedLoop reads the state; FeedForward's state equals x after detection.
         column_src = r.state.as<float>();
-        DilateCompactArgs dc{};
-        dc.in_map[0] = r.inmap.as<uint8_t>();
-        dc.n_in = 1;
-        dc.out_map = r.outmap;
-        dc.idx = r.idx;
-        dc.count = counts + r.count_slot * S_;
-        dc.tile_ctr = dc_ctr(i, false);
-        dc.frame = frame;
-        dc.boot = boot;
-        dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
-        dc.kh = c.kernel_h, dc.kw = c.kernel_w, dc.stride = c.stride, dc.pad = c.padding;
-        dc.rows_per_tile = r.dc_rows, dc.n_tiles = r.dc_tiles, dc.S = S_, dc.smem_bytes = r.dc_smem;
+        const uint32_t* in[1] = {r.inmap};
+        const DilateCompactArgs dc = compaction(i, in, 1);
         timed(d.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
-        CK(cudaEventRecord(ev_map_[i], st));
+        done_map(i, st);
       } else if (d.policy == CBG_POLICY_PROPAGATE) {
-        DilateCompactArgs dc{};
-        dc.in_map[0] = prod->outmap;
-        dc.n_in = 1;
-        dc.out_map = r.outmap;
-        dc.idx = r.idx;
-        dc.count = counts + r.count_slot * S_;
-        dc.tile_ctr = dc_ctr(i, false);
-        dc.frame = frame;
-        dc.boot = boot;
-        dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
-        dc.kh = c.kernel_h, dc.kw = c.kernel_w, dc.stride = c.stride, dc.pad = c.padding;
-        dc.rows_per_tile = r.dc_rows, dc.n_tiles = r.dc_tiles, dc.S = S_, dc.smem_bytes = r.dc_smem;
-        map_compaction(i, dc);
+        const uint32_t* in[1] = {prod->outmap};
+        map_compaction(i, compaction(i, in, 1));
       }
       if ((flags & CBG_FWD_RECORD_WORST_CASE) && prod) {
-        DilateCompactArgs dc{};
+        DilateCompactArgs dc = r.dc_wc;
         dc.in_map[0] = prod->outmap;
         dc.n_in = 1;
-        dc.out_map = r.wc_map.as<uint8_t>();
+        dc.out_map = r.wc_map.as<uint32_t>();
         dc.idx = r.wc_idx.as<int32_t>();
-        dc.count = counts + r.wc_slot * S_;
-        dc.tile_ctr = dc_ctr(i, true);
-        dc.frame = frame;
+        dc.count = counts + r.wc_slot;
+        dc.cnt_stride = cnt_stride_;
         dc.boot = boot;
-        dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
-        dc.kh = c.kernel_h, dc.kw = c.kernel_w, dc.stride = c.stride, dc.pad = c.padding;
-        dc.rows_per_tile = r.dc_wc_rows, dc.n_tiles = r.dc_wc_tiles, dc.S = S_, dc.smem_bytes = r.dc_wc_smem;
         timed(d.name + ".worstcase", [&] { launch_dilate_compact(dc, st); });
       }
       if (r.exact) {
@@ -805,7 +835,8 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
         }
         x.out = r.out.as<float>();
         x.idx = r.idx;
-        x.count = counts + r.count_slot * S_;
+        x.count = counts + r.count_slot;
+        x.cnt_stride = cnt_stride_;
         x.w = r.wraw.as<float>();
         x.bias = r.bias.as<float>();
         x.Cin = c.in_channels, x.Cout = c.out_channels, x.Co4 = r.Cs;
@@ -826,7 +857,8 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
       }
       g.out = r.out.as<float>();
       g.idx = r.idx;
-      g.count = counts + r.count_slot * S_;
+      g.count = counts + r.count_slot;
+      g.cnt_stride = cnt_stride_;
       g.wimg = r.wimg.as<uint8_t>();
       g.ktab = r.ktab.as<uint32_t>();
       g.bias = r.bias.as<float>();
@@ -843,36 +875,17 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
       g.amax_out = amax_entry(i);
       timed(d.name + ".gemm", [&] { launch_conv_gemm(g, st); });
     } else if (d.kind == CBG_LAYER_POOL) {
-      DilateCompactArgs dc{};
-      dc.in_map[0] = prod->outmap;
-      dc.n_in = 1;
-      dc.out_map = r.outmap;
-      dc.idx = r.idx;
-      dc.count = counts + r.count_slot * S_;
-      dc.tile_ctr = dc_ctr(i, false);
-      dc.frame = frame;
-      dc.boot = boot;
-      dc.Hin = d.Hi, dc.Win = d.Wi, dc.Hout = d.H, dc.Wout = d.W;
-      dc.kh = d.pool_size, dc.kw = d.pool_size, dc.stride = d.pool_stride, dc.pad = 0;
-      dc.rows_per_tile = r.dc_rows, dc.n_tiles = r.dc_tiles, dc.S = S_, dc.smem_bytes = r.dc_smem;
-      map_compaction(i, dc);
-      PoolArgs pa{prod->out.as<float>(), r.out.as<float>(), r.idx, counts + r.count_slot * S_, r.Cs, d.Hi, d.Wi,
-                  d.H, d.W, d.pool_size, d.pool_stride, S_};
+      if (r.fused_into < 0) {
+        const uint32_t* in[1] = {prod->outmap};
+        map_compaction(i, compaction(i, in, 1));
+      }
+      PoolArgs pa{prod->out.as<float>(), r.out.as<float>(), r.idx, counts + r.count_slot, r.Cs, d.Hi, d.Wi,
+                  d.H, d.W, d.pool_size, d.pool_stride, S_, cnt_stride_};
       timed(d.name + ".pool", [&] { launch_pool(pa, st); });
     } else {  // Add / Concat
-      DilateCompactArgs dc{};
-      for (size_t k = 0; k < d.inputs.size(); ++k) dc.in_map[k] = nodes_[d.inputs[k]].outmap;
-      dc.n_in = static_cast<int>(d.inputs.size());
-      dc.out_map = r.outmap;
-      dc.idx = r.idx;
-      dc.count = counts + r.count_slot * S_;
-      dc.tile_ctr = dc_ctr(i, false);
-      dc.frame = frame;
-      dc.boot = boot;
-      dc.Hin = d.H, dc.Win = d.W, dc.Hout = d.H, dc.Wout = d.W;
-      dc.kh = 1, dc.kw = 1, dc.stride = 1, dc.pad = 0;
-      dc.rows_per_tile = r.dc_rows, dc.n_tiles = r.dc_tiles, dc.S = S_, dc.smem_bytes = r.dc_smem;
-      map_compaction(i, dc);
+      const uint32_t* in[4] = {};
+      for (size_t k = 0; k < d.inputs.size(); ++k) in[k] = nodes_[d.inputs[k]].outmap;
+      map_compaction(i, compaction(i, in, static_cast<int>(d.inputs.size())));
       JoinArgs ja{};
       for (size_t k = 0; k < d.inputs.size(); ++k) {
         const NodeRT& p = nodes_[d.inputs[k]];
@@ -885,7 +898,8 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
       ja.out = r.out.as<float>();
       ja.Cs_out = r.Cs;
       ja.idx = r.idx;
-      ja.count = counts + r.count_slot * S_;
+      ja.count = counts + r.count_slot;
+      ja.cnt_stride = cnt_stride_;
       ja.HW = d.H * d.W;
       ja.S = S_;
       ja.amax_out = amax_entry(i);
@@ -986,7 +1000,6 @@ void Net::run_frame(unsigned flags, unsigned graph_key) {
   cudaStream_t st = ctx_->stream;
   if (flags & CBG_FWD_FORCE_FULL) CK(cudaMemsetAsync(boot_req_.p, 1, S_, st));
   ++host_frame_;
-  if (host_frame_ > 1 && (host_frame_ - 1) % 255 == 0) clear_maps();  // epoch8 wraps
   const unsigned gflags = flags & CBG_FWD_RECORD_WORST_CASE;
   const bool u8 = (graph_key >> 31) != 0;
   const bool bcast = ((graph_key >> 30) & 1u) != 0;
@@ -1034,6 +1047,10 @@ void Net::run_frame(unsigned flags, unsigned graph_key) {
 
 template <class F>
 void Net::timed(const std::string& label, F&& launch, cudaStream_t on) {
+  if (dry_) {
+    dry_labels_.push_back(label);
+    return;
+  }
   if (!timing_) {
     launch();
     return;
@@ -1050,6 +1067,21 @@ void Net::timed(const std::string& label, F&& launch, cudaStream_t on) {
   launch();
   CK(cudaEventRecord(b, on));
   pending_.push_back({label, {a, b}});
+}
+
+std::vector<std::string> Net::kernel_labels(unsigned flags) {
+  dry_ = true;
+  dry_labels_.clear();
+  try {
+    enqueue_frame(flags & CBG_FWD_RECORD_WORST_CASE);
+  } catch (...) {
+    dry_ = false;
+    throw;
+  }
+  dry_ = false;
+  CK(cudaStreamSynchronize(ctx_->stream));  // (event records / waits only)
+  CK(cudaStreamSynchronize(side_st_));
+  return std::move(dry_labels_);
 }
 
 void Net::set_timing(bool on) {
@@ -1072,7 +1104,7 @@ std::string Net::timing_report() const {
 }
 
 void Net::copy_counts_async(int32_t* host_dst) {
-  CK(cudaMemcpyAsync(host_dst, counts_.p, static_cast<size_t>(std::max(1, n_slots_)) * S_ * sizeof(int32_t),
+  CK(cudaMemcpyAsync(host_dst, counts_.p, counts_.bytes,
                      cudaMemcpyDeviceToHost, ctx_->stream));
 }
 
@@ -1124,17 +1156,17 @@ void Net::set_external(const float* x_chw, const uint8_t* map, const int32_t* ro
   // the frame of the external node is a CHW staging copy
   CK(cudaMemcpyAsync(frame_.p, x_chw, static_cast<size_t>(d.C) * HW * sizeof(float), cudaMemcpyHostToDevice, st));
   launch_chw_to_nhwc(frame_.as<float>(), e.out.as<float>(), d.C, e.Cs, static_cast<int>(HW), st);
-  // map / indexes tagged with the epoch of the coming frame
-  const uint32_t next = host_frame_ + 1;
-  const uint8_t tag = static_cast<uint8_t>((next - 1) % 255 + 1);
-  // full: a forced full update sees every upstream pixel as changed (a
-  // Reuse1x1 layer then recomputes everything, layers.cpp:64-71)
-  std::vector<uint8_t> m(HW, full ? tag : 0);
-  if (map && !full)
-    for (size_t i = 0; i < HW; ++i) m[i] = map[i] ? tag : 0;
+  // the upstream map as a bitmap (common.cuh); full: a forced full update sees
+  // every upstream pixel as changed (a Reuse1x1 layer then recomputes
+  // everything, layers.cpp:64-71)
+  const int nw = (d.W + 31) / 32;
+  std::vector<uint32_t> m(static_cast<size_t>(d.H) * nw, 0u);
+  for (int row = 0; row < d.H; ++row)
+    for (int col = 0; col < d.W; ++col)
+      if (full || (map && map[static_cast<size_t>(row) * d.W + col])) m[static_cast<size_t>(row) * nw + (col >> 5)] |= 1u << (col & 31);
   // ordered on the ctx stream after the previous frame's kernels, which may
   // still read the map, list and count (pageable sources are staged at call time)
-  CK(cudaMemcpyAsync(e.outmap, m.data(), HW, cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(e.outmap, m.data(), m.size() * 4, cudaMemcpyHostToDevice, st));
   std::vector<int32_t> idx;
   if (full) {
     idx.resize(HW);
@@ -1146,7 +1178,7 @@ void Net::set_external(const float* x_chw, const uint8_t* map, const int32_t* ro
     if (n) CK(cudaMemcpyAsync(e.idx, idx.data(), n * sizeof(int32_t), cudaMemcpyHostToDevice, st));
   }
   const int32_t cnt = static_cast<int32_t>(full ? HW : rowcol ? n : 0);
-  CK(cudaMemcpyAsync(counts_.as<int32_t>() + e.count_slot * S_, &cnt, sizeof(cnt), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(counts_.as<int32_t>() + e.count_slot, &cnt, sizeof(cnt), cudaMemcpyHostToDevice, st));
 }
 
 void Net::reset(int stream) {
@@ -1268,7 +1300,7 @@ void Net::read_state(int node, int stream, float* out_chw) {
 }
 
 void Net::read_counts(std::vector<int32_t>& counts) {
-  counts.resize(static_cast<size_t>(std::max(1, n_slots_)) * S_);
+  counts.resize(static_cast<size_t>(cnt_stride_) * S_);
   CK(cudaMemcpyAsync(counts.data(), counts_.p, counts.size() * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx_->stream));
   CK(cudaStreamSynchronize(ctx_->stream));
 }
@@ -1277,7 +1309,7 @@ int64_t Net::count_of(const std::vector<int32_t>& counts, int node, int stream, 
   const NodeRT& r = nodes_[node];
   const int slot = worst ? r.wc_slot : r.count_slot;
   if (slot < 0) return -1;
-  return counts[static_cast<size_t>(slot) * S_ + stream];
+  return counts[static_cast<size_t>(stream) * cnt_stride_ + slot];
 }
 
 void Net::read_changes(int node, int stream, uint8_t* map, int32_t* rowcol, int64_t* count, bool worst) {

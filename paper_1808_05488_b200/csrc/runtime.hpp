@@ -21,6 +21,7 @@
 #include <vector>
 
 #include "../../include/cbg.h"
+#include "kernels.hpp"
 
 namespace cbg {
 
@@ -98,20 +99,26 @@ struct NodeRT {
   bool exact = false;            // CUDA-core bit-exact path (conv_exact.cu) instead of tcgen05
   bool state_chw = false;        // first-layer exact conv: input state as CHW planes (= the frame layout)
   DevBuf wimg, ktab, bias, wraw; // wraw: [Cout][Cin*kh*kw] fp32 for the exact path
-  DevBuf state, inmap;           // Detect policy
+  DevBuf state;                  // Detect policy
+  uint32_t* inmap = nullptr;     // Detect policy: bitmap of detected input pixels [S][Hi][nw] (in Net::clear_)
+  size_t inmap_words = 0;
+  bool inmap_plain = false;      // first detect: words merged in registers (DetectFrameArgs::map_plain)
   DevBuf state8;                 // first layer, 8-bit ingest: byte shadow of the state (DetectFrameArgs::state8)
   DevBuf split, split_e;         // 3xFP16 GEMM input: pre-split copy of the state (DetectListArgs::split)
   // every node
   DevBuf out;                    // [S][H][W][Cs]
-  DevBuf outmap_own, idx_own;
-  uint8_t* outmap = nullptr;     // may alias the producer (Reuse1x1)
+  DevBuf outmap_own, idx_own;    // output bitmap [S][H][nw] and index list [S][H*W]
+  uint32_t* outmap = nullptr;    // may alias the producer (Reuse1x1)
   int32_t* idx = nullptr;
-  int count_slot = 0;            // index into Net::counts ([slot][S])
-  int dc_rows = 1, dc_tiles = 1, dc_smem = 0;
+  int count_slot = 0;            // index into Net::counts ([slot][S]): output list length
+  int det_slot = -1;             // Detect policy: detected (pre-dilation) input pixels
+  DilateCompactArgs dc{};        // geometry of this node's compaction (rows, bands, warps, smem)
+  int pool_child = -1;           // 2x2/2 pool whose map and list this node's compaction also derives
+  int fused_into = -1;           // pool: the producer whose compaction derives its map and list
   // worst-case map (record_worst_case)
   DevBuf wc_map, wc_idx;
   int wc_slot = -1;
-  int dc_wc_rows = 1, dc_wc_tiles = 1, dc_wc_smem = 0;
+  DilateCompactArgs dc_wc{};
 };
 
 class Net {
@@ -139,7 +146,7 @@ class Net {
   void read_output(int node, int stream, float* out_chw);
   void read_state(int node, int stream, float* out_chw);
   void read_changes(int node, int stream, uint8_t* map, int32_t* rowcol, int64_t* count, bool worst = false);
-  void read_counts(std::vector<int32_t>& counts);  // [slot][S]
+  void read_counts(std::vector<int32_t>& counts);  // [S][count_slots()]
   int64_t count_of(const std::vector<int32_t>& counts, int node, int stream, bool worst = false) const;
   bool has_worst_case(int node) const { return nodes_[node].wc_slot >= 0 && last_flags_ & CBG_FWD_RECORD_WORST_CASE; }
 
@@ -148,13 +155,16 @@ class Net {
   // "<node>.<kernel>" -> accumulated ms and launch count. Instrumentation only.
   void set_timing(bool on);
   std::string timing_report() const;  // JSON object
+  // labels of the kernels one frame launches, in launch order (no launches)
+  std::vector<std::string> kernel_labels(unsigned flags);
   void copy_output_async(int node, void* host_dst);  // raw NHWC [S][H][W][Cs] on the ctx stream
   // the same bytes through a device staging buffer: D2D on the ctx stream, D2H
   // on the ctx's copy-out stream, so the next frame does not wait for PCIe
   void copy_output_detached(int node, void* host_dst);
-  void copy_counts_async(int32_t* host_dst);         // [slot][S] on the ctx stream
-  int count_slots() const { return n_slots_; }
+  void copy_counts_async(int32_t* host_dst);         // [S][count_slots()] on the ctx stream
+  int count_slots() const { return cnt_stride_; }  // counters per stream in the [S][slots] count array
   int node_slot(int node) const { return nodes_[node].count_slot; }
+  int det_slot(int node) const { return nodes_[node].det_slot; }
 
  private:
   void build();
@@ -162,7 +172,6 @@ class Net {
   // s8 = the first detect compares against the 8-bit state shadow
   void enqueue_frame(unsigned flags, bool u8 = false, bool bcast = false, int slot8 = 0, bool s8 = false);
   int launch_count(unsigned flags) const;
-  void clear_maps();
 
   Ctx* ctx_;
   Topology topo_;
@@ -173,11 +182,10 @@ class Net {
   // running max |value| per stream: entry 0 = network input (state of the first
   // layer), entry i+1 = node i's output; the fp16 GEMM scales come from these
   DevBuf amax_;
-  // compaction counters [node][main, worst-case][S][offset, tiles done], zeroed per frame
-  DevBuf dc_ctr_;
-  int32_t* dc_ctr(int node, bool worst) const {
-    return dc_ctr_.as<int32_t>() + (static_cast<size_t>(node) * 2 + (worst ? 1 : 0)) * S_ * 2;
-  }
+  // bitmaps written by OR (sparse detections): one arena, zeroed by begin_frame
+  DevBuf clear_;
+  int n_ext_slots_ = 0;
+  int cnt_stride_ = 32;  // ints per stream in counts_  // count slots [0, n_ext_slots_) are uploaded (external nodes), the rest zeroed per frame
   // 8-bit ingest: two staging buffers filled on a copy stream while the other
   // one is being consumed, and three device pointer slots (buffer 0, buffer 1,
   // caller's device pointer) the first detect reads through
@@ -214,6 +222,8 @@ class Net {
   std::vector<cudaEvent_t> ev_map_;
   bool side_dc_ = true;
   bool timing_ = false;
+  bool dry_ = false;  // kernel_labels(): record labels, launch nothing
+  std::vector<std::string> dry_labels_;
   std::vector<cudaEvent_t> ev_pool_;
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending_;
   std::map<std::string, std::pair<double, long long>> times_;

@@ -4,20 +4,18 @@ kernel label ("<node>.<kernel>", the labels bench.py's roofline uses).
 
   ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum \
       --clock-control none --print-units base --csv --log-file gpurun_out/traffic.csv \
-      python tools/profile_run.py --streams 64 --frames 6
-  python tools/ncu_traffic.py gpurun_out/traffic.csv --streams 64
+      python tools/profile_run.py --streams 64 --frames 6 --labels gpurun_out/labels.json
+  python tools/ncu_traffic.py gpurun_out/traffic.csv --streams 64 --labels gpurun_out/labels.json
 """
 import argparse
 import csv
 import json
 import os
 
-LABELS = ["frame.begin", "L1.detect", "L1.dilcomp", "L1.gemm", "L2b.dilcomp", "L2b.pool", "L3.detect", "L3.dilcomp",
-          "L3.gemm", "L4b.dilcomp", "L4b.pool", "L5.detect", "L5.dilcomp", "L5.gemm", "L6.detect", "L6.dilcomp",
-          "L6.gemm", "L7.detect", "L7.dilcomp", "L7.gemm"]
 
 ap = argparse.ArgumentParser()
 ap.add_argument("csv")
+ap.add_argument("--labels", required=True, help="labels.json written by tools/profile_run.py --labels")
 ap.add_argument("--streams", type=int, required=True)
 ap.add_argument("--height", type=int, default=480)
 ap.add_argument("--width", type=int, default=640)
@@ -38,6 +36,7 @@ for r in rows:
         unit = d.get("Metric Unit", "")
         v *= {"Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "usecond": 1e3, "msecond": 1e6}.get(unit, 1.0)
         launches.setdefault(lid, {"name": d["Kernel Name"]})[d["Metric Name"]] = v
+LABELS = json.load(open(a.labels))
 ids = sorted(launches)
 frame = [launches[i] for i in ids[-len(LABELS):]]  # the last frame
 assert "begin_frame" in frame[0]["name"], frame[0]["name"]

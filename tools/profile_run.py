@@ -23,6 +23,7 @@ ap.add_argument("--object-size", type=int, default=40)
 ap.add_argument("--velocity", type=int, default=4)
 ap.add_argument("--dense", action="store_true")
 ap.add_argument("--ingest", choices=["u8", "f32"], default="u8", help="frame format, as bench.py --ingest")
+ap.add_argument("--labels", default="", help="write the frame's kernel labels (launch order) here")
 a = ap.parse_args()
 S, H, W = a.streams, a.height, a.width
 spec = cbi.make_seg_spec(1, H, W)
@@ -38,4 +39,8 @@ for t in range(a.frames):
     else:
         net.enqueue(np.ascontiguousarray(cbi.from_pnm8(pnm[t])))
 net.synchronize()
+if a.labels:
+    import json
+    with open(a.labels, "w") as fh:
+        json.dump(net.kernel_labels(), fh)
 print("counts L1..L7 (stream 0):", net.counts()[:, 0].tolist())
