@@ -390,8 +390,9 @@ def main():
     nodes = net.nodes()
     counts_pinned = torch.empty((G, a.steps + 1, Sg, n_slots), dtype=torch.int32, pin_memory=True)
 
-    def timed_region(step_fn, steps):
-        """device time of `steps` calls of step_fn(k) across all groups (CUDA events)"""
+    def timed_region(step_fn, steps, finish=None):
+        """device time of `steps` calls of step_fn(k) across all groups (CUDA
+        events); finish() runs on the host before the end event is recorded"""
         t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         torch.cuda.synchronize()
         t0.record(ext)
@@ -399,6 +400,8 @@ def main():
             e.wait_event(t0)
         for k in range(steps):
             step_fn(k)
+        if finish is not None:
+            finish()
         for e in exts[1:]:
             ev = torch.cuda.Event()
             ev.record(e)
@@ -671,7 +674,7 @@ def main():
     # ---- e2e: host frames through the C ABI, H2D + D2H in the timed region -------
     # headline: 8-bit PNM payloads (cbg_net_forward_u8, load_pnm's conversion on
     # the device); also the fp32 Tensor3 API (cbg_net_forward) with host frames
-    e2e = e2e_f32 = None
+    e2e = e2e_f32 = e2e_full = None
     if not a.no_e2e:
         hnp = None
         if a.config == "cfg2":  # host fp32 frames (4x the bytes) for the Tensor3 arm
@@ -679,45 +682,95 @@ def main():
             for t in range(L):
                 hnp[t] = cbi.from_pnm8(h8np[t])
 
-        def run_e2e(u8):
+        def run_e2e(u8, delta):
+            """host frames in (H2D inside), the step's result out: delta = this
+            frame's changed pixels of the last node + their output vectors, written
+            into pinned host memory by the copy-out kernel and scattered into a
+            persistent host mirror of the full output (step k applied while steps
+            k+1..k+LAG run, one host thread per stream group); else the whole
+            output (copy_output_detached)"""
+            LAG = 3
             enets = [cbi.convert_to_cb(spec, taus, n_streams=Sg, ctx=ctxs[g]) for g in range(G)]
             out_bytes = enets[0].output_bytes(-1)
-            out_host = [torch.empty(out_bytes // 4, dtype=torch.float32, pin_memory=True) for _ in range(G)]
+            if delta:
+                dbufs = [[cbi.HostBuffer(enets[g].output_delta_bytes(-1)) for _ in range(LAG + 1)] for g in range(G)]
+                mirrors = [np.zeros(out_bytes // 4, np.float32) for _ in range(G)]
+                appl = ThreadPoolExecutor(max_workers=G)
+                dbytes, dma = [], []
+            else:
+                out_host = [torch.empty(out_bytes // 4, dtype=torch.float32, pin_memory=True) for _ in range(G)]
 
             def put(g, k):
                 if u8:
                     enets[g].enqueue_u8(h8np[k, g * Sg:(g + 1) * Sg])
                 else:
                     enets[g].enqueue(hnp[k, g * Sg:(g + 1) * Sg])
+
+            def out(g, k):
+                if delta:
+                    enets[g].copy_output_delta(dbufs[g][k % (LAG + 1)].ptr)
+                    dma.append(enets[g].last_delta_dma_bytes())
+                else:
+                    enets[g].copy_output_detached(out_host[g].data_ptr())
+
+            def apply(k):  # host mirrors take step k's deltas
+                list(appl.map(lambda g: enets[g].apply_output_delta(dbufs[g][k % (LAG + 1)].ptr, mirrors[g].ctypes.data),
+                              range(G)))
+                n = sum(int(enets[g].delta_counts(dbufs[g][k % (LAG + 1)].array).sum()) for g in range(G))
+                px_bytes = out_bytes // (Sg * nodes[-1].out_shape[1] * nodes[-1].out_shape[2])  # Cs floats
+                dbytes.append(G * ((4 * Sg + 15) // 16 * 16) + n * (4 + px_bytes))
             for g in range(G):
                 put(g, 0)
+                out(g, 0)
             for k in range(a.warmup):
                 for g in range(G):
                     put(g, frame_at(k))
-                    enets[g].copy_output_detached(out_host[g].data_ptr())  # staging buffers allocated here
+                    out(g, k + 1)  # staging / host buffers allocated here
             for c in ctxs:
                 c.synchronize()
+            if delta:
+                for k in range(a.warmup + 1):
+                    apply(k)
+                dbytes.clear()
+                dma.clear()
             barrier()
 
             def e2e_step(k):
                 for g in range(G):
                     put(g, frame_at(base_k + k))
-                    enets[g].copy_output_detached(out_host[g].data_ptr())
+                    out(g, k)
+                if delta and k >= LAG:
+                    apply(k - LAG)
 
-            ems = max_over_ranks(timed_region(e2e_step, a.steps))
+            def finish():
+                for k in range(max(0, a.steps - LAG), a.steps):
+                    apply(k)
+            ems = max_over_ranks(timed_region(e2e_step, a.steps, finish if delta else None))
             del enets
-            return {"value": total_streams * a.steps / (ems / 1000.0), "unit": "frames/s",
-                    "h2d_bytes_per_step": frame8_bytes if u8 else frame_bytes, "d2h_bytes_per_step": out_bytes * G,
-                    "ms_per_step": ems / a.steps}
-        e2e = run_e2e(True)
+            r = {"value": total_streams * a.steps / (ems / 1000.0), "unit": "frames/s",
+                 "h2d_bytes_per_step": frame8_bytes if u8 else frame_bytes,
+                 "d2h_bytes_per_step": (sum(dma) / a.steps) if delta else out_bytes * G,
+                 "ms_per_step": ems / a.steps}
+            if delta:
+                appl.shutdown()
+                r["d2h_full_output_bytes"] = out_bytes * G
+                r["d2h_delta_bytes_in_use"] = sum(dbytes) / len(dbytes)
+            return r
+        e2e = run_e2e(True, True)
         e2e["api"] = ("cbg_net_forward_u8: pinned host 8-bit PNM payloads [S][H][W][3], load_pnm conversion "
-                      "(byte/255.0f) fused into the first layer's detect; D2H of the last node's output "
-                      "(cbg_net_copy_output_detached: staged on the device, copied out on the context's "
-                      "copy-out stream)")
+                      "(byte/255.0f) fused into the first layer's detect; result: cbg_net_copy_output_delta (the "
+                      "last node's changed pixels and their output vectors, packed on the device and copied into "
+                      "pinned host memory on the copy-out stream) + cbg_net_apply_output_delta into a host mirror of the full "
+                      "output (the reference's whole-Tensor3 result, network.cpp:412-413), step k applied while "
+                      "steps k+1..k+3 run; d2h bytes = bytes moved (DMA of the recent delta size + 25%, overflow "
+                      "kernel for the rest)")
+        e2e_full = run_e2e(True, False)
+        e2e_full["api"] = ("as e2e, but the whole last-node output D2H every step (cbg_net_copy_output_detached: "
+                           "staged on the device, copied out on the context's copy-out stream)")
         if hnp is not None:
-            e2e_f32 = run_e2e(False)
-            e2e_f32["api"] = ("cbg_net_forward: pinned host fp32 CHW frames (Tensor3); D2H of the last node's "
-                              "output (cbg_net_copy_output_detached)")
+            e2e_f32 = run_e2e(False, True)
+            e2e_f32["api"] = ("cbg_net_forward: pinned host fp32 CHW frames (Tensor3); result as e2e (delta + "
+                              "host mirror)")
 
     # ---- CPU baseline (rank 0, N=1) ---------------------------------------------
     cpu = None
@@ -767,7 +820,8 @@ def main():
                           "per_layer_changed_frac": per_layer},
                "dense_path_fps": dense_fps, "speedup_vs_dense": (value / dense_fps) if dense_fps else None,
                "sweep": sweep, "crossover_l1_changed_pct": crossover,
-               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_f32": e2e_f32, "parity": parity,
+               "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_full_output": e2e_full, "e2e_f32": e2e_f32,
+               "parity": parity,
                "gpu_launches": launches * a.steps,
                "clocks": clocks.summary()}
         print(json.dumps(out))

@@ -315,6 +315,29 @@ int cbg_net_copy_output_async(cbg_net net, int node, void* host_dst);
  * or after the copy-out stream. host_dst should be pinned. */
 int cbg_net_copy_output_detached(cbg_net net, int node, void* host_dst);
 void* cbg_ctx_copy_stream(cbg_ctx ctx);
+/* Delta output, the reference's full-output semantics (forward_frame returns
+ * the whole retained output, network.cpp:412-413) with only this frame's
+ * changes crossing PCIe: after a frame, the node's changed pixels and their raw
+ * output vectors [Cs floats, the layout of cbg_net_copy_output_async] are
+ * packed on the ctx stream and copied into host_buf (pinned, mapped host
+ * memory of cbg_net_output_delta_bytes) on the copy-out stream:
+ *   int32 n[S] (padded to 16 B), then per stream: int32 ids[n_s] (padded to
+ *   16 B), float vals[n_s][Cs]. cbg_net_apply_output_delta
+ * waits for the copy into host_buf, then scatters streams [stream_begin,
+ * stream_end) into a host mirror [S][H][W][Cs] of the raw output that the
+ * caller keeps across frames (initialised from a full copy, or zeros before the
+ * first frame: every pixel of a full update is in the delta). */
+int cbg_net_output_delta_bytes(cbg_net net, int node, int64_t* bytes);
+/* Pinned, mapped, portable host memory (what the copy functions above expect). */
+int cbg_host_alloc(int64_t bytes, void** ptr);
+void cbg_host_free(void* ptr);
+int cbg_net_copy_output_delta(cbg_net net, int node, void* host_buf);
+/* Bytes the last cbg_net_copy_output_delta moved by DMA (an estimate from the
+ * recently applied deltas + 25%; a larger delta's remaining bytes are written
+ * by an overflow kernel). */
+int cbg_net_last_delta_dma_bytes(cbg_net net, int64_t* bytes);
+int cbg_net_apply_output_delta(cbg_net net, int node, const void* host_buf, float* mirror, int stream_begin,
+                               int stream_end);
 int cbg_net_output_bytes(cbg_net net, int node, int64_t* bytes);
 /* Asynchronous D2H copy of the per-frame change counts [n_streams][slots]
  * (int32, slots = cbg_net_count_slots) into host memory; node_slot (nullable)

@@ -160,6 +160,12 @@ SIGNATURES = {
     "cbg_net_copy_output_async": (C.c_int, [_vp, C.c_int, _vp]),
     "cbg_net_copy_output_detached": (C.c_int, [_vp, C.c_int, _vp]),
     "cbg_net_output_bytes": (C.c_int, [_vp, C.c_int, _P(C.c_int64)]),
+    "cbg_net_output_delta_bytes": (C.c_int, [_vp, C.c_int, _P(C.c_int64)]),
+    "cbg_host_alloc": (C.c_int, [C.c_int64, _P(_vp)]),
+    "cbg_host_free": (None, [_vp]),
+    "cbg_net_copy_output_delta": (C.c_int, [_vp, C.c_int, _vp]),
+    "cbg_net_last_delta_dma_bytes": (C.c_int, [_vp, _P(C.c_int64)]),
+    "cbg_net_apply_output_delta": (C.c_int, [_vp, C.c_int, _vp, _vp, C.c_int, C.c_int]),
     "cbg_net_copy_counts_async": (C.c_int, [_vp, _vp, _vp]),
     "cbg_net_count_slots": (C.c_int, [_vp, _P(C.c_int)]),
     "cbg_net_detect_slots": (C.c_int, [_vp, _vp]),

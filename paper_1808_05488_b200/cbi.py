@@ -429,6 +429,24 @@ def make_small_spec(seed: int, in_channels: int, height: int, width: int) -> Net
     return spec
 
 
+class HostBuffer:
+    """Pinned, mapped host memory (cbg_host_alloc) viewed as a numpy array."""
+
+    def __init__(self, nbytes: int, dtype=np.uint8):
+        p = C.c_void_p()
+        check(lib.cbg_host_alloc(int(nbytes), C.byref(p)))
+        self.ptr = p.value
+        self.nbytes = int(nbytes)
+        itemsize = np.dtype(dtype).itemsize
+        self.array = np.ctypeslib.as_array((C.c_uint8 * self.nbytes).from_address(self.ptr)).view(dtype)[
+            :self.nbytes // itemsize]
+
+    def __del__(self):
+        if getattr(self, "ptr", None):
+            lib.cbg_host_free(C.c_void_p(self.ptr))
+            self.ptr = None
+
+
 # ---------------------------------------------------------------------------
 # device context
 # ---------------------------------------------------------------------------
@@ -896,6 +914,34 @@ class CBNetwork:
         """copy_output_async through a device staging buffer, D2H on the context's
         copy-out stream: the next frame does not wait for PCIe (Context.synchronize waits for it)"""
         check(lib.cbg_net_copy_output_detached(self.handle, node, C.c_void_p(host_ptr)))
+    def output_delta_bytes(self, node: int = -1) -> int:
+        n = C.c_int64()
+        check(lib.cbg_net_output_delta_bytes(self.handle, node, C.byref(n)))
+        return n.value
+
+    def copy_output_delta(self, host_ptr: int, node: int = -1):
+        """this frame's changed pixels of `node` and their raw output vectors into
+        pinned host memory (cbg_net_copy_output_delta layout: packed, only the
+        changed bytes cross PCIe), on the context's copy-out stream"""
+        check(lib.cbg_net_copy_output_delta(self.handle, node, C.c_void_p(host_ptr)))
+
+    def last_delta_dma_bytes(self) -> int:
+        n = C.c_int64()
+        check(lib.cbg_net_last_delta_dma_bytes(self.handle, C.byref(n)))
+        return n.value
+
+    def apply_output_delta(self, host_ptr: int, mirror_ptr: int, node: int = -1, streams=None):
+        """wait for the delta in host_ptr, scatter streams [s0, s1) into the host
+        mirror of the raw output [S][H][W][Cs] (releases the GIL: callers may
+        split the streams over threads)"""
+        s0, s1 = streams if streams is not None else (0, self.n_streams)
+        check(lib.cbg_net_apply_output_delta(self.handle, node, C.c_void_p(host_ptr), C.c_void_p(mirror_ptr),
+                                             s0, s1))
+
+    def delta_counts(self, host_buf: np.ndarray) -> np.ndarray:
+        """per-stream changed-pixel counts at the head of a delta buffer"""
+        return np.frombuffer(host_buf, np.int32, count=self.n_streams)
+
     def count_layout(self):
         """(slots, node->slot) of the device change-count array [S][slots]."""
         n = C.c_int()

@@ -405,6 +405,48 @@ int cbg_net_count_slots(cbg_net net, int* slots) {
     *slots = std::max(1, net->net->count_slots());
   });
 }
+int cbg_host_alloc(int64_t bytes, void** ptr) {
+  return guard([&] {
+    need(ptr, "cbg_host_alloc");
+    if (bytes < 0) cbg::throw_invalid("cbg_host_alloc: negative size");
+    *ptr = nullptr;
+    cbg::cuda_check(cudaHostAlloc(ptr, static_cast<size_t>(std::max<int64_t>(bytes, 1)),
+                                  cudaHostAllocMapped | cudaHostAllocPortable), "cudaHostAlloc");
+  });
+}
+void cbg_host_free(void* ptr) {
+  if (ptr) cudaFreeHost(ptr);
+}
+int cbg_net_output_delta_bytes(cbg_net net, int node, int64_t* bytes) {
+  return guard([&] {
+    need(net, "cbg_net_output_delta_bytes");
+    need(bytes, "cbg_net_output_delta_bytes");
+    *bytes = static_cast<int64_t>(net->net->output_delta_bytes(node));
+  });
+}
+int cbg_net_last_delta_dma_bytes(cbg_net net, int64_t* bytes) {
+  return guard([&] {
+    need(net, "cbg_net_last_delta_dma_bytes");
+    need(bytes, "cbg_net_last_delta_dma_bytes");
+    *bytes = static_cast<int64_t>(net->net->last_delta_dma_bytes());
+  });
+}
+int cbg_net_copy_output_delta(cbg_net net, int node, void* host_buf) {
+  return guard([&] {
+    need(net, "cbg_net_copy_output_delta");
+    need(host_buf, "cbg_net_copy_output_delta");
+    net->net->copy_output_delta(node, host_buf);
+  });
+}
+int cbg_net_apply_output_delta(cbg_net net, int node, const void* host_buf, float* mirror, int stream_begin,
+                               int stream_end) {
+  return guard([&] {
+    need(net, "cbg_net_apply_output_delta");
+    need(host_buf, "cbg_net_apply_output_delta");
+    need(mirror, "cbg_net_apply_output_delta");
+    net->net->apply_output_delta(node, host_buf, mirror, stream_begin, stream_end);
+  });
+}
 int cbg_net_copy_output_detached(cbg_net net, int node, void* host_dst) {
   return guard([&] {
     need(net, "cbg_net_copy_output_detached");

@@ -968,6 +968,49 @@ __global__ void begin_frame_kernel(BeginFrameArgs a) {
     a.clear[i] = make_uint4(0u, 0u, 0u, 0u);
 }
 
+// ---------------------------------------------------------------------------
+// delta output: pack (device -> staging, on the frame's stream); the copy-out
+// stream then moves an estimated prefix [0, copied) to the host by DMA, and
+// the pack itself writes any byte past that prefix straight into the mapped
+// host buffer (from the SMs, only when a frame changed more than estimated)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kThreads) pack_delta_kernel(DeltaArgs a) {
+  const int s = blockIdx.y;
+  __shared__ size_t s_off;
+  if (threadIdx.x == 0) {
+    size_t off = delta_header_bytes(a.S);
+    for (int j = 0; j < s; ++j) off += delta_stream_bytes(a.count[j * a.cnt_stride], a.Cs);
+    s_off = off;
+  }
+  __syncthreads();
+  const int n = a.count[s * a.cnt_stride];
+  const size_t copied = static_cast<size_t>(a.copied);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    reinterpret_cast<int32_t*>(a.dst)[s] = n;
+    if (4u * s >= copied) reinterpret_cast<int32_t*>(a.host)[s] = n;
+  }
+  const size_t ids_off = s_off, vals_off = s_off + (static_cast<size_t>(n) * 4 + 15) / 16 * 16;
+  int32_t* ids = reinterpret_cast<int32_t*>(a.dst + ids_off);
+  float4* vals = reinterpret_cast<float4*>(a.dst + vals_off);
+  const int32_t* list = a.idx + s * a.HW;
+  const int nv = a.Cs / 4;
+  const float4* out = reinterpret_cast<const float4*>(a.out) + s * a.HW * nv;
+  const long long total = static_cast<long long>(n) * nv;
+  for (long long w = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; w < total;
+       w += static_cast<long long>(gridDim.x) * blockDim.x) {
+    const long long k = w / nv;
+    const int v = static_cast<int>(w - k * nv);
+    const int p = __ldg(list + k);
+    const float4 x = ldg_nc_f4(reinterpret_cast<const float*>(out + static_cast<long long>(p) * nv + v));
+    if (v == 0) {
+      ids[k] = p;
+      if (ids_off + 4 * k >= copied) reinterpret_cast<int32_t*>(a.host + ids_off)[k] = p;
+    }
+    vals[w] = x;
+    if (vals_off + 16 * w >= copied) reinterpret_cast<float4*>(a.host + vals_off)[w] = x;
+  }
+}
+
 __global__ void nhwc_to_chw_kernel(const float* src, float* dst, int C, int Cs, long long HW) {
   for (long long w = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; w < C * HW;
        w += static_cast<long long>(gridDim.x) * blockDim.x) {
@@ -1077,6 +1120,11 @@ void launch_join(const JoinArgs& a, cudaStream_t st) {
 void launch_begin_frame(const BeginFrameArgs& a, cudaStream_t st) {
   const long long g = std::min<long long>(2 * sm_count(), (a.n_clear + 255) / 256);
   begin_frame_kernel<<<static_cast<int>(std::max<long long>(1, g)), 256, 0, st>>>(a);
+}
+
+void launch_pack_delta(const DeltaArgs& a, cudaStream_t st) {
+  dim3 grid(std::max(1, 2 * sm_count() / std::max(1, a.S)), a.S);
+  pack_delta_kernel<<<grid, kThreads, 0, st>>>(a);
 }
 
 void launch_nhwc_to_chw(const float* src, float* dst, int C, int Cs, int HW, cudaStream_t st) {

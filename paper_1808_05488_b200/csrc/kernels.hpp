@@ -212,6 +212,35 @@ struct BeginFrameArgs {
 };
 void launch_begin_frame(const BeginFrameArgs& a, cudaStream_t st);
 
+// Delta output of a node (its changed pixels and their output vectors),
+// packed contiguously — the layout of the device staging copy and of the
+// pinned host buffer:
+//   int32 n[S] (padded to 16 B), then per stream s in order: int32 ids[n_s]
+//   (padded to 16 B) and float vals[n_s][Cs]
+// so the bytes in use are delta_header_bytes(S) + sum_s delta_stream_bytes(n_s, Cs).
+struct DeltaArgs {
+  const float* out;      // pack: the node's output [S][HW][Cs]
+  const int32_t* idx;    // pack: its index list [S][HW]
+  const int32_t* count;  // pack: [s * cnt_stride]
+  int cnt_stride;
+  uint8_t* dst;          // the staging buffer
+  uint8_t* host;         // the host buffer (device address of mapped pinned memory)
+  long long copied;      // bytes [0, copied) go to the host by DMA; the kernel writes the rest there
+  int Cs, S;
+  long long HW;
+};
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline size_t delta_header_bytes(int S) { return (static_cast<size_t>(S) * 4 + 15) / 16 * 16; }
+#ifdef __CUDACC__
+__host__ __device__
+#endif
+inline size_t delta_stream_bytes(long long n, int Cs) {
+  return (static_cast<size_t>(n) * 4 + 15) / 16 * 16 + static_cast<size_t>(n) * Cs * 4;
+}
+void launch_pack_delta(const DeltaArgs& a, cudaStream_t st);
+
 // Layout conversions for the synchronising readers and standalone uploads.
 void launch_nhwc_to_chw(const float* src, float* dst, int C, int Cs, int HW, cudaStream_t st);
 void launch_chw_to_nhwc(const float* src, float* dst, int C, int Cs, int HW, cudaStream_t st);

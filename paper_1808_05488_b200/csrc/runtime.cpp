@@ -480,6 +480,14 @@ Net::~Net() {
   }
   for (auto& e : ev_map_) cudaEventDestroy(e);
   for (int b = 0; b < 2; ++b) {
+    if (ev_dstaged_[b]) cudaEventDestroy(ev_dstaged_[b]);
+    if (ev_dpushed_[b]) {
+      cudaEventSynchronize(ev_dpushed_[b]);
+      cudaEventDestroy(ev_dpushed_[b]);
+    }
+  }
+  for (auto& kv : delta_host_) cudaEventDestroy(kv.second.ev);
+  for (int b = 0; b < 2; ++b) {
     if (ev_staged_[b]) cudaEventDestroy(ev_staged_[b]);
     if (ev_drained_[b]) {
       cudaEventSynchronize(ev_drained_[b]);
@@ -1138,6 +1146,99 @@ void Net::copy_output_detached(int node, void* host_dst) {
   CK(cudaStreamWaitEvent(ctx_->d2h, ev_staged_[b], 0));
   CK(cudaMemcpyAsync(host_dst, out_stage_[b].p, r.out.bytes, cudaMemcpyDeviceToHost, ctx_->d2h));
   CK(cudaEventRecord(ev_drained_[b], ctx_->d2h));
+}
+
+size_t Net::output_delta_bytes(int node) const {
+  if (node < 0) node = static_cast<int>(nodes_.size()) - 1;
+  if (node >= static_cast<int>(nodes_.size())) throw_invalid("output_delta_bytes: bad node");
+  const NodeRT& r = nodes_[node];
+  const long long HW = static_cast<long long>(r.d.H) * r.d.W;
+  return delta_header_bytes(S_) + static_cast<size_t>(S_) * delta_stream_bytes(HW, r.Cs);
+}
+
+void Net::copy_output_delta(int node, void* host_buf) {
+  if (node < 0) node = static_cast<int>(nodes_.size()) - 1;
+  if (node >= static_cast<int>(nodes_.size())) throw_invalid("copy_output_delta: bad node");
+  const NodeRT& r = nodes_[node];
+  void* dptr = nullptr;
+  if (cudaHostGetDevicePointer(&dptr, host_buf, 0) != cudaSuccess || dptr == nullptr) {
+    cudaGetLastError();
+    throw_invalid("copy_output_delta: host buffer is not pinned, mapped host memory");
+  }
+  cudaStream_t st = ctx_->stream;
+  const size_t cap = output_delta_bytes(node);
+  if (!ev_dstaged_[0])
+    for (int b = 0; b < 2; ++b) {
+      CK(cudaEventCreateWithFlags(&ev_dstaged_[b], cudaEventDisableTiming));
+      CK(cudaEventCreateWithFlags(&ev_dpushed_[b], cudaEventDisableTiming));
+    }
+  const int b = delta_buf_;
+  delta_buf_ ^= 1;
+  if (delta_stage_[b].bytes < cap) {
+    CK(cudaEventSynchronize(ev_dpushed_[b]));
+    delta_stage_[b].alloc(cap);
+  }
+  // staging b is free once its previous copy-out (two calls ago) has finished
+  CK(cudaStreamWaitEvent(st, ev_dpushed_[b], 0));
+  // DMA of the expected size: the largest of the last applied deltas + 25%
+  // (the whole capacity until one was seen); the pack writes bytes past it
+  // into the host buffer itself (no kernel on the copy-out stream: it would
+  // share a hardware queue with other streams' work)
+  size_t est = cap;
+  if (delta_seen_ > 0) {
+    size_t m = 0;
+    for (size_t v : delta_recent_) m = std::max(m, v);
+    est = std::min(cap, (m + m / 4 + 65536 + 15) / 16 * 16);
+  }
+  DeltaArgs a{};
+  a.out = r.out.as<float>();
+  a.idx = r.idx;
+  a.count = counts_.as<int32_t>() + r.count_slot;
+  a.cnt_stride = cnt_stride_;
+  a.dst = delta_stage_[b].as<uint8_t>();
+  a.host = static_cast<uint8_t*>(dptr);
+  a.copied = static_cast<long long>(est);
+  a.Cs = r.Cs, a.S = S_;
+  a.HW = static_cast<long long>(r.d.H) * r.d.W;
+  launch_pack_delta(a, st);
+  CK(cudaEventRecord(ev_dstaged_[b], st));
+  CK(cudaStreamWaitEvent(ctx_->d2h, ev_dstaged_[b], 0));
+  CK(cudaMemcpyAsync(host_buf, delta_stage_[b].p, est, cudaMemcpyDeviceToHost, ctx_->d2h));
+  delta_dma_last_ = est;
+  CK(cudaEventRecord(ev_dpushed_[b], ctx_->d2h));
+  DeltaCopy& dc = delta_host_[host_buf];
+  if (!dc.ev) CK(cudaEventCreateWithFlags(&dc.ev, cudaEventDisableTiming));
+  CK(cudaEventRecord(dc.ev, ctx_->d2h));
+}
+
+void Net::apply_output_delta(int node, const void* host_buf, float* mirror, int s0, int s1) {
+  if (node < 0) node = static_cast<int>(nodes_.size()) - 1;
+  if (node >= static_cast<int>(nodes_.size())) throw_invalid("apply_output_delta: bad node");
+  if (s0 < 0 || s1 > S_ || s0 > s1) throw_invalid("apply_output_delta: bad stream range");
+  auto it = delta_host_.find(host_buf);
+  if (it == delta_host_.end()) throw_invalid("apply_output_delta: no delta was copied into this buffer");
+  CK(cudaEventSynchronize(it->second.ev));
+  const NodeRT& r = nodes_[node];
+  const int Cs = r.Cs;
+  const uint8_t* buf = static_cast<const uint8_t*>(host_buf);
+  const int32_t* hdr = reinterpret_cast<const int32_t*>(buf);
+  size_t off = delta_header_bytes(S_);
+  const size_t HWC = static_cast<size_t>(r.d.H) * r.d.W * Cs;
+  for (int s = 0; s < s1; ++s) {
+    const int n = hdr[s];
+    if (s >= s0) {
+      const int32_t* ids = reinterpret_cast<const int32_t*>(buf + off);
+      const float* vals = reinterpret_cast<const float*>(buf + off + (static_cast<size_t>(n) * 4 + 15) / 16 * 16);
+      float* m = mirror + s * HWC;
+      for (int k = 0; k < n; ++k)
+        std::memcpy(m + static_cast<size_t>(ids[k]) * Cs, vals + static_cast<size_t>(k) * Cs, Cs * 4);
+    }
+    off += delta_stream_bytes(n, Cs);
+  }
+  if (s1 == S_) {  // the whole buffer's size feeds the next DMA estimates
+    for (int s = s1; s < S_; ++s) off += delta_stream_bytes(hdr[s], Cs);
+    delta_recent_[delta_seen_++ % 4] = off;
+  }
 }
 
 void Net::set_external(const float* x_chw, const uint8_t* map, const int32_t* rowcol, int64_t n, bool full) {

@@ -162,6 +162,16 @@ class Net {
   // on the ctx's copy-out stream, so the next frame does not wait for PCIe
   void copy_output_detached(int node, void* host_dst);
   void copy_counts_async(int32_t* host_dst);         // [S][count_slots()] on the ctx stream
+  // Delta output (kernels.hpp DeltaArgs layout): the node's changed pixels of
+  // this frame and their raw output vectors, packed on the ctx stream, then on
+  // the copy-out stream a DMA of an estimated prefix (the recent sizes + 25%)
+  // and an overflow kernel that writes any bytes past it into the pinned
+  // (mapped) host buffer; apply_output_delta waits for that copy and scatters
+  // streams [s0, s1) into a host mirror of the raw output [S][H][W][Cs].
+  size_t output_delta_bytes(int node) const;
+  void copy_output_delta(int node, void* host_buf);
+  void apply_output_delta(int node, const void* host_buf, float* mirror, int s0, int s1);
+  size_t last_delta_dma_bytes() const { return delta_dma_last_; }  // DMA size of the last copy_output_delta
   int count_slots() const { return cnt_stride_; }  // counters per stream in the [S][slots] count array
   int node_slot(int node) const { return nodes_[node].count_slot; }
   int det_slot(int node) const { return nodes_[node].det_slot; }
@@ -197,6 +207,16 @@ class Net {
   // host view of the 8-bit state shadow: valid per stream once a full update
   // went through the 8-bit ingest; any fp32 frame invalidates it
   std::vector<uint8_t> s8_valid_, s8_pending_;
+  DevBuf delta_stage_[2];
+  cudaEvent_t ev_dstaged_[2] = {nullptr, nullptr}, ev_dpushed_[2] = {nullptr, nullptr};
+  int delta_buf_ = 0;
+  struct DeltaCopy {
+    cudaEvent_t ev = nullptr;  // the copy into this host buffer completed
+  };
+  std::map<const void*, DeltaCopy> delta_host_;     // host buffer -> its last copy
+  size_t delta_recent_[4] = {0, 0, 0, 0};           // bytes in use of the last applied deltas
+  int delta_seen_ = 0;
+  size_t delta_dma_last_ = 0;
   DevBuf out_stage_[2];
   cudaEvent_t ev_staged_[2] = {nullptr, nullptr}, ev_drained_[2] = {nullptr, nullptr};
   int out_buf_ = 0;

@@ -8,7 +8,7 @@ import ctypes as C
 import numpy as np
 import pytest
 
-from paper_1808_05488_b200 import cbi
+from paper_1808_05488_b200 import _lib, cbi
 from tests import oracle
 from tests.oracle import p
 from tests.test_oracle import conv_spec, random_net
@@ -344,3 +344,46 @@ def test_detached_output_copy_pipelines(gpu):
     a.synchronize()
     for t in range(T):
         assert np.array_equal(bufs[t], want[t]), t
+
+
+def test_output_delta_mirror_equals_full_output(gpu):
+    """cbg_net_copy_output_delta + cbg_net_apply_output_delta: a host mirror kept
+    from the per-frame deltas (changed pixels + their output vectors only) equals
+    the full raw output (copy_output_async) after every frame, with frames
+    enqueued back to back (two host buffers alternating), through a full update
+    (reset of one stream), a tau change and a forced full frame — larger than the
+    DMA estimate from the recent deltas, so its tail takes the overflow path."""
+    S, H, W, T = 3, 240, 320, 9
+    spec = cbi.make_seg_spec(8, H, W)
+    frames = np.stack([cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, T, 2, 10, 2, 3, 0.01, 70 + s))
+                       for s in range(S)], axis=1)
+    net = cbi.convert_to_cb(spec, [0.03] * 5, n_streams=S)
+    nbytes = net.output_bytes(-1)
+    bufs = [cbi.HostBuffer(net.output_delta_bytes(-1)) for _ in range(2)]
+    mirror = np.zeros(nbytes // 4, np.float32)
+    full = cbi.HostBuffer(nbytes, np.float32)
+    pending = None
+    for t in range(T):
+        if t == 4:
+            net.reset(1)
+        if t == 6:
+            net.set_thresholds([0.02] * 5)
+        net.enqueue(frames[t], flags=_lib.FWD_FORCE_FULL if t == 7 else 0)
+        net.copy_output_delta(bufs[t % 2].ptr)
+        dma = net.last_delta_dma_bytes()
+        if pending is not None:  # the previous frame's delta, applied while this frame runs
+            net.apply_output_delta(bufs[pending % 2].ptr, mirror.ctypes.data)
+            np.testing.assert_array_equal(mirror, want, err_msg=f"frame {pending}")
+        net.copy_output_async(full.ptr)
+        net.synchronize()
+        want = full.array.copy()
+        n = net.delta_counts(bufs[t % 2].array)
+        cnt = net.counts()[-1]
+        assert np.array_equal(n, cnt), (t, n, cnt)
+        used = 16 + sum((4 * int(k) + 15) // 16 * 16 + 32 * int(k) for k in n)  # Cs = 8
+        if t == 7:
+            assert used > dma, (used, dma)  # the forced full frame overflowed the estimate
+        pending = t
+    net.apply_output_delta(bufs[pending % 2].ptr, mirror.ctypes.data, streams=(0, 2))
+    net.apply_output_delta(bufs[pending % 2].ptr, mirror.ctypes.data, streams=(2, 3))
+    np.testing.assert_array_equal(mirror, want)
