@@ -49,7 +49,10 @@ enum {
 
 /* ---- enums mirroring the reference ---------------------------------------- */
 /* LayerKind, network.hpp:10 */
-enum { CBG_LAYER_CONV = 0, CBG_LAYER_ACT = 1, CBG_LAYER_POOL = 2, CBG_LAYER_ADD = 3, CBG_LAYER_CONCAT = 4 };
+enum { CBG_LAYER_CONV = 0, CBG_LAYER_ACT = 1, CBG_LAYER_POOL = 2, CBG_LAYER_ADD = 3, CBG_LAYER_CONCAT = 4,
+       /* extension beyond the reference (network.hpp:10 has no upsample): nearest-neighbour
+        * upsampling by an integer factor (YOLOv3-style detectors) */
+       CBG_LAYER_UPSAMPLE = 5 };
 /* DetectionPolicy, layers.hpp:8 */
 enum { CBG_POLICY_DETECT = 0, CBG_POLICY_PROPAGATE = 1, CBG_POLICY_REUSE1X1 = 2 };
 /* DetectMode, change.hpp:34 */
@@ -83,6 +86,15 @@ typedef struct cbg_layer_desc {
   cbg_conv_spec conv;      /* CONV */
   int fuse_relu;           /* CONV */
   int pool_size, pool_stride, pool_out_h, pool_out_w; /* POOL (out dims 0 = floor formula) */
+  /* Extensions beyond the reference (parity checked against the test-side C
+   * restatement oracle/cbi_oracle.c only: "parity unpinned"):
+   *   act_slope: ACT rows, and CONV rows with fuse_relu — 0 = ReLU
+   *              (std::max(v, 0.f), the reference), > 0 = leaky ReLU
+   *              v < 0 ? v * act_slope : v (Darknet's leaky, slope 0.1);
+   *   upsample:  UPSAMPLE rows, the integer factor: out(j, i) = in(j / f, i / f),
+ *              out dims in * f, or pool_out_h / pool_out_w when > 0 (a crop). */
+  float act_slope;
+  int upsample;
 } cbg_layer_desc;
 
 /* NetworkSpec, network.hpp:39-44 */

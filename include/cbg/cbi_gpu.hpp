@@ -100,7 +100,8 @@ struct ConvSpec {
 
 enum class DetectionPolicy { Detect = CBG_POLICY_DETECT, Propagate = CBG_POLICY_PROPAGATE, Reuse1x1 = CBG_POLICY_REUSE1X1 };
 enum class DetectMode { FeedForward = CBG_MODE_FEEDFORWARD, ClosedLoop = CBG_MODE_CLOSEDLOOP };
-enum class LayerKind { Conv = CBG_LAYER_CONV, Act = CBG_LAYER_ACT, Pool = CBG_LAYER_POOL, Add = CBG_LAYER_ADD, Concat = CBG_LAYER_CONCAT };
+enum class LayerKind { Conv = CBG_LAYER_CONV, Act = CBG_LAYER_ACT, Pool = CBG_LAYER_POOL, Add = CBG_LAYER_ADD, Concat = CBG_LAYER_CONCAT,
+                       Upsample = CBG_LAYER_UPSAMPLE /* extension: not in the reference */ };
 
 // ---- device context -----------------------------------------------------------------------
 class Context {
@@ -287,6 +288,8 @@ struct LayerDesc {
   ConvSpec conv;
   bool fuse_relu = false;
   int pool_size = 0, pool_stride = 0, pool_out_h = 0, pool_out_w = 0;
+  float act_slope = 0.0f;  // extension: leaky ReLU slope of an Act row / fused activation (0 = ReLU)
+  int upsample = 0;        // extension: Upsample rows' factor
 };
 
 struct NetworkSpec {
@@ -351,6 +354,8 @@ struct CSpec {
       c.pool_stride = d.pool_stride;
       c.pool_out_h = d.pool_out_h;
       c.pool_out_w = d.pool_out_w;
+      c.act_slope = d.act_slope;
+      c.upsample = d.upsample;
     }
     spec = cbg_network_spec{s.in_channels, s.in_height, s.in_width, static_cast<int>(layers.size()), layers.data()};
   }

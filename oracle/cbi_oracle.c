@@ -13,6 +13,14 @@
  *                    reset, set_thresholds                     (:37-503)
  * Built with -ffp-contract=off so every fp32 multiply and add rounds separately,
  * matching the reference's non-FMA SSE code at its own flags.
+ *
+ * EXTENSIONS (marked EXTENSION below): leaky ReLU (act_slope) and nearest
+ * upsampling (CBG_LAYER_UPSAMPLE) for the YOLOv3-style config. The reference
+ * has neither (network.hpp:10; PAPER.md:647 names the leaky ReLU), so these
+ * two are PARITY UNPINNED: no reference output or golden vector checks them;
+ * they restate the obvious definitions (Darknet's leaky: v < 0 ? v * slope :
+ * v; out(j, i) = in(j / f, i / f)) with the change map of a layer whose
+ * output depends on exactly one input pixel (the map expands like the data).
  */
 #include "cbi_oracle.h"
 
@@ -265,6 +273,8 @@ typedef struct {
   cbg_conv_spec spec;   /* conv: owns weights/bias */
   float tau;
   int policy, relu;
+  float slope;          /* EXTENSION (not in the reference): leaky ReLU slope of the fused act, 0 = ReLU */
+  int up;               /* EXTENSION: upsample factor */
   float* state;         /* conv Detect */
   float* prev;          /* retained output */
   int psize, pstride;   /* pool */
@@ -366,9 +376,20 @@ int cbo_net_create(const cbg_network_spec* spec, const float* taus, int n_taus,
         break;
       }
       case CBG_LAYER_ACT:
+        if (!(d->act_slope >= 0.0f)) BAIL(CBG_ERR_INVALID_INPUT, "layer %d: act slope must be >= 0", i);
         shp[i * 3] = sc;
         shp[i * 3 + 1] = sh;
         shp[i * 3 + 2] = sw;
+        break;
+      case CBG_LAYER_UPSAMPLE: /* EXTENSION: nearest-neighbour, integer factor */
+        if (n_in[i] != 1) BAIL(CBG_ERR_INVALID_INPUT, "layer %d: upsample takes exactly one producer", i);
+        if (d->upsample < 1) BAIL(CBG_ERR_INVALID_INPUT, "layer %d: upsample factor must be >= 1", i);
+        /* pool_out_h / pool_out_w > 0: cropped output dims (<= in * factor) */
+        if (d->pool_out_h < 0 || d->pool_out_w < 0 || d->pool_out_h > sh * d->upsample || d->pool_out_w > sw * d->upsample)
+          BAIL(CBG_ERR_INVALID_INPUT, "layer %d: upsample output dims out of range", i);
+        shp[i * 3] = sc;
+        shp[i * 3 + 1] = d->pool_out_h > 0 ? d->pool_out_h : sh * d->upsample;
+        shp[i * 3 + 2] = d->pool_out_w > 0 ? d->pool_out_w : sw * d->upsample;
         break;
       case CBG_LAYER_POOL: {
         if (d->pool_size < 1 || d->pool_stride < 1) BAIL(CBG_ERR_INVALID_INPUT, "layer %d: pool size/stride must be >= 1", i);
@@ -425,6 +446,7 @@ int cbo_net_create(const cbg_network_spec* spec, const float* taus, int n_taus,
         if (src0 < 0 || spec->layers[src0].kind != CBG_LAYER_CONV) BAIL(CBG_ERR_CONFIG, "layer %d: standalone activation can only be absorbed into a conv", i);
         if (consumers[src0] != 1) BAIL(CBG_ERR_CONFIG, "layer %d: cannot absorb activation, conv output has other consumers", i);
         net->nodes[new_id[src0]].relu = 1;
+        net->nodes[new_id[src0]].slope = d->act_slope;
         new_id[i] = new_id[src0];
         continue;
       }
@@ -455,12 +477,17 @@ int cbo_net_create(const cbg_network_spec* spec, const float* taus, int n_taus,
         nd->tau = taus[conv_idx];
         nd->policy = pol;
         nd->relu = d->fuse_relu != 0;
+        nd->slope = d->act_slope;
+        if (!(nd->slope >= 0.0f)) BAIL(CBG_ERR_INVALID_INPUT, "layer %d: act slope must be >= 0", i);
         if (pol == CBG_POLICY_DETECT) nd->state = calloc(tsize(nd->ic, nd->ih, nd->iw), sizeof(float));
         ++conv_idx;
       } else if (d->kind == CBG_LAYER_POOL) {
         if (nd->in[0] < 0) BAIL(CBG_ERR_CONFIG, "layer %d: change-based pooling needs an upstream layer", i);
         nd->psize = d->pool_size;
         nd->pstride = d->pool_stride;
+      } else if (d->kind == CBG_LAYER_UPSAMPLE) {
+        if (nd->in[0] < 0) BAIL(CBG_ERR_CONFIG, "layer %d: change-based upsampling needs an upstream layer", i);
+        nd->up = d->upsample;
       } else {
         for (int k = 0; k < nd->n_in; ++k)
           if (nd->in[k] < 0) BAIL(CBG_ERR_CONFIG, "layer %d: change-based joins need upstream layers, not the input", i);
@@ -532,7 +559,8 @@ static int conv_forward(cbo_net* net, onode* nd, const float* x, const onode* up
       float acc = 0.0f;
       for (size_t r = 0; r < rows; ++r) acc += kr[r] * col[r];
       float v = acc + s->bias[o];
-      if (nd->relu) v = (v < 0.0f) ? 0.0f : v;
+      /* ReLU as std::max(v, 0.f) (the reference); EXTENSION: leaky ReLU v * slope */
+      if (nd->relu) v = (v < 0.0f) ? (nd->slope != 0.0f ? v * nd->slope : 0.0f) : v;
       nd->prev[(size_t)o * HWo + (size_t)jo * nd->ow + io] = v;
     }
   }
@@ -564,6 +592,20 @@ int cbo_net_forward(cbo_net* net, const float* frame) {
         for (int c = 0; c < nd->oc; ++c)
           nd->prev[(size_t)c * HWo + (size_t)jo * nd->ow + io] =
               window_max(up->prev + (size_t)c * nd->ih * nd->iw, nd->ih, nd->iw, jo * nd->pstride, io * nd->pstride, nd->psize);
+      }
+    } else if (nd->kind == CBG_LAYER_UPSAMPLE) {
+      /* EXTENSION (no reference counterpart): an output pixel is dirty when
+       * its source pixel (j/up, i/up) is; dirty pixels copy the source vector */
+      const onode* up = &net->nodes[nd->in[0]];
+      for (int j = 0; j < nd->oh; ++j)
+        for (int i2 = 0; i2 < nd->ow; ++i2)
+          nd->map[(size_t)j * nd->ow + i2] = boot ? 1 : up->map[(size_t)(j / nd->up) * nd->iw + i2 / nd->up];
+      cbo_extract_indexes(nd->map, nd->oh, nd->ow, nd->idx, &nd->nidx);
+      for (int64_t k = 0; k < nd->nidx; ++k) {
+        const int jo = nd->idx[2 * k], io = nd->idx[2 * k + 1];
+        for (int c = 0; c < nd->oc; ++c)
+          nd->prev[(size_t)c * HWo + (size_t)jo * nd->ow + io] =
+              up->prev[((size_t)c * nd->ih + jo / nd->up) * nd->iw + io / nd->up];
       }
     } else { /* Add / Concat, network.cpp:364-398 */
       if (boot) memset(nd->map, 1, HWo);

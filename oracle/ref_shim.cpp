@@ -73,6 +73,8 @@ NetworkSpec to_network(const cbg_network_spec& n) {
   spec.in_width = n.in_width;
   for (int i = 0; i < n.n_layers; ++i) {
     const cbg_layer_desc& d = n.layers[i];
+    if (d.kind == CBG_LAYER_UPSAMPLE || d.act_slope != 0.0f)
+      throw ConfigError("the reference has no upsample layer and no leaky ReLU (network.hpp:10)");
     LayerDesc l;
     l.kind = static_cast<LayerKind>(d.kind);
     l.name = d.name ? d.name : "";

@@ -17,7 +17,7 @@ LIB_PATH = os.path.join(_HERE, os.environ.get("CBG_LIB", "libcbg.so"))
 
 # ---- status codes / enums (include/cbg.h) -----------------------------------
 OK, ERR_INVALID_INPUT, ERR_CONFIG, ERR_CUDA, ERR_OOM, ERR_UNSUPPORTED = range(6)
-LAYER_CONV, LAYER_ACT, LAYER_POOL, LAYER_ADD, LAYER_CONCAT = range(5)
+LAYER_CONV, LAYER_ACT, LAYER_POOL, LAYER_ADD, LAYER_CONCAT, LAYER_UPSAMPLE = range(6)
 POLICY_DETECT, POLICY_PROPAGATE, POLICY_REUSE1X1 = range(3)
 MODE_FEEDFORWARD, MODE_CLOSEDLOOP = range(2)
 FWD_FORCE_FULL = 1
@@ -43,6 +43,7 @@ class LayerDescC(C.Structure):
         ("conv", ConvSpecC), ("fuse_relu", C.c_int),
         ("pool_size", C.c_int), ("pool_stride", C.c_int),
         ("pool_out_h", C.c_int), ("pool_out_w", C.c_int),
+        ("act_slope", C.c_float), ("upsample", C.c_int),
     ]
 
 

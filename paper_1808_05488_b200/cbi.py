@@ -31,7 +31,7 @@ __all__ = [
     "LayerFrameStats", "FrameStats", "RunStats", "SequenceResult", "Context", "CBConvLayer",
     "CBPoolLayer", "CBNetwork", "convert_to_cb", "validate_network", "forward_sequence", "write_stats_csv",
     "loss_value", "select_thresholds", "sweep_threshold_factor",
-    "gen_synthetic", "fill_random_weights", "make_seg7_spec", "make_seg_spec", "make_small_spec",
+    "gen_synthetic", "fill_random_weights", "make_seg7_spec", "make_seg_spec", "make_small_spec", "make_yolov3_spec",
     "InvalidInputError", "ConfigError", "device_available",
 ]
 
@@ -42,6 +42,7 @@ class LayerKind(enum.IntEnum):  # network.hpp:10
     Pool = _lib.LAYER_POOL
     Add = _lib.LAYER_ADD
     Concat = _lib.LAYER_CONCAT
+    Upsample = _lib.LAYER_UPSAMPLE  # extension: not in the reference
 
 
 class DetectionPolicy(enum.IntEnum):  # layers.hpp:8
@@ -121,6 +122,8 @@ class LayerDesc:
     pool_stride: int = 0
     pool_out_h: int = 0
     pool_out_w: int = 0
+    act_slope: float = 0.0  # extension: leaky ReLU slope of an Act row / a conv's fused act (0 = ReLU)
+    upsample: int = 0       # extension: Upsample rows' factor
 
 
 @dataclass
@@ -141,7 +144,8 @@ class NetworkSpec:
             keep += [names, from_arr, name]
             conv = d.conv._c(keep) if d.kind == LayerKind.Conv else _lib.ConvSpecC()
             arr[i] = _lib.LayerDescC(int(d.kind), name, len(names), from_arr, conv, int(bool(d.fuse_relu)),
-                                     d.pool_size, d.pool_stride, d.pool_out_h, d.pool_out_w)
+                                     d.pool_size, d.pool_stride, d.pool_out_h, d.pool_out_w,
+                                     float(d.act_slope), int(d.upsample))
         keep.append(arr)
         return _lib.NetworkSpecC(self.in_channels, self.in_height, self.in_width, len(self.layers), arr)
 
@@ -306,8 +310,9 @@ def fill_random_weights(spec: NetworkSpec, seed: int) -> None:
     check(lib.cbg_fill_random_weights(C.byref(cspec), seed, W, B))
 
 
-def _conv(name, cin, cout, k, pad, relu, oh=0, ow=0, stride=1):
-    return LayerDesc(LayerKind.Conv, name, [], ConvSpec(cin, cout, k, k, stride, pad, oh, ow), relu)
+def _conv(name, cin, cout, k, pad, relu, oh=0, ow=0, stride=1, slope=0.0, from_=None):
+    return LayerDesc(LayerKind.Conv, name, list(from_ or []), ConvSpec(cin, cout, k, k, stride, pad, oh, ow), relu,
+                     act_slope=slope)
 
 
 def _act(name):
@@ -414,6 +419,48 @@ def make_yolo_spec(seed: int, height: int = 1080, width: int = 1920, width_div: 
     L.append(_conv("conv7", ch(512), ch(1024), 3, 1, True))
     L.append(_conv("conv8", ch(1024), ch(1024), 3, 1, True))
     L.append(_conv("head", ch(1024), 125, 1, 0, False))
+    spec = NetworkSpec(3, height, width, L)
+    fill_random_weights(spec, seed)
+    return spec
+
+
+def make_yolov3_spec(seed: int, height: int = 1080, width: int = 1920, width_div: int = 1,
+                     slope: float = 0.1) -> NetworkSpec:
+    """YOLOv3-style two-scale detector (BASELINE configs[3], the tiny-YOLOv3 layer
+    graph): 3x3 convs 16..1024 with leaky ReLU (slope 0.1) and 2x2 / stride-2
+    max-pools, a 1/32 head, and a route back from the 1x1 bottleneck through a
+    1x1 conv and a x2 nearest upsampling, concatenated with the 1/16 features,
+    to a second head; heads are linear 1x1 convs of 3 anchors x (5 + 80 classes).
+    Leaky ReLU and upsampling are extensions (the reference has neither,
+    network.hpp:10): they are checked against oracle/cbi_oracle.c only. Pools are
+    ceil-mode (pinned output dims) and the upsampling is cropped to the 1/16
+    dims, so the route meets them at any input size (1920x1080: 68x120).
+    Widths are divided by ``width_div`` (heads kept)."""
+    def ch(c):
+        return max(4, c // width_div)
+
+    def up2(x):
+        return (x + 1) // 2
+
+    L = []
+    c, h, w = 3, height, width
+    for i, cout in enumerate((16, 32, 64, 128, 256)):
+        L.append(_conv(f"conv{i + 1}", c, ch(cout), 3, 1, True, slope=slope))
+        if i == 4:
+            h16, w16 = h, w  # conv5's dims: the route's partner
+        h, w = up2(h), up2(w)
+        L.append(_pool(f"pool{i + 1}", h, w))
+        c = ch(cout)
+    L.append(_conv("conv6", c, ch(512), 3, 1, True, slope=slope))
+    L.append(_conv("conv7", ch(512), ch(1024), 3, 1, True, slope=slope))
+    L.append(_conv("conv8", ch(1024), ch(256), 1, 0, True, slope=slope))
+    L.append(_conv("conv9", ch(256), ch(512), 3, 1, True, slope=slope))
+    L.append(_conv("head1", ch(512), 255, 1, 0, False))
+    L.append(_conv("conv10", ch(256), ch(128), 1, 0, True, slope=slope, from_=["conv8"]))
+    L.append(LayerDesc(LayerKind.Upsample, "up", upsample=2, pool_out_h=h16, pool_out_w=w16))
+    L.append(LayerDesc(LayerKind.Concat, "route", ["up", "conv5"]))
+    L.append(_conv("conv11", ch(128) + ch(256), ch(256), 3, 1, True, slope=slope))
+    L.append(_conv("head2", ch(256), 255, 1, 0, False))
     spec = NetworkSpec(3, height, width, L)
     fill_random_weights(spec, seed)
     return spec

@@ -766,6 +766,22 @@ __global__ void __launch_bounds__(512) dilate_compact_kernel(DilateCompactArgs a
       const int rr = i / nwo, wo = i - rr * nwo;
       if (boot) {
         v = row_mask(a.Wout, wo);
+      } else if (a.up > 1) {  // nearest upsampling: out (jo, io) <- in (jo / up, io / up)
+        const uint32_t* row = in_s + static_cast<long long>((r0 + rr) / a.up) * nwi;
+        if (a.up == 2) {  // the 16 source bits of the word, each doubled
+          uint32_t x = (__ldg(row + (wo >> 1)) >> (16 * (wo & 1))) & 0xFFFFu;
+          x = (x | (x << 8)) & 0x00FF00FFu;
+          x = (x | (x << 4)) & 0x0F0F0F0Fu;
+          x = (x | (x << 2)) & 0x33333333u;
+          x = (x | (x << 1)) & 0x55555555u;
+          v = x | (x << 1);
+        } else {
+          for (int b = 0; b < 32; ++b) {
+            const int c = (wo * 32 + b) / a.up;
+            if (c < a.Win) v |= ((__ldg(row + (c >> 5)) >> (c & 31)) & 1u) << b;
+          }
+        }
+        v &= row_mask(a.Wout, wo);
       } else if (ident) {
         const long long off = in_off + static_cast<long long>(r0 + rr) * nwi + wo;
         for (int q = 0; q < a.n_in; ++q) v |= __ldg(a.in_map[q] + off);
@@ -911,6 +927,31 @@ __global__ void __launch_bounds__(kFrameThreads) pool_kernel(PoolArgs a, int glo
         }
       *reinterpret_cast<float4*>(y + static_cast<long long>(p) * a.Cs + 4 * v) = m;
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// nearest upsampling at listed output pixels (extension): out(j, i) = in(j/f, i/f)
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(kFrameThreads) upsample_kernel(PoolArgs a, int glog) {
+  const int s = blockIdx.y;
+  const long long n = a.count[s * a.cnt_stride];
+  const long long HWi = static_cast<long long>(a.Hin) * a.Win;
+  const long long HWo = static_cast<long long>(a.Hout) * a.Wout;
+  const float* x = a.x + s * HWi * a.Cs;
+  float* y = a.out + s * HWo * a.Cs;
+  const int32_t* list = a.idx + s * HWo;
+  const int g = 1 << glog;
+  const int sub = threadIdx.x & (g - 1);
+  const long long gid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> glog;
+  const long long gstride = (static_cast<long long>(gridDim.x) * blockDim.x) >> glog;
+  const int nv = a.Cs >> 2;
+  for (long long k = gid; k < n; k += gstride) {
+    const int p = list[k];
+    const int jo = p / a.Wout, io = p - jo * a.Wout;
+    const float* src = x + (static_cast<long long>(jo / a.stride) * a.Win + io / a.stride) * a.Cs;
+    for (int v = sub; v < nv; v += g)
+      *reinterpret_cast<float4*>(y + static_cast<long long>(p) * a.Cs + 4 * v) = ldg_nc_f4(src + 4 * v);
   }
 }
 
@@ -1110,6 +1151,13 @@ void launch_pool(const PoolArgs& a, cudaStream_t st) {
   const long long HWo = static_cast<long long>(a.Hout) * a.Wout;
   dim3 grid(2 * blocks_for(HWo, kThreads >> glog, a.S, sm_count()), a.S);
   pool_kernel<<<grid, kFrameThreads, 0, st>>>(a, glog);
+}
+
+void launch_upsample(const PoolArgs& a, cudaStream_t st) {
+  const int glog = group_log2(a.Cs);
+  const long long HWo = static_cast<long long>(a.Hout) * a.Wout;
+  dim3 grid(2 * blocks_for(HWo, kThreads >> glog, a.S, sm_count()), a.S);
+  upsample_kernel<<<grid, kFrameThreads, 0, st>>>(a, glog);
 }
 
 void launch_join(const JoinArgs& a, cudaStream_t st) {

@@ -259,7 +259,7 @@ __global__ void __maxnreg__(88) conv_exact_kernel(ConvExactArgs a) {  // launche
             float alo, ahi;
             f2_unpack(acc[u][2 * q + (e >> 1)], alo, ahi);
             float y = __fadd_rn((e & 1) ? ahi : alo, o + e < a.Cout ? __ldg(a.bias + o + e) : 0.0f);
-            if (a.relu) y = (y < 0.0f) ? 0.0f : y;  // std::max(v, 0.f)
+            if (a.relu) y = (y < 0.0f) ? (a.slope != 0.0f ? y * a.slope : 0.0f) : y;  // std::max(v, 0.f) / leaky
             v[e] = o + e < a.Cout ? y : 0.0f;
             vmax = fmaxf(vmax, fabsf(v[e]));
           }

@@ -589,7 +589,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
             // rounds once, like the reference's y + b
             if constexpr (is_f16(PREC)) y = fmaf(y * ys, ws, (&b.x)[u]);
             else y = y + (&b.x)[u];
-            if (a.relu) y = (y < 0.0f) ? 0.0f : y;  // std::max(v, 0.f)
+            if (a.relu) y = (y < 0.0f) ? (a.slope != 0.0f ? y * a.slope : 0.0f) : y;  // std::max(v, 0.f) / leaky
             o[u] = y;
             vmax = fmaxf(vmax, fabsf(y));
           }

@@ -96,6 +96,7 @@ struct DilateCompactArgs {
   int cnt_stride;
   const uint8_t* boot;
   int Hin, Win, Hout, Wout, kh, kw, stride, pad;
+  int up;                     // > 1: nearest upsampling map (out (j, i) <- in (j/up, i/up)) instead of a window
   int rows;                   // output rows per band (even): one CTA
   int n_bands;                // bands per stream
   int S;
@@ -122,6 +123,8 @@ struct PoolArgs {
   int cnt_stride;
 };
 void launch_pool(const PoolArgs& a, cudaStream_t st);
+// Nearest upsampling at the node's index list (extension; PoolArgs with stride = the factor).
+void launch_upsample(const PoolArgs& a, cudaStream_t st);
 
 // Add / Concat joins at the join's index list (reference network.cpp:364-398).
 struct JoinArgs {
@@ -159,6 +162,7 @@ struct ConvGemmArgs {
   int npad;                // N tile: 16, 32, 64, 128 or 256
   int n_tiles;             // ceil(Co4 / npad)
   int relu;
+  float slope;             // relu: 0 = ReLU (std::max(v, 0.f)), > 0 = leaky ReLU v * slope (extension)
   int S;
   int grid;                // persistent CTAs (<= SM count)
   int prec;                // 0: 3xTF32, 1: 3xFP16 with power-of-two scaling (conv_tcgen05.cu)
@@ -186,6 +190,7 @@ struct ConvExactArgs {
   int Cin, Cout, Co4, kh, kw, stride, pad;
   int Hin, Win, Hout, Wout;
   int relu;
+  float slope;             // as ConvGemmArgs::slope
   int S;
   int sm_count;
   float* amax_out;         // [S] running max |written value|

@@ -148,8 +148,20 @@ Topology convert(const cbg_network_spec& spec, const float* taus, int n_taus, co
         }
         case CBG_LAYER_ACT:
           if (in.size() != 1) throw_invalid("act takes exactly one producer");
+          if (!(d.act_slope >= 0.0f) || !std::isfinite(d.act_slope)) throw_invalid("act slope must be >= 0");
           shape[i] = shape_of(in[0]);
           break;
+        case CBG_LAYER_UPSAMPLE: {  // extension: nearest-neighbour, integer factor
+          if (in.size() != 1) throw_invalid("upsample takes exactly one producer");
+          if (d.upsample < 1 || d.upsample > 64) throw_invalid("upsample factor must be in [1, 64]");
+          const Shape s = shape_of(in[0]);
+          // pool_out_h / pool_out_w > 0: cropped output dims (<= in * factor)
+          if (d.pool_out_h < 0 || d.pool_out_w < 0 || d.pool_out_h > s.h * d.upsample || d.pool_out_w > s.w * d.upsample)
+            throw_invalid("upsample output dims out of range");
+          shape[i] = {s.c, d.pool_out_h > 0 ? d.pool_out_h : s.h * d.upsample,
+                      d.pool_out_w > 0 ? d.pool_out_w : s.w * d.upsample};
+          break;
+        }
         case CBG_LAYER_POOL: {
           if (in.size() != 1) throw_invalid("pool takes exactly one producer");
           if (d.pool_size < 1 || d.pool_stride < 1) throw_invalid("pool size/stride must be >= 1");
@@ -220,6 +232,7 @@ Topology convert(const cbg_network_spec& spec, const float* taus, int n_taus, co
         throw_config(where + ": standalone activation can only be absorbed into a conv");
       if (consumers[src] != 1) throw_config(where + ": cannot absorb activation, conv output has other consumers");
       topo.nodes[new_id[src]].relu = true;
+      topo.nodes[new_id[src]].slope = d.act_slope;
       new_id[i] = new_id[src];
       continue;
     }
@@ -242,6 +255,8 @@ Topology convert(const cbg_network_spec& spec, const float* taus, int n_taus, co
       nd.tau = taus[conv_idx];
       nd.policy = policy;
       nd.relu = d.fuse_relu != 0;
+      nd.slope = d.act_slope;
+      if (!(nd.slope >= 0.0f) || !std::isfinite(nd.slope)) throw_invalid(where + ": act slope must be >= 0");
       if (policy == CBG_POLICY_REUSE1X1 &&
           !(nd.conv.kernel_h == 1 && nd.conv.kernel_w == 1 && nd.conv.stride == 1 && nd.H == nd.Hi && nd.W == nd.Wi))
         throw_config(where + ": reuse_1x1 policy requires a 1x1 stride-1 shape-preserving layer");
@@ -250,6 +265,9 @@ Topology convert(const cbg_network_spec& spec, const float* taus, int n_taus, co
       if (nd.inputs[0] < 0) throw_config(where + ": change-based pooling needs an upstream layer");
       nd.pool_size = d.pool_size;
       nd.pool_stride = d.pool_stride;
+    } else if (d.kind == CBG_LAYER_UPSAMPLE) {
+      if (nd.inputs[0] < 0) throw_config(where + ": change-based upsampling needs an upstream layer");
+      nd.up = d.upsample;
     } else {
       for (int id : nd.inputs)
         if (id < 0) throw_config(where + ": change-based joins need upstream layers, not the input");
@@ -642,6 +660,9 @@ void Net::build() {
       } else {
         r.dc = dc_geometry(d.Hi, d.Wi, d.H, d.W, d.pool_size, d.pool_size, d.pool_stride, 0, S_);
       }
+    } else if (d.kind == CBG_LAYER_UPSAMPLE) {
+      r.dc = dc_geometry(d.Hi, d.Wi, d.H, d.W, 1, 1, 1, 0, S_);
+      r.dc.up = d.up;
     } else {  // joins: OR of the parents' maps, 1x1 identity window
       r.dc = dc_geometry(d.H, d.W, d.H, d.W, 1, 1, 1, 0, S_);
     }
@@ -690,7 +711,8 @@ void Net::build() {
 }
 
 int Net::amax_origin(int node) const {
-  while (node >= 0 && nodes_[node].d.kind == CBG_LAYER_POOL) node = nodes_[node].d.inputs[0];
+  while (node >= 0 && (nodes_[node].d.kind == CBG_LAYER_POOL || nodes_[node].d.kind == CBG_LAYER_UPSAMPLE))
+    node = nodes_[node].d.inputs[0];
   return node;  // -1 = network input
 }
 
@@ -851,6 +873,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
         x.kh = c.kernel_h, x.kw = c.kernel_w, x.stride = c.stride, x.pad = c.padding;
         x.Hin = d.Hi, x.Win = d.Wi, x.Hout = d.H, x.Wout = d.W;
         x.relu = d.relu;
+        x.slope = d.slope;
         x.S = S_;
         x.sm_count = ctx_->sm_count;
         x.amax_out = amax_entry(i);
@@ -875,6 +898,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
       g.kh = c.kernel_h, g.kw = c.kernel_w;
       g.KB = r.KB, g.npad = r.npad, g.n_tiles = r.n_tiles;
       g.relu = d.relu;
+      g.slope = d.slope;
       g.S = S_;
       g.grid = ctx_->sm_count;
       g.prec = r.prec;
@@ -890,6 +914,12 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
       PoolArgs pa{prod->out.as<float>(), r.out.as<float>(), r.idx, counts + r.count_slot, r.Cs, d.Hi, d.Wi,
                   d.H, d.W, d.pool_size, d.pool_stride, S_, cnt_stride_};
       timed(d.name + ".pool", [&] { launch_pool(pa, st); });
+    } else if (d.kind == CBG_LAYER_UPSAMPLE) {
+      const uint32_t* in[1] = {prod->outmap};
+      map_compaction(i, compaction(i, in, 1));
+      PoolArgs pa{prod->out.as<float>(), r.out.as<float>(), r.idx, counts + r.count_slot, r.Cs, d.Hi, d.Wi,
+                  d.H, d.W, 0, d.up, S_, cnt_stride_};
+      timed(d.name + ".upsample", [&] { launch_upsample(pa, st); });
     } else {  // Add / Concat
       const uint32_t* in[4] = {};
       for (size_t k = 0; k < d.inputs.size(); ++k) in[k] = nodes_[d.inputs[k]].outmap;

@@ -54,7 +54,9 @@ struct NodeDesc {
   float tau = 0.0f;
   int policy = CBG_POLICY_DETECT;
   bool relu = false;
+  float slope = 0.0f;         // fused activation: 0 = ReLU (the reference), > 0 = leaky ReLU (extension)
   int pool_size = 0, pool_stride = 0;
+  int up = 0;                 // CBG_LAYER_UPSAMPLE factor (extension)
 };
 constexpr int kExternal = -100;
 

@@ -264,6 +264,8 @@ def _row_shapes(spec: cbi.NetworkSpec):
             shp = (c, oh, ow)
         elif d.kind == cbi.LayerKind.Concat:
             shp = (sum(s[0] for s in src), h, w)
+        elif d.kind == cbi.LayerKind.Upsample:
+            shp = (c, d.pool_out_h or h * d.upsample, d.pool_out_w or w * d.upsample)
         else:
             shp = (c, h, w)
         shapes.append(shp)
@@ -458,6 +460,62 @@ def ref_seg_stats_csv(seed, height, width, taus, synth: "cbi.SyntheticConfig", w
 # observed max_rel_err per test (tests/conftest.py writes it to $CBG_PARITY_OUT:
 # the measured maxima behind every tolerance in the GPU tests)
 OBSERVED: dict = {}
+
+
+def dense_forward64(spec: cbi.NetworkSpec, frame):
+    """Float64 dense evaluation of a layer manifest in numpy, an independent
+    formulation (no im2col, no fp32 rounding) used to pin the oracle's EXTENSIONS
+    (leaky ReLU, upsampling) that the reference cannot check. Returns every row's
+    output, Act rows included."""
+    outs = []
+    names = {}
+    x0 = np.asarray(frame, np.float64)
+    for i, d in enumerate(spec.layers):
+        ins = [(-1 if s == "input" else names[s]) for s in d.from_] if d.from_ else [i - 1]
+        src = [x0 if j < 0 else outs[j] for j in ins]
+        x = src[0]
+        if d.kind == cbi.LayerKind.Conv:
+            cv = d.conv
+            c, h, w = x.shape
+            oh, ow = cv.output_height(h), cv.output_width(w)
+            xp = np.zeros((c, h + 2 * cv.padding + cv.kernel_h, w + 2 * cv.padding + cv.kernel_w))
+            xp[:, cv.padding:cv.padding + h, cv.padding:cv.padding + w] = x
+            wt = np.asarray(cv.weights, np.float64).reshape(cv.out_channels, c, cv.kernel_h, cv.kernel_w)
+            y = np.zeros((cv.out_channels, oh, ow))
+            for kj in range(cv.kernel_h):
+                for ki in range(cv.kernel_w):
+                    patch = xp[:, kj:kj + (oh - 1) * cv.stride + 1:cv.stride, ki:ki + (ow - 1) * cv.stride + 1:cv.stride]
+                    y += np.einsum("oc,chw->ohw", wt[:, :, kj, ki], patch)
+            y += np.asarray(cv.bias, np.float64)[:, None, None]
+            if d.fuse_relu:
+                y = np.where(y < 0, y * d.act_slope, y)
+        elif d.kind == cbi.LayerKind.Act:
+            y = np.where(x < 0, x * d.act_slope, x)
+        elif d.kind == cbi.LayerKind.Pool:
+            c, h, w = x.shape
+            oh = d.pool_out_h if d.pool_out_h > 0 else (h - d.pool_size) // d.pool_stride + 1
+            ow = d.pool_out_w if d.pool_out_w > 0 else (w - d.pool_size) // d.pool_stride + 1
+            y = np.full((c, oh, ow), -np.inf)
+            for kj in range(d.pool_size):
+                for ki in range(d.pool_size):
+                    for jo in range(oh):
+                        j = jo * d.pool_stride + kj
+                        if j >= h:
+                            continue
+                        cols = np.arange(ow) * d.pool_stride + ki
+                        ok = cols < w
+                        y[:, jo, ok] = np.maximum(y[:, jo, ok], x[:, j, cols[ok]])
+        elif d.kind == cbi.LayerKind.Upsample:
+            y = x.repeat(d.upsample, axis=1).repeat(d.upsample, axis=2)
+            y = y[:, :d.pool_out_h or y.shape[1], :d.pool_out_w or y.shape[2]]
+        elif d.kind == cbi.LayerKind.Concat:
+            y = np.concatenate(src, axis=0)
+        else:  # Add
+            y = sum(src)
+        outs.append(y)
+        if d.name:
+            names[d.name] = i
+    return outs
 
 
 def max_rel_err(a, b) -> float:

@@ -387,3 +387,38 @@ def test_output_delta_mirror_equals_full_output(gpu):
     net.apply_output_delta(bufs[pending % 2].ptr, mirror.ctypes.data, streams=(0, 2))
     net.apply_output_delta(bufs[pending % 2].ptr, mirror.ctypes.data, streams=(2, 3))
     np.testing.assert_array_equal(mirror, want)
+
+
+@pytest.mark.parametrize("h,w,wd", [(1080, 1920, 8), (270, 480, 1)])
+def test_yolov3_leaky_upsample_against_port(gpu, h, w, wd):
+    """BASELINE configs[3] with the features the reference lacks (network.hpp:10,
+    PAPER.md:647): the tiny-YOLOv3 graph — leaky ReLU (slope 0.1) on every conv,
+    a x2 nearest upsampling concatenated with the 1/16 features, two heads —
+    checked against the C restatement's extension (oracle/cbi_oracle.c; parity
+    unpinned against the reference itself, which cannot run it). Full frame at
+    channels / 8, and full width at quarter resolution. conv1 (Cout <= 16) runs
+    the CUDA-core path: its leaky output is bit-exact; every map agrees."""
+    spec = cbi.make_yolov3_spec(9, h, w, width_div=wd)
+    n_conv = sum(1 for d in spec.layers if d.kind == cbi.LayerKind.Conv)
+    taus = [0.03] * n_conv
+    net = cbi.convert_to_cb(spec, taus)
+    ref = oracle.PortNet(spec, taus)
+    raw = cbi.gen_synthetic(cbi.SyntheticConfig(h, w, 3, 4, 3, 48, 4, 6, 0.002, 77))
+    frames = cbi.from_pnm8(cbi.to_pnm8(raw))
+    names = [n.name for n in net.nodes()]
+    assert "up" in names and any(n.kind == cbi.LayerKind.Upsample for n in net.nodes())
+    for t, f in enumerate(frames):
+        got = net.forward_frame(f)
+        want = ref.forward(f)
+        assert np.array_equal(net.node_output(0), ref.output(0)), f"frame {t}: conv1 (leaky) not bit-exact"
+        gm, gi = net.node_changes(0)
+        wm, wi = ref.changes(0)
+        assert np.array_equal(gm, wm) and np.array_equal(gi, wi), f"frame {t}: layer-1 map / list"
+        up = names.index("up")
+        assert np.array_equal(net.node_output(up), ref.output(up)) or \
+            oracle.max_rel_err(net.node_output(up), ref.output(up)) <= 3e-4, t
+        for i, nm in enumerate(names):
+            assert float(np.mean(net.node_changes(i)[0] == ref.changes(i)[0])) >= 0.999, (t, nm)
+            assert oracle.max_rel_err(net.node_output(i), ref.output(i)) <= 3e-4, (t, nm)
+        assert oracle.max_rel_err(got, want) <= 3e-4, t
+    assert len(net.node_changes(names.index("up"))[1]) > 0

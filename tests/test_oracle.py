@@ -255,3 +255,62 @@ def test_golden_sequence_fixture_matches_port():
         _, idx = q.changes(0)
         n = int(z["l1_count"][t])
         assert np.array_equal(idx, z["l1_idx"][t, :n])
+
+
+# ---------------------------------------------------------------------------
+# EXTENSIONS beyond the reference (leaky ReLU, upsampling): parity unpinned
+# against the reference, so the C restatement is checked against an
+# independent float64 numpy formulation instead (tests/oracle.py dense_forward64)
+# ---------------------------------------------------------------------------
+def test_reference_rejects_the_extensions():
+    spec = cbi.make_yolov3_spec(3, 64, 96, width_div=16)
+    with pytest.raises(cbi.ConfigError):
+        oracle.RefNet(spec, [0.0] * 13)
+
+
+@pytest.mark.parametrize("seed", [1, 2])
+def test_extensions_port_matches_float64_dense(seed):
+    """YOLOv3-style graph (leaky convs, ceil pools, x2 upsample + concat route)
+    at tau = 0: every frame the CB restatement equals the float64 dense net
+    (acceptance C1's property), and its change maps cover every pixel whose
+    dense output moved."""
+    rng = np.random.default_rng(seed)
+    spec = cbi.make_yolov3_spec(seed, 72, 104, width_div=16)
+    net = oracle.PortNet(spec, [0.0] * 13)
+    rows = {d.name: i for i, d in enumerate(spec.layers)}
+    x = rng.uniform(0, 1, (3, 72, 104)).astype(np.float32)
+    prev = None
+    for t in range(4):
+        net.forward(x)
+        dense = oracle.dense_forward64(spec, x)
+        for node, name in enumerate(n for n in (d.name for d in spec.layers)):
+            want = dense[rows[name]]
+            got = net.output(node)
+            assert got.shape == want.shape, name
+            err = np.abs(got - want).max() / max(1e-30, np.abs(want).max())
+            assert err < 2e-5, (t, name, err)
+        if prev is not None:  # changed output pixels are marked (tau = 0: exactly the moved ones or more)
+            node = [d.name for d in spec.layers].index("up")
+            m, _ = net.changes(node)
+            moved = np.any(dense[rows["up"]] != prev[rows["up"]], axis=0)
+            assert not np.any(moved & (m == 0))
+        prev = dense
+        x = x.copy()
+        j, i = rng.integers(0, 60), rng.integers(0, 90)
+        x[:, j:j + 9, i:i + 11] = rng.uniform(0, 1, (3, 9, 11)).astype(np.float32)
+
+
+def test_leaky_slope_on_a_single_conv():
+    """fused leaky ReLU: v < 0 ? v * slope : v with one fp32 rounding (Darknet's leaky)"""
+    rng = np.random.default_rng(5)
+    cs = cbi.ConvSpec(4, 6, 3, 3, 1, 1, 0, 0, rng.normal(0, 1, 6 * 4 * 9).astype(np.float32),
+                      rng.normal(0, 1, 6).astype(np.float32))
+    spec = cbi.NetworkSpec(4, 10, 12, [cbi.LayerDesc(cbi.LayerKind.Conv, "c", [], cs, False),
+                                       cbi.LayerDesc(cbi.LayerKind.Act, "a", act_slope=0.1)])
+    lin = cbi.NetworkSpec(4, 10, 12, [cbi.LayerDesc(cbi.LayerKind.Conv, "c", [], cs, False)])
+    x = rng.uniform(-1, 1, (4, 10, 12)).astype(np.float32)
+    a, b = oracle.PortNet(spec, [0.0]), oracle.PortNet(lin, [0.0])
+    ya, yb = a.forward(x), b.forward(x)
+    want = np.where(yb < 0, yb * np.float32(0.1), yb).astype(np.float32)
+    assert np.array_equal(ya, want)
+    assert np.any(yb < 0)

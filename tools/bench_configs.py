@@ -12,8 +12,11 @@ gen_synthetic sequences played ping-pong (as in bench.py).
         reference's CPU-runnable case; 1024 streams per launch)
   cfg3  OpenPose-style pose net (make_openpose_spec, full width, 2 stages) at
         368x368, one moving subject
-  cfg4  tiny-YOLO-style detector (make_yolo_spec, full width) at 1920x1080,
-        change-rate sweep
+  cfg4  tiny-YOLO-style detector (make_yolo_spec, full width, ReLU) at 1920x1080,
+        change-rate sweep 0.1-100%
+  cfg4v3  tiny-YOLOv3-style detector (make_yolov3_spec: leaky ReLU, x2 upsample +
+        concat route, two heads; the extensions the reference lacks) at
+        1920x1080, change-rate sweep 0.1-100%
   cfg5  scene-labeling net at 1920x1080, 64 streams on one GPU (the N=1 point
         of the 64-stream scaling config)
 """
@@ -82,7 +85,7 @@ def measure(name, spec, taus, dev, steps, warmup, extra):
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="cfg1,cfg3,cfg4,cfg5")
+    ap.add_argument("--only", default="cfg1,cfg3,cfg4,cfg4v3,cfg5")
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     a = ap.parse_args()
@@ -117,13 +120,23 @@ def main():
                 {"synthetic": "1 moving subject (96 px, v=4)"})
         del dev
 
-    if "cfg4" in want:
-        spec = cbi.make_yolo_spec(1, 1080, 1920)
+    for key, make, label in (("cfg4", cbi.make_yolo_spec, "cfg4 tiny-YOLO-style detector, 1920x1080"),
+                             ("cfg4v3", cbi.make_yolov3_spec,
+                              "cfg4 tiny-YOLOv3-style detector (leaky ReLU, upsample route), 1920x1080")):
+        if key not in want:
+            continue
+        spec = make(1, 1080, 1920)
         n = sum(1 for d in spec.layers if d.kind == cbi.LayerKind.Conv)
-        for objects, size, noise in ((1, 16, 0.0), (4, 32, 0.0), (12, 64, 0.0), (40, 96, 0.0), (120, 128, 0.0)):
-            dev = frames_for(8, 1080, 1920, 5, objects, size, 4, noise)
-            measure("cfg4 tiny-YOLO-style detector, 1920x1080", spec, [0.05] * n, dev, a.steps, a.warmup,
-                    {"synthetic": f"{objects} objects x {size} px, v=4"})
+        for pt in ((1, 16), (4, 32), (12, 64), (40, 96), (120, 128), "noise"):
+            if pt == "noise":  # every pixel changes every frame: the change-based path's worst case
+                gen = torch.Generator(device="cuda").manual_seed(99)
+                dev = torch.randint(0, 256, (5, 8, 3, 1080, 1920), generator=gen, device="cuda",
+                                    dtype=torch.uint8).float() / 255.0
+                syn = "uniform noise every frame"
+            else:
+                dev = frames_for(8, 1080, 1920, 5, pt[0], pt[1], 4, 0.0)
+                syn = f"{pt[0]} objects x {pt[1]} px, v=4"
+            measure(label, spec, [0.05] * n, dev, a.steps, a.warmup, {"synthetic": syn})
             del dev
             torch.cuda.empty_cache()
 
