@@ -174,6 +174,28 @@ CBG_DEV void umma_f16x3_kblock_ts(uint32_t d_tmem, uint32_t a_hi, uint32_t a_lo,
       "r"(a_hi), "r"(a_lo), "l"(b_hi), "l"(b_lo), "r"(idesc), "r"(accumulate)
       : "memory");
 }
+// The same product with the two correction terms in their own accumulator
+// (N <= 128): one MMA of width 2N takes A_hi against [B_hi; B_lo] (the weight
+// image's hi and lo rows are contiguous), filling [main | corr], and one of
+// width N adds A_lo * B_hi into corr. 4 MMA instructions per K-block instead
+// of 6 (same tensor time), and the truncating fp32 accumulation of the
+// hi*hi main sum no longer absorbs the small terms (the epilogue adds the two
+// accumulators once, in fp32).
+CBG_DEV void umma_f16x3p_kblock_ts(uint32_t d_tmem, uint32_t d_corr, uint32_t a_hi, uint32_t a_lo, uint64_t b_hi,
+                                   uint32_t idesc2, uint32_t idesc1, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred e, p;\n\t.reg .b32 ah, al;\n\t.reg .b64 bh;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %7, 0;\n\t"
+      "mov.b32 ah, %2;\n\tmov.b32 al, %3;\n\tmov.b64 bh, %4;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, p;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [al], bh, %6, 1;\n\t"
+      "add.u32 ah, ah, 8;\n\tadd.u32 al, al, 8;\n\tadd.s64 bh, bh, 2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ah], bh, %5, 1;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%1], [al], bh, %6, 1;\n\t}" ::"r"(d_tmem),
+      "r"(d_corr), "r"(a_hi), "r"(a_lo), "l"(b_hi), "r"(idesc2), "r"(idesc1), "r"(accumulate)
+      : "memory");
+}
 // 32 lanes x 32 bit, 8 consecutive columns per thread.
 CBG_DEV void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),

@@ -11,32 +11,36 @@
 // K = kh*kw*Cs ordered (kj, ki, c) so one 16-B chunk of a K-row is one
 // contiguous run of a source pixel's channel vector.
 //
-// Precision: 3xTF32 (x = hi + lo; D += Ahi*Bhi + Ahi*Blo + Alo*Bhi) on
-// tcgen05.mma kind::tf32 with fp32 accumulation in TMEM — near-fp32 accuracy,
-// the same precision on the sparse and the dense (full-update) path.
+// Precision: 3xFP16 by default — x * 2^-e = hi + lo in fp16
+// (11 + 11 significant bits, power-of-two operand scales from running magnitude
+// bounds), D += Ahi*Bhi + Ahi*Blo + Alo*Bhi on tcgen05.mma kind::f16 with fp32
+// accumulation in TMEM; for N <= 64 the two correction terms accumulate in
+// their own TMEM columns (umma_f16x3p_kblock_ts). 3xTF32 (kind::tf32) remains
+// selectable (CBG_GEMM_PREC=tf32). The same precision on the sparse and the
+// dense (full-update) path.
 //
 // Warp roles (672 threads, 1 CTA/SM, persistent over (stream, m-tile, n-tile)):
-//   warps 0-3   epilogue: tcgen05.ld TMEM -> +bias -> ReLU -> scatter (lane = row)
-//   warps 4-11  fetch: gather the A tile (changed pixels' receptive fields) with
-//               16-B cp.async copies (zero-fill for padding taps) straight into
-//               the stage (rows of 128 B, 16-B chunks XOR-swizzled by row so the
-//               convert warps' row reads are conflict-free), completion signalled with
-//               cp.async.mbarrier.arrive.noinc so they never wait on data;
-//               fetch thread 0 also streams the pre-swizzled B (weight) image of
-//               the K-block with a bulk copy on the TMA engine
-//   warps 12-19 convert: thread = row of the tile; read the landed fp32 row from
-//               shared memory, split it into tf32 hi / lo and store both into
-//               TENSOR MEMORY (tcgen05.st), arrive for the MMA. The MMAs take
-//               A from TMEM ("ts" form), so per K-block the tensor core reads
-//               only B from shared memory: the stage traffic was 208 KB per
-//               K-block (N=256) / 136 KB (N=64) with A in smem (raw write + read,
-//               hi/lo write, 3 A reads), above the MMA time at 128 B/clk; it is
-//               128 KB / 56 KB now.
-//   warp 20     TMEM allocator + single-thread tcgen05.mma issuer
-// Pipelines: stages full/empty (producers <-> MMA; a stage = raw A rows and the
-// B hi/lo image in smem + A hi/lo columns in TMEM), TMEM accumulators
-// full/empty (MMA <-> epilogue): two for N <= 128 so tile t's epilogue overlaps
-// tile t+1's MMAs, one for N = 256 (TMEM holds 512 columns).
+//   epilogue (4, or 8 for N = 256): tcgen05.ld TMEM -> undo the operand scales,
+//               +bias -> ReLU / leaky ReLU -> smem transpose -> 128-B stores of
+//               each pixel's Cout vector
+//   direct A path (default): 16 (12 for N = 256) convert warps in groups of 4,
+//               one per TMEM lane quarter, each group owning every G-th K-block:
+//               load the changed pixels' receptive-field chunks from global
+//               memory into registers (already split by the layer's detect:
+//               the pre-split copy), split if needed, tcgen05.st into the
+//               stage's TMEM columns; the group leader streams the K-block's
+//               pre-swizzled weight image (hi | lo) into shared memory with a
+//               bulk copy on the TMA engine. A never touches shared memory.
+//   staged A path (CBG_GEMM_DIRECT=0): 8 fetch warps gather the A rows with
+//               16-B cp.async (zero-fill for padding taps) into swizzled smem
+//               stages, completion on an mbarrier; 8 (4) convert warps split them
+//               into TMEM
+//   warp 20     TMEM allocator + the converged MMA issuer (elect.sync): the MMAs
+//               take A from TMEM ("ts" form) and B from shared memory
+// Pipelines: stages full/empty (producers <-> MMA; a stage = the B hi/lo image
+// in smem + A hi/lo columns in TMEM), TMEM accumulators full/empty (MMA <->
+// epilogue): two for N <= 128 so tile t's epilogue overlaps tile t+1's MMAs,
+// one for N = 256 (TMEM holds 512 columns).
 #include <climits>
 #include <cstdio>
 
@@ -66,6 +70,10 @@ CBG_DEV unsigned long long gtimer() {
 #define CTA_MARK(ev) do { } while (0)
 #define EPI_MARK(ev, t) do { } while (0)
 #define CHUNK_MARK(ev, c) do { } while (0)
+#endif
+
+#ifndef CBG_GEMM_PACK
+#define CBG_GEMM_PACK 1
 #endif
 
 namespace {
@@ -139,9 +147,13 @@ struct Cfg {
                                                  : (NPAD >= 256 ? 2 : NPAD >= 128 ? 4 : 6);
   static_assert(kStages % Roles<NPAD, PREC>::kConvGroups == 0, "stages must be a multiple of the convert groups");
   static constexpr int kNAcc = NPAD >= 256 ? 1 : 2;  // TMEM accumulator buffers
+  // fp16, N <= 64: a separate accumulator for the two correction terms
+  // (umma_f16x3p_kblock_ts), so an accumulator buffer is [main | corr]
+  static constexpr bool kPack = is_f16(PREC) && NPAD <= 64 && CBG_GEMM_PACK;
+  static constexpr int kAccCols = kPack ? 2 * NPAD : NPAD;
   static constexpr uint32_t kTmemCols = 512;
-  static constexpr uint32_t kAColBase = kNAcc * NPAD;  // first A stage column
-  static_assert(kNAcc * NPAD + kStages * kACols <= 512, "TMEM budget");
+  static constexpr uint32_t kAColBase = kNAcc * kAccCols;  // first A stage column
+  static_assert(kNAcc * kAccCols + kStages * kACols <= 512, "TMEM budget");
 };
 
 __host__ __device__ constexpr int tail_bytes(int stages, int KB, int S, int nbias, int npad, bool direct) {
@@ -480,6 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     // The whole warp runs the loop (warp-uniform control flow and operands);
     // elect.sync inside the asm picks the issuing lane.
     constexpr uint32_t idesc = is_f16(PREC) ? umma_idesc_f16(kBM, NPAD) : umma_idesc_tf32(kBM, NPAD);
+    constexpr uint32_t idesc2 = umma_idesc_f16(kBM, 2 * NPAD);  // packed: A_hi x [B_hi; B_lo]
     // stage 0 base; B by offset (K-major, 128-B rows for tf32, 64-B rows for fp16)
     const uint64_t desc0 = is_f16(PREC) ? umma_desc_sw64(smem_u32(smem)) : umma_desc_sw128(smem_u32(smem));
     const uint32_t tbase = __shfl_sync(0xffffffffu, tmem_base, 0);
@@ -491,7 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     for (int w = blockIdx.x; w < total; w += gridDim.x) {
       mbar_wait(&tempty[acc], acc_phase ^ 1);
       tc_fence_after();
-      const uint32_t d = tbase + acc * NPAD;
+      const uint32_t d = tbase + acc * C::kAccCols;
       for (int kb = 0; kb < a.KB; ++kb) {
         mbar_wait(&full[stage], phase);
         TRACE(2, gm);
@@ -501,7 +514,9 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
             desc0 + static_cast<uint64_t>((stage * C::kStageBytes + (is_direct(PREC) ? 0 : kABytes)) >> 4);
         const uint64_t b_lo = b_hi + (C::kBBytes >> 4);
         const uint32_t a_hi = tbase + C::kAColBase + stage * C::kACols;
-        if constexpr (is_f16(PREC))
+        if constexpr (C::kPack)
+          umma_f16x3p_kblock_ts(d, d + NPAD, a_hi, a_hi + C::kALo, b_hi, idesc2, idesc, kb != 0);
+        else if constexpr (is_f16(PREC))
           umma_f16x3_kblock_ts(d, a_hi, a_hi + C::kALo, b_hi, b_lo, idesc, kb != 0);
         else
           umma_tf32x3_kblock_ts(d, a_hi, a_hi + C::kALo, b_hi, b_lo, idesc, kb != 0);
@@ -526,7 +541,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     // bias, ReLU -> the warp's smem transpose buffer -> global stores in which
     // CH/4 consecutive lanes write one pixel's CH contiguous outputs (full
     // 32-B sectors; lane = row would scatter 32 rows per store instruction).
-    constexpr int CH = NPAD >= 32 ? 32 : 16;
+    constexpr int CH = (NPAD >= 32 && !C::kPack) ? 32 : 16;  // packed: two CH-column loads per chunk
     constexpr int LPR = CH / 4;     // lanes per pixel row in the store phase
     constexpr int RPI = 32 / LPR;   // pixel rows per store instruction
     constexpr int NCOL = NPAD / (R::kEpiWarps / 4);  // accumulator columns of this warp
@@ -556,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
       mbar_wait(&tfull[acc], acc_phase);
       EPI_MARK(0, tile_no);
       tc_fence_after();
-      const uint32_t tb = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * NPAD;
+      const uint32_t tb = tmem_base + (static_cast<uint32_t>(quarter * 32) << 16) + acc * C::kAccCols;
 #pragma unroll 1
       for (int n0 = col0; n0 < col0 + NCOL; n0 += CH) {
         const int cidx = tile_no * (NCOL / CH) + (n0 - col0) / CH;
@@ -565,6 +580,13 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
         uint32_t r[CH];
         if constexpr (CH == 32) tmem_ld32(tb + n0, r);
         else tmem_ld16(tb + n0, r);
+        if constexpr (C::kPack) {  // main + correction accumulator, one fp32 add
+          uint32_t r2[CH];
+          tmem_ld16(tb + NPAD + n0, r2);
+          tmem_ld_wait();
+#pragma unroll
+          for (int j = 0; j < CH; ++j) r[j] = __float_as_uint(__uint_as_float(r[j]) + __uint_as_float(r2[j]));
+        }
         tmem_ld_wait();
         CHUNK_MARK(1, cidx);
         if (n0 + CH >= col0 + NCOL) {  // this warp's last TMEM read of the tile: hand its part back

@@ -900,7 +900,10 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
       g.relu = d.relu;
       g.slope = d.slope;
       g.S = S_;
-      g.grid = ctx_->sm_count;
+      {
+        static const int ctas = std::getenv("CBG_GEMM_CTAS") ? std::atoi(std::getenv("CBG_GEMM_CTAS")) : 0;
+        g.grid = ctas > 0 ? std::min(ctas, ctx_->sm_count) : ctx_->sm_count;
+      }
       g.prec = r.prec;
       g.w_exp = r.w_exp;
       g.amax_in = amax_entry(amax_origin(src));  // state / producer output values come from here
