@@ -153,6 +153,12 @@ void cbg_ctx_destroy(cbg_ctx ctx);
 int cbg_ctx_sync(cbg_ctx ctx);
 /* The context's cudaStream_t, for interop (returned as void*). */
 void* cbg_ctx_stream(cbg_ctx ctx);
+/* SMs the persistent kernels of this context (the tcgen05 GEMMs, the CUDA-core
+ * convs) spread over; 0 = all (default). With several contexts' stream sets in
+ * flight at once, a share of the GPU per GEMM lets the sets' GEMMs and their
+ * memory-bound kernels run side by side (bench.py: a third of the SMs for 4
+ * sets). Applies to frames captured after the call (set it before the first). */
+int cbg_ctx_set_persistent_sms(cbg_ctx ctx, int sms);
 
 /* ---- host-side harness mirrors of the reference io.cpp (no device) -------- */
 /* gen_synthetic, io.cpp:499-552: frames_out holds n_frames*channels*height*width

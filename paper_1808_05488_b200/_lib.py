@@ -170,6 +170,7 @@ SIGNATURES = {
     "cbg_net_copy_counts_async": (C.c_int, [_vp, _vp, _vp]),
     "cbg_net_count_slots": (C.c_int, [_vp, _P(C.c_int)]),
     "cbg_net_detect_slots": (C.c_int, [_vp, _vp]),
+    "cbg_ctx_set_persistent_sms": (C.c_int, [_vp, C.c_int]),
     "cbg_net_kernel_labels": (C.c_int, [_vp, C.c_uint, C.c_char_p, C.c_int]),
     "cbg_debug_gemm_trace": (C.c_int, [_vp, C.c_int]),
 }

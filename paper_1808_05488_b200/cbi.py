@@ -516,6 +516,11 @@ class Context:
     def synchronize(self):
         check(lib.cbg_ctx_sync(self.handle))
 
+    def set_persistent_sms(self, sms: int):
+        """SMs the persistent kernels of this context spread over (0 = all);
+        for frames captured afterwards"""
+        check(lib.cbg_ctx_set_persistent_sms(self.handle, int(sms)))
+
     @property
     def stream(self) -> int:
         return lib.cbg_ctx_stream(self.handle) or 0

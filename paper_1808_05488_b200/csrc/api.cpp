@@ -391,6 +391,13 @@ int cbg_net_kernel_labels(cbg_net net, unsigned flags, char* buf, int len) {
     std::memcpy(buf, js.c_str(), js.size() + 1);
   });
 }
+int cbg_ctx_set_persistent_sms(cbg_ctx ctx, int sms) {
+  return guard([&] {
+    need(ctx, "cbg_ctx_set_persistent_sms");
+    if (sms < 0) cbg::throw_invalid("cbg_ctx_set_persistent_sms: negative SM count");
+    ctx->ctx.persistent_sms = sms;
+  });
+}
 int cbg_net_detect_slots(cbg_net net, int32_t* det_slot) {
   return guard([&] {
     need(net, "cbg_net_detect_slots");

@@ -875,7 +875,10 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
         x.relu = d.relu;
         x.slope = d.slope;
         x.S = S_;
-        x.sm_count = ctx_->sm_count;
+        {
+          static const int ectas = std::getenv("CBG_EXACT_SMS") ? std::atoi(std::getenv("CBG_EXACT_SMS")) : -1;
+          x.sm_count = ectas == 0 ? ctx_->sm_count : ectas > 0 ? std::min(ectas, ctx_->sm_count) : ctx_->persistent();
+        }
         x.amax_out = amax_entry(i);
         timed(d.name + ".gemm", [&] { launch_conv_exact(x, st); });
         continue;
@@ -900,10 +903,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
       g.relu = d.relu;
       g.slope = d.slope;
       g.S = S_;
-      {
-        static const int ctas = std::getenv("CBG_GEMM_CTAS") ? std::atoi(std::getenv("CBG_GEMM_CTAS")) : 0;
-        g.grid = ctas > 0 ? std::min(ctas, ctx_->sm_count) : ctx_->sm_count;
-      }
+      g.grid = ctx_->persistent();
       g.prec = r.prec;
       g.w_exp = r.w_exp;
       g.amax_in = amax_entry(amax_origin(src));  // state / producer output values come from here
