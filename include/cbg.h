@@ -153,8 +153,7 @@ void cbg_ctx_destroy(cbg_ctx ctx);
 int cbg_ctx_sync(cbg_ctx ctx);
 /* The context's cudaStream_t, for interop (returned as void*). */
 void* cbg_ctx_stream(cbg_ctx ctx);
-/* SMs the persistent kernels of this context (the tcgen05 GEMMs, the CUDA-core
- * convs) spread over; 0 = all (default). With several contexts' stream sets in
+/* SMs the persistent tcgen05 GEMMs of this context spread over; 0 = all (default). With several contexts' stream sets in
  * flight at once, a share of the GPU per GEMM lets the sets' GEMMs and their
  * memory-bound kernels run side by side (bench.py: a third of the SMs for 4
  * sets). Applies to frames captured after the call (set it before the first). */

@@ -875,8 +875,10 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
         x.relu = d.relu;
         x.slope = d.slope;
         x.S = S_;
+        // the CUDA-core conv keeps every SM (measured: 60.4k vs 59.3k frames/s with
+        // the GEMMs' share); CBG_EXACT_SMS=-1 gives it the share, n > 0 n SMs
         {
-          static const int ectas = std::getenv("CBG_EXACT_SMS") ? std::atoi(std::getenv("CBG_EXACT_SMS")) : -1;
+          static const int ectas = std::getenv("CBG_EXACT_SMS") ? std::atoi(std::getenv("CBG_EXACT_SMS")) : 0;
           x.sm_count = ectas == 0 ? ctx_->sm_count : ectas > 0 ? std::min(ectas, ctx_->sm_count) : ctx_->persistent();
         }
         x.amax_out = amax_entry(i);

@@ -85,10 +85,10 @@ struct DevBuf {
 struct Ctx {
   int device = 0;
   int sm_count = 148;
-  // SMs the persistent kernels (tcgen05 GEMM, CUDA-core conv) of this context
-  // spread over (0 = all): with several contexts' stream sets in flight, a
-  // share of the GPU per GEMM lets their GEMMs and the memory-bound kernels
-  // run side by side instead of queueing for every SM
+  // SMs the persistent tcgen05 GEMMs of this context spread over (0 = all):
+  // with several contexts' stream sets in flight, a share of the GPU per GEMM
+  // lets their GEMMs and the memory-bound kernels run side by side instead of
+  // queueing for every SM
   int persistent_sms = 0;
   int persistent() const { return persistent_sms > 0 && persistent_sms < sm_count ? persistent_sms : sm_count; }
   cudaStream_t stream = nullptr;
