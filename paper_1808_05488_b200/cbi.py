@@ -489,7 +489,7 @@ class HostBuffer:
             :self.nbytes // itemsize]
 
     def __del__(self):
-        if getattr(self, "ptr", None):
+        if getattr(self, "ptr", None) and lib is not None:
             lib.cbg_host_free(C.c_void_p(self.ptr))
             self.ptr = None
 
@@ -604,7 +604,7 @@ class CBConvLayer:
         self.out_h, self.out_w = oh.value, ow.value
 
     def __del__(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and lib is not None:
             lib.cbg_conv_destroy(self.handle)
             self.handle = None
 
@@ -675,7 +675,7 @@ class CBPoolLayer:
         self.in_h, self.in_w, self.out_h, self.out_w = in_height, in_width, out_height, out_width
 
     def __del__(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and lib is not None:
             lib.cbg_pool_destroy(self.handle)
             self.handle = None
 
@@ -798,7 +798,7 @@ class CBNetwork:
         self._frame_no = 0
 
     def __del__(self):
-        if getattr(self, "handle", None):
+        if getattr(self, "handle", None) and lib is not None:
             lib.cbg_net_destroy(self.handle)
             self.handle = None
 

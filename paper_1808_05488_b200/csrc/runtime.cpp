@@ -905,7 +905,7 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
       g.relu = d.relu;
       g.slope = d.slope;
       g.S = S_;
-      g.grid = ctx_->persistent();
+      g.grid = ctx_->persistent();  // (the share for L5 alone: 58.8k vs 60.2k frames/s with it for every GEMM)
       g.prec = r.prec;
       g.w_exp = r.w_exp;
       g.amax_in = amax_entry(amax_origin(src));  // state / producer output values come from here
