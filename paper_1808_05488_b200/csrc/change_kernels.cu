@@ -1002,7 +1002,10 @@ __global__ void begin_frame_kernel(BeginFrameArgs a) {
     }
     for (int i = threadIdx.x; i < a.n_counts; i += blockDim.x)
       if (i % a.cnt_stride >= a.keep) a.counts[i] = 0;
-    if (threadIdx.x == 0) *a.frame += 1u;
+    if (threadIdx.x == 0) {
+      *a.frame += 1u;
+      if (a.in_slot) *a.in_slot = a.in_ptr;
+    }
   }
   for (long long i = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; i < a.n_clear;
        i += static_cast<long long>(gridDim.x) * blockDim.x)
@@ -1164,6 +1167,8 @@ void launch_join(const JoinArgs& a, cudaStream_t st) {
   dim3 grid(blocks_for(static_cast<long long>(a.HW) * a.Cs_out, kThreads, a.S, sm_count()), a.S);
   join_kernel<<<grid, kThreads, 0, st>>>(a);
 }
+
+const void* begin_frame_fn() { return reinterpret_cast<const void*>(&begin_frame_kernel); }
 
 void launch_begin_frame(const BeginFrameArgs& a, cudaStream_t st) {
   const long long g = std::min<long long>(2 * sm_count(), (a.n_clear + 255) / 256);

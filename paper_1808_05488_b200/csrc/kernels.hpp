@@ -214,8 +214,14 @@ struct BeginFrameArgs {
   uint4* clear;          // bitmaps written by OR (sparse detections), zeroed
   long long n_clear;     // 16-B units
   int S, n_nodes;
+  // the frame's input pointer into the slot the first detect reads (nullable):
+  // a captured graph serves any device input, the pointer set per launch as a
+  // kernel-node parameter instead of a host-to-device copy of the slot
+  const void* in_ptr;
+  const void** in_slot;
 };
 void launch_begin_frame(const BeginFrameArgs& a, cudaStream_t st);
+const void* begin_frame_fn();  // the kernel's function (finds its node in a captured graph)
 
 // Delta output of a node (its changed pixels and their output vectors),
 // packed contiguously — the layout of the device staging copy and of the

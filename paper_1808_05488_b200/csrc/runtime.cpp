@@ -486,7 +486,10 @@ Net::Net(Ctx* ctx, Topology topo, int n_streams) : ctx_(ctx), topo_(std::move(to
 }
 
 Net::~Net() {
-  for (auto& g : graphs_) cudaGraphExecDestroy(g.second);
+  for (auto& g : graphs_) {
+    cudaGraphExecDestroy(g.second.exec);
+    cudaGraphDestroy(g.second.graph);
+  }
   for (auto& e : ev_pool_) cudaEventDestroy(e);
   for (int b = 0; b < 2; ++b) {
     if (ev_copied_[b]) cudaEventDestroy(ev_copied_[b]);
@@ -676,7 +679,6 @@ void Net::build() {
   {
     const float* p = frame_.as<float>();
     CK(cudaMemcpy(frame_slot_.p, &p, sizeof(p), cudaMemcpyHostToDevice));
-    slot_value_ = p;
   }
   if (const char* e = std::getenv("CBG_SIDE_DILCOMP")) side_dc_ = std::atoi(e) != 0;
   CK(cudaStreamCreateWithFlags(&side_st_, cudaStreamNonBlocking));
@@ -738,10 +740,16 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
   const uint8_t* boot = boot_now_.as<uint8_t>();
   const int n = static_cast<int>(nodes_.size());
   {
+    const bool ext_in = n > 0 && nodes_[0].d.kind == kExternal;
+    const void** in_slot = ext_in ? nullptr
+                           : u8  ? (slot8 == 2 ? reinterpret_cast<const void**>(frame8_slot_.as<const uint8_t*>() + 2)
+                                               : nullptr)
+                                 : reinterpret_cast<const void**>(frame_slot_.p);
     BeginFrameArgs b{frame_ctr_.as<uint32_t>(), boot_now_.as<uint8_t>(), boot_req_.as<uint8_t>(),
                      dense_flag_.as<uint8_t>(), rescan_now_.as<uint8_t>(), rescan_req_.as<uint8_t>(),
                      counts, cnt_stride_ * S_, cnt_stride_, n_ext_slots_,
-                     clear_.as<uint4>(), static_cast<long long>(clear_.bytes / 16), S_, n};
+                     clear_.as<uint4>(), static_cast<long long>(clear_.bytes / 16), S_, n,
+                     in_slot ? in_ptr_ : nullptr, in_slot};
     timed("frame.begin", [&] { launch_begin_frame(b, st); });
   }
   // node whose compaction wrote node k's map (Reuse1x1 nodes alias their producer's)
@@ -957,15 +965,10 @@ void Net::forward(const float* frames, unsigned flags) {
   const bool ext = !nodes_.empty() && nodes_[0].d.kind == kExternal;
   if (!ext) {
     if (frames == nullptr) throw_invalid("forward_frame: null frame");
-    const float* want = (flags & CBG_FWD_INPUT_ON_DEVICE) ? frames : frame_.as<float>();
-    if (want != slot_value_) {
-      // zero-copy for device inputs: the ingest kernel reads through a device
-      // pointer slot, so the captured graph stays valid (pageable source: the
-      // value is consumed before cudaMemcpyAsync returns)
-      const float* v = want;
-      CK(cudaMemcpyAsync(frame_slot_.p, &v, sizeof(v), cudaMemcpyHostToDevice, st));
-      slot_value_ = want;
-    }
+    // zero-copy for device inputs: the ingest kernel reads through a device
+    // pointer slot that begin_frame fills (a kernel-node parameter of the
+    // captured graph, set per launch), so one graph serves any input buffer
+    in_ptr_ = (flags & CBG_FWD_INPUT_ON_DEVICE) ? frames : frame_.as<float>();
     if (!(flags & CBG_FWD_INPUT_ON_DEVICE))
       CK(cudaMemcpyAsync(frame_.p, frames, (flags & CBG_FWD_BROADCAST_INPUT) ? frame_.bytes / S_ : frame_.bytes,
                          cudaMemcpyHostToDevice, st));
@@ -1015,11 +1018,7 @@ void Net::forward_u8(const uint8_t* frames, unsigned flags) {
     }
   };
   if (flags & CBG_FWD_INPUT_ON_DEVICE) {
-    if (frames != slot8_value_) {
-      const uint8_t* v = frames;  // pageable source: consumed before cudaMemcpyAsync returns
-      CK(cudaMemcpyAsync(frame8_slot_.as<const uint8_t*>() + 2, &v, sizeof(v), cudaMemcpyHostToDevice, st));
-      slot8_value_ = frames;
-    }
+    in_ptr_ = frames;  // into pointer slot 2 by begin_frame (no copy of the slot)
     run_frame(flags, key | (2u << 28));
     s8_after();
     return;
@@ -1079,12 +1078,37 @@ void Net::run_frame(unsigned flags, unsigned graph_key) {
       throw;
     }
     CK(cudaStreamEndCapture(st, &g));
-    cudaGraphExec_t ge;
-    CK(cudaGraphInstantiate(&ge, g, 0));
-    cudaGraphDestroy(g);
-    it = graphs_.emplace(graph_key, ge).first;
+    GraphRec rec;
+    rec.graph = g;
+    size_t n_roots = 0;
+    CK(cudaGraphGetRootNodes(g, nullptr, &n_roots));
+    std::vector<cudaGraphNode_t> roots(n_roots);
+    if (n_roots) CK(cudaGraphGetRootNodes(g, roots.data(), &n_roots));
+    for (cudaGraphNode_t nd : roots) {
+      cudaGraphNodeType t;
+      CK(cudaGraphNodeGetType(nd, &t));
+      if (t != cudaGraphNodeTypeKernel) continue;
+      cudaKernelNodeParams p{};
+      CK(cudaGraphKernelNodeGetParams(nd, &p));
+      if (p.func != begin_frame_fn()) continue;
+      rec.begin = nd;
+      rec.begin_params = p;
+      rec.begin_args = *static_cast<const BeginFrameArgs*>(p.kernelParams[0]);
+    }
+    if (!rec.begin) throw Error(CBG_ERR_CUDA, "captured frame graph has no begin_frame root");
+    CK(cudaGraphInstantiate(&rec.exec, g, 0));
+    it = graphs_.emplace(graph_key, rec).first;
   }
-  CK(cudaGraphLaunch(it->second, st));
+  GraphRec& rec = it->second;
+  if (rec.begin_args.in_slot && rec.begin_args.in_ptr != in_ptr_) {  // this frame's input buffer
+    rec.begin_args.in_ptr = in_ptr_;
+    void* kp[1] = {&rec.begin_args};
+    cudaKernelNodeParams p = rec.begin_params;
+    p.kernelParams = kp;
+    p.extra = nullptr;
+    CK(cudaGraphExecKernelNodeSetParams(rec.exec, rec.begin, &p));
+  }
+  CK(cudaGraphLaunch(rec.exec, st));
   CK(cudaGetLastError());
 }
 

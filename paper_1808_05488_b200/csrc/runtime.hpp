@@ -208,7 +208,7 @@ class Net {
   // one is being consumed, and three device pointer slots (buffer 0, buffer 1,
   // caller's device pointer) the first detect reads through
   DevBuf frame8_, frame8_slot_;
-  const uint8_t* slot8_value_ = nullptr;  // host mirror of slot 2
+
   cudaStream_t copy_st_ = nullptr;
   cudaEvent_t ev_copied_[2] = {nullptr, nullptr}, ev_consumed_[2] = {nullptr, nullptr};
   int u8_buf_ = 0;
@@ -237,7 +237,15 @@ class Net {
   uint32_t host_frame_ = 0;
   unsigned last_flags_ = 0;
   int last_launches_ = 0;
-  std::map<unsigned, cudaGraphExec_t> graphs_;
+  struct GraphRec {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphNode_t begin = nullptr;  // the begin_frame node: its in_ptr is set per launch
+    cudaKernelNodeParams begin_params{};
+    BeginFrameArgs begin_args{};
+  };
+  std::map<unsigned, GraphRec> graphs_;
+  const void* in_ptr_ = nullptr;      // this frame's input pointer (begin_frame writes it into the slot)
   std::vector<float> host_taus_;      // network thresholds per node (thresholds())
   std::vector<float> stream_taus_;    // [node][S] mirror of the device thresholds
   bool dense_ = false;
@@ -256,7 +264,7 @@ class Net {
   std::vector<std::pair<std::string, std::pair<cudaEvent_t, cudaEvent_t>>> pending_;
   std::map<std::string, std::pair<double, long long>> times_;
   int timed_frames_ = 0;
-  const float* slot_value_ = nullptr;
+
 };
 
 // Threshold calibration with the replays on the GPU (calib.cpp;
