@@ -16,6 +16,7 @@
 // comparisons are bit-identical to the reference.
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -94,6 +95,7 @@ CBG_DEV void detect_count(int32_t* dc, int nch, bool boot, long long HW) {
 // ---------------------------------------------------------------------------
 template <bool kVec4>
 __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs a) {
+  CBG_PDL_ENTRY;
   const int s = blockIdx.y;
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(kThreads) detect_frame_kernel(DetectFrameArgs 
 // pixels (HW % 4 == 0), C <= 4 kept in registers.
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kFrameThreads) detect_frame_chw_kernel(DetectFrameArgs a) {
+  CBG_PDL_ENTRY;
   const int s = blockIdx.y;
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
@@ -253,6 +256,7 @@ __global__ void __launch_bounds__(kFrameThreads) detect_frame_chw_kernel(DetectF
 
 // scalar fallback (any C, any HW): CHW state, one thread per pixel
 __global__ void __launch_bounds__(kThreads) detect_frame_chw_scalar_kernel(DetectFrameArgs a) {
+  CBG_PDL_ENTRY;
   const int s = blockIdx.y;
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
@@ -303,6 +307,7 @@ CBG_DEV float byte_to_unit(uint32_t word, int b) {
 }
 template <bool kChw, int kC>
 __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(DetectFrameArgs a) {
+  CBG_PDL_ENTRY;
   constexpr int CM = kC ? kC : 4;  // register arrays
   const int s = blockIdx.y;
   const int CC = kC ? kC : a.C;
@@ -410,6 +415,7 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_u8_kernel(Detec
 // batches kQ quads, a grid stride apart, with all their loads issued first.
 template <int kQ, bool kPlain>
 __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_s8_kernel(DetectFrameArgs a) {
+  CBG_PDL_ENTRY;
   const int s = blockIdx.y;
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
@@ -518,6 +524,7 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_s8_kernel(Detec
 
 // scalar fallback for 8-bit frames (HW % 4 != 0)
 __global__ void __launch_bounds__(kThreads) detect_frame_u8_scalar_kernel(DetectFrameArgs a) {
+  CBG_PDL_ENTRY;
   const int s = blockIdx.y;
   const bool boot = a.boot[s] != 0;
   const long long HW = static_cast<long long>(a.H) * a.W;
@@ -559,6 +566,7 @@ __global__ void __launch_bounds__(kThreads) detect_frame_u8_scalar_kernel(Detect
 // (ceil(Cs/4 / g), 1, 2 or 4; wider pixels re-read the rest)
 template <int kCache>
 __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListArgs a, int glog) {
+  CBG_PDL_ENTRY;
   const int s = blockIdx.y;
   const uint32_t fno = *a.frame;
   const bool boot = a.boot[s] != 0;
@@ -745,6 +753,7 @@ CBG_DEV void emit_words(uint32_t v, bool valid, int i, int r0, int nw, int W, ui
 // words go to shared memory and the pool's rows inside the band (ORs of row
 // pairs and bit pairs) are emitted after one barrier.
 __global__ void __launch_bounds__(512) dilate_compact_kernel(DilateCompactArgs a) {
+  CBG_PDL_ENTRY;
   extern __shared__ __align__(16) uint32_t s_out[];  // [rows][nwo], fused pool only
   const int s = blockIdx.y, band = blockIdx.x;
   const int nwi = (a.Win + 31) >> 5, nwo = (a.Wout + 31) >> 5;
@@ -879,6 +888,7 @@ __global__ void __launch_bounds__(512) dilate_compact_kernel(DilateCompactArgs a
 __device__ __forceinline__ float ref_max(float m, float v) { return (m < v) ? v : m; }
 
 __global__ void __launch_bounds__(kFrameThreads) pool_kernel(PoolArgs a, int glog) {
+  CBG_PDL_ENTRY;
   const int s = blockIdx.y;
   const long long n = a.count[s * a.cnt_stride];
   const long long HWi = static_cast<long long>(a.Hin) * a.Win;
@@ -934,6 +944,7 @@ __global__ void __launch_bounds__(kFrameThreads) pool_kernel(PoolArgs a, int glo
 // nearest upsampling at listed output pixels (extension): out(j, i) = in(j/f, i/f)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kFrameThreads) upsample_kernel(PoolArgs a, int glog) {
+  CBG_PDL_ENTRY;
   const int s = blockIdx.y;
   const long long n = a.count[s * a.cnt_stride];
   const long long HWi = static_cast<long long>(a.Hin) * a.Win;
@@ -959,6 +970,7 @@ __global__ void __launch_bounds__(kFrameThreads) upsample_kernel(PoolArgs a, int
 // joins: one thread per (pixel, output channel).
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) join_kernel(JoinArgs a) {
+  CBG_PDL_ENTRY;
   const int s = blockIdx.y;
   const long long n = a.count[s * a.cnt_stride];
   const int32_t* list = a.idx + static_cast<long long>(s) * a.HW;
@@ -1019,6 +1031,7 @@ __global__ void begin_frame_kernel(BeginFrameArgs a) {
 // host buffer (from the SMs, only when a frame changed more than estimated)
 // ---------------------------------------------------------------------------
 __global__ void __launch_bounds__(kThreads) pack_delta_kernel(DeltaArgs a) {
+  CBG_PDL_ENTRY;
   const int s = blockIdx.y;
   __shared__ size_t s_off;
   if (threadIdx.x == 0) {
@@ -1092,31 +1105,31 @@ void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
     if (HW % 4 == 0 && (a.state_chw || a.Cs == 4)) {
       dim3 grid(2 * blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
       if (a.state_chw && a.C == 3 && a.use_state8 && a.state8)
-        a.map_plain ? detect_frame_s8_kernel<2, true><<<grid, kFrameThreads, 0, st>>>(a)
-                    : detect_frame_s8_kernel<2, false><<<grid, kFrameThreads, 0, st>>>(a);
-      else if (a.state_chw && a.C == 3) detect_frame_u8_kernel<true, 3><<<grid, kFrameThreads, 0, st>>>(a);
-      else if (a.state_chw) detect_frame_u8_kernel<true, 0><<<grid, kFrameThreads, 0, st>>>(a);
-      else detect_frame_u8_kernel<false, 0><<<grid, kFrameThreads, 0, st>>>(a);
+        a.map_plain ? launch_k(detect_frame_s8_kernel<2, true>, grid, dim3(kFrameThreads), 0, st, a)
+                    : launch_k(detect_frame_s8_kernel<2, false>, grid, dim3(kFrameThreads), 0, st, a);
+      else if (a.state_chw && a.C == 3) launch_k(detect_frame_u8_kernel<true, 3>, grid, dim3(kFrameThreads), 0, st, a);
+      else if (a.state_chw) launch_k(detect_frame_u8_kernel<true, 0>, grid, dim3(kFrameThreads), 0, st, a);
+      else launch_k(detect_frame_u8_kernel<false, 0>, grid, dim3(kFrameThreads), 0, st, a);
     } else {
       dim3 grid(blocks_for(HW, kThreads, a.S, sm_count()), a.S);
-      detect_frame_u8_scalar_kernel<<<grid, kThreads, 0, st>>>(a);
+      launch_k(detect_frame_u8_scalar_kernel, grid, dim3(kThreads), 0, st, a);
     }
     return;
   }
   if (a.state_chw) {
     if (a.C <= 4 && HW % 4 == 0) {
       dim3 grid(2 * blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
-      detect_frame_chw_kernel<<<grid, kFrameThreads, 0, st>>>(a);
+      launch_k(detect_frame_chw_kernel, grid, dim3(kFrameThreads), 0, st, a);
     } else {
       dim3 grid(blocks_for(HW, kThreads, a.S, sm_count()), a.S);
-      detect_frame_chw_scalar_kernel<<<grid, kThreads, 0, st>>>(a);
+      launch_k(detect_frame_chw_scalar_kernel, grid, dim3(kThreads), 0, st, a);
     }
   } else if (a.Cs == 4 && HW % 4 == 0) {
     dim3 grid(blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
-    detect_frame_kernel<true><<<grid, kThreads, 0, st>>>(a);
+    launch_k(detect_frame_kernel<true>, grid, dim3(kThreads), 0, st, a);
   } else {
     dim3 grid(blocks_for(HW, kThreads, a.S, sm_count()), a.S);
-    detect_frame_kernel<false><<<grid, kThreads, 0, st>>>(a);
+    launch_k(detect_frame_kernel<false>, grid, dim3(kThreads), 0, st, a);
   }
 }
 
@@ -1126,9 +1139,9 @@ void launch_detect_list(const DetectListArgs& a, cudaStream_t st) {
   // 128-thread CTAs (<= 88 registers) co-reside with a persistent GEMM CTA
   dim3 grid(2 * blocks_for(HW, kThreads >> glog, a.S, sm_count()), a.S);
   const int per_lane = (a.Cs / 4 + (1 << glog) - 1) >> glog;
-  if (per_lane <= 1) detect_list_kernel<1><<<grid, kFrameThreads, 0, st>>>(a, glog);
-  else if (per_lane <= 2) detect_list_kernel<2><<<grid, kFrameThreads, 0, st>>>(a, glog);
-  else detect_list_kernel<4><<<grid, kFrameThreads, 0, st>>>(a, glog);
+  if (per_lane <= 1) launch_k(detect_list_kernel<1>, grid, dim3(kFrameThreads), 0, st, a, glog);
+  else if (per_lane <= 2) launch_k(detect_list_kernel<2>, grid, dim3(kFrameThreads), 0, st, a, glog);
+  else launch_k(detect_list_kernel<4>, grid, dim3(kFrameThreads), 0, st, a, glog);
 }
 
 bool dilate_compact_tiling(int Hin, int Win, int Hout, int Wout, int kh, int stride, int Wp, int* rows, int* bands,
@@ -1146,26 +1159,34 @@ bool dilate_compact_tiling(int Hin, int Win, int Hout, int Wout, int kh, int str
 }
 
 void launch_dilate_compact(const DilateCompactArgs& a, cudaStream_t st) {
-  dilate_compact_kernel<<<dim3(a.n_bands, a.S), a.threads, a.pool_map ? a.smem_bytes : 0, st>>>(a);
+  launch_k(dilate_compact_kernel, dim3(a.n_bands, a.S), dim3(a.threads), a.pool_map ? a.smem_bytes : 0, st, a);
 }
 
 void launch_pool(const PoolArgs& a, cudaStream_t st) {
   const int glog = group_log2(a.Cs);
   const long long HWo = static_cast<long long>(a.Hout) * a.Wout;
   dim3 grid(2 * blocks_for(HWo, kThreads >> glog, a.S, sm_count()), a.S);
-  pool_kernel<<<grid, kFrameThreads, 0, st>>>(a, glog);
+  launch_k(pool_kernel, grid, dim3(kFrameThreads), 0, st, a, glog);
 }
 
 void launch_upsample(const PoolArgs& a, cudaStream_t st) {
   const int glog = group_log2(a.Cs);
   const long long HWo = static_cast<long long>(a.Hout) * a.Wout;
   dim3 grid(2 * blocks_for(HWo, kThreads >> glog, a.S, sm_count()), a.S);
-  upsample_kernel<<<grid, kFrameThreads, 0, st>>>(a, glog);
+  launch_k(upsample_kernel, grid, dim3(kFrameThreads), 0, st, a, glog);
 }
 
 void launch_join(const JoinArgs& a, cudaStream_t st) {
   dim3 grid(blocks_for(static_cast<long long>(a.HW) * a.Cs_out, kThreads, a.S, sm_count()), a.S);
-  join_kernel<<<grid, kThreads, 0, st>>>(a);
+  launch_k(join_kernel, grid, dim3(kThreads), 0, st, a);
+}
+
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("CBG_PDL");
+    return !(e && std::atoi(e) == 0);
+  }();
+  return on;
 }
 
 const void* begin_frame_fn() { return reinterpret_cast<const void*>(&begin_frame_kernel); }
@@ -1177,7 +1198,7 @@ void launch_begin_frame(const BeginFrameArgs& a, cudaStream_t st) {
 
 void launch_pack_delta(const DeltaArgs& a, cudaStream_t st) {
   dim3 grid(std::max(1, 2 * sm_count() / std::max(1, a.S)), a.S);
-  pack_delta_kernel<<<grid, kThreads, 0, st>>>(a);
+  launch_k(pack_delta_kernel, grid, dim3(kThreads), 0, st, a);
 }
 
 void launch_nhwc_to_chw(const float* src, float* dst, int C, int Cs, int HW, cudaStream_t st) {

@@ -94,6 +94,7 @@ CBG_DEV void exact_row(unsigned long long (&acc)[kPix][G / 2], const float (&xv)
 template <int G, int KW, bool CHECK, int PS>
 // <= 88 registers: a 128-thread CTA (11k) still fits beside a resident GEMM CTA
 __global__ void __maxnreg__(88) conv_exact_kernel(ConvExactArgs a) {  // launched with kThreads = 128
+  CBG_PDL_ENTRY;
   extern __shared__ __align__(16) float sw[];  // [K][G] weights of this output group, reference r order
   __shared__ int s_prefix[kMaxStreams + 1];
   const int og = blockIdx.y;  // output-channel group
@@ -291,7 +292,7 @@ void launch_k(const ConvExactArgs& a, cudaStream_t st) {
   if (bx > most) bx = most;
   if (bx < 1) bx = 1;
   dim3 grid(static_cast<unsigned>(bx), (a.Cout + G - 1) / G);
-  conv_exact_kernel<G, KW, CHECK, PS><<<grid, kThreads, smem, st>>>(a);
+  launch_k(conv_exact_kernel<G, KW, CHECK, PS>, grid, dim3(kThreads), smem, st, a);
 }
 
 template <int G, int KW>

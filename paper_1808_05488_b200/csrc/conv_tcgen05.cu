@@ -183,6 +183,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
+  pdl_trigger();
   if (tid == 0) CTA_MARK(0);
   const long long HWin = static_cast<long long>(a.Hin) * a.Win;
   const long long HWout = static_cast<long long>(a.Hout) * a.Wout;
@@ -204,6 +205,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
   for (int i = tid; i < a.n_tiles * NPAD; i += kThreads) s_bias[i] = a.bias[i];  // zero-padded to n_tiles*NPAD
   if constexpr (is_direct(PREC))
     for (int i = tid; i < a.KB * 8; i += kThreads) s_ktab[i] = reinterpret_cast<const uint2*>(a.ktab)[i];
+  pdl_wait();  // the setup above (barriers, TMEM, bias, tap table) does not read the predecessor's results
   if (warp == 0) {
     int carry = 0;
     if (lane == 0) tprefix[0] = 0;
@@ -665,7 +667,7 @@ void launch_impl(const ConvGemmArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(conv_gemm_kernel<NPAD, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     configured = true;
   }
-  conv_gemm_kernel<NPAD, PREC><<<a.grid, kThreads, smem, st>>>(a);
+  launch_k(conv_gemm_kernel<NPAD, PREC>, dim3(a.grid), dim3(kThreads), smem, st, a);
 }
 
 template <int PREC>

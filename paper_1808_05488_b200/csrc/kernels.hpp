@@ -24,6 +24,25 @@
 
 namespace cbg {
 
+// Kernel launch with programmatic stream serialization (common.cuh pdl_*):
+// the next kernel of a frame is scheduled while this one drains; every kernel
+// launched this way starts with griddepcontrol.wait. CBG_PDL=0 turns it off.
+bool pdl_enabled();
+template <typename... P, typename... A>
+inline void launch_k(void (*kern)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, A... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, args...);
+}
+
 // Fused change detection on the network-input frame (CHW) against a
 // closed-loop / feed-forward state (NHWC), reference change.cpp:20-43.
 struct DetectFrameArgs {
