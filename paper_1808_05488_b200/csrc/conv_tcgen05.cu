@@ -162,7 +162,7 @@ __host__ __device__ constexpr int tail_bytes(int stages, int KB, int S, int nbia
 }
 
 template <int NPAD, int PREC>
-__global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) {
+__global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(const __grid_constant__ ConvGemmArgs a) {
   using C = Cfg<NPAD, PREC>;
   using R = Roles<NPAD, PREC>;
   extern __shared__ uint8_t smem_raw[];
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     for (int i = 0; i < C::kStages; ++i) {
       mbar_init(&full[i], R::kConvWarps / R::kConvGroups + 1);  // one convert group + 1 expect_tx arrive
       mbar_init(&empty[i], 1);              // tcgen05.commit
-      mbar_init(&raw[i], R::kFetchG);       // one cp.async.mbarrier.arrive per fetch thread of a group
+      mbar_init(&raw[i], a.use_tma ? 1 : R::kFetchG);  // one cp.async arrive per fetch thread of a group, or the TMA
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tfull[i], 1);
@@ -242,7 +242,67 @@ __global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(ConvGemmArgs a) 
     nt = local - mt * a.n_tiles;
   };
 
-  if (warp >= R::kFirstFetchWarp && warp < R::kFirstConvWarp) {
+  if (!is_direct(PREC) && a.use_tma && warp >= R::kFirstFetchWarp && warp < R::kFirstConvWarp) {
+    // ===================== fetch by TMA gather4 (1x1 layers) =====================
+    // one thread per fetch group issues, per K-block, 32 gather4 copies of 4 rows
+    // x 128 B (the K-block's 32 fp32 of 4 changed pixels) into the stage, 128-B
+    // swizzled exactly like the cp.async path's manual XOR, completing on the
+    // stage's `raw` barrier; rows past the count read an out-of-range row (zeros)
+    const int wpg = R::kFetchWarps / R::kFetchGroups;
+    const int fgrp = (warp - R::kFirstFetchWarp) / wpg;
+    const bool lead_warp = (warp - R::kFirstFetchWarp) % wpg == 0;
+    const int oob = a.S * static_cast<int>(HWin);  // first row past the tensor
+    int* s_rows = reinterpret_cast<int*>(rowinfo) + fgrp * kBM;  // this group's tile rows (tensor rows)
+    uint32_t g = 0;
+    for (int w = blockIdx.x; w < total; w += gridDim.x) {
+      int s, mt, nt;
+      decode(w, s, mt, nt);
+      if (!lead_warp) {
+        g += a.KB;
+        continue;
+      }
+      const int cnt = a.count[s * a.cnt_stride];
+      // the tile's rows -> input pixels (1x1, stride 1, pad 0; the output may be a crop)
+      for (int j = lane; j < kBM; j += 32) {
+        const int k = mt * kBM + j;
+        int row = oob;
+        if (k < cnt) {
+          const int p = __ldg(a.idx + s * HWout + k);
+          const int jo = p / a.Wout, io = p - jo * a.Wout;
+          row = s * static_cast<int>(HWin) + jo * a.Win + io;
+        }
+        s_rows[j] = row;
+      }
+      __syncwarp();
+      const uint8_t* bimg = a.wimg + static_cast<long long>(nt) * a.KB * 2 * C::kBBytes;
+#pragma unroll 1
+      for (int kb = 0; kb < a.KB; ++kb, ++g) {
+        if (static_cast<int>(g % R::kFetchGroups) != fgrp) continue;
+        const int stage = g % C::kStages;
+        const uint32_t phase = (g / C::kStages) & 1;
+        if (lane == 0) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_arrive_expect_tx(&raw[stage], kABytes);
+        }
+        __syncwarp();
+        uint8_t* sA = smem + stage * C::kStageBytes;
+        {  // lane i issues the gather4 of rows 4i..4i+3 (32 lanes x 4 rows = the tile)
+          const int4 r = make_int4(s_rows[4 * lane], s_rows[4 * lane + 1], s_rows[4 * lane + 2], s_rows[4 * lane + 3]);
+          asm volatile(
+              "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+              " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(sA + 512 * lane)),
+              "l"(reinterpret_cast<uint64_t>(&a.tmap)), "r"(32 * kb), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w),
+              "r"(smem_u32(&raw[stage]))
+              : "memory");
+        }
+        if (lane == 0) {
+          mbar_arrive_expect_tx(&full[stage], 2 * C::kBBytes);
+          bulk_g2s(sA + kABytes, bimg + static_cast<long long>(kb) * 2 * C::kBBytes, 2 * C::kBBytes, &full[stage]);
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp >= R::kFirstFetchWarp && warp < R::kFirstConvWarp) {
     // ========================= fetch =========================
     constexpr int kFetchG = R::kFetchG, kFetchChunks = R::kFetchChunks;
     const int fgrp = (tid - 32 * R::kFirstFetchWarp) / kFetchG;  // K-blocks g with g % groups == fgrp

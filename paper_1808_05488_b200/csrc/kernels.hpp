@@ -20,6 +20,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace cbg {
@@ -165,6 +166,11 @@ void launch_join(const JoinArgs& a, cudaStream_t st);
 // Gather + 3xTF32 tcgen05 GEMM + bias/ReLU scatter (reference im2col + gemm +
 // update_output: dense.cpp:44-112, layers.cpp:10-31).
 struct ConvGemmArgs {
+  // staged A path of a 1x1 layer (prec 1): the A rows come by TMA
+  // tile::gather4 over this map of the source [S*Hin*Win][Cs] fp32 (box 32
+  // elements x 1 row, 128-B swizzle) instead of the fetch warps' cp.async
+  CUtensorMap tmap;
+  int use_tma;
   const float* src;        // [S][Hin][Win][Cs] column source (state or producer output)
   int src_presplit;        // src is the detect's pre-split copy (DetectListArgs::split), not fp32
   float* out;              // [S][Hout][Wout][Co4]

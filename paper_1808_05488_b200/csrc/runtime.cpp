@@ -602,6 +602,12 @@ void Net::build() {
         if (r.KB > 512) throw Error(CBG_ERR_UNSUPPORTED, "Cin*kh*kw too large for the GEMM kernel (K > 16384)");
         if (r.Csi >= 32768) throw Error(CBG_ERR_UNSUPPORTED, "too many input channels");
         r.prec = gemm_prec(r.npad);
+        {
+          const char* te = std::getenv("CBG_TMA_1X1");
+          r.tma_a = te && std::atoi(te) != 0 && c.kernel_h == 1 && c.kernel_w == 1 && c.stride == 1 &&
+                    c.padding == 0 && r.prec == 2;
+          if (r.tma_a) r.prec = 1;  // staged A path, rows by TMA
+        }
         constexpr int kSmemMax = 232448;  // 227 KB opt-in per CTA
         if (conv_gemm_smem_bytes(r.npad, r.KB, S_, r.prec, r.n_tiles) > kSmemMax) r.prec = 0;  // fewer stages (tf32)
         if (conv_gemm_smem_bytes(r.npad, r.KB, S_, r.prec, r.n_tiles) > kSmemMax)
@@ -910,6 +916,30 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
       g.stride = c.stride, g.pad = c.padding;
       g.kh = c.kernel_h, g.kw = c.kernel_w;
       g.KB = r.KB, g.npad = r.npad, g.n_tiles = r.n_tiles;
+      if (r.tma_a) {  // TMA gather4 map of the column source [S*Hi*Wi][Csi] fp32 (encoded once per source)
+        if (r.tmap_src != g.src) {
+          using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                        const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                        CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+          static EncodeFn encode = [] {
+            void* fn = nullptr;
+            cudaDriverEntryPointQueryResult q;
+            CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+            return reinterpret_cast<EncodeFn>(fn);
+          }();
+          const cuuint64_t dims[2] = {static_cast<cuuint64_t>(r.Csi), static_cast<cuuint64_t>(S_) * d.Hi * d.Wi};
+          const cuuint64_t strides[1] = {static_cast<cuuint64_t>(r.Csi) * 4};
+          const cuuint32_t box[2] = {32, 1};
+          const cuuint32_t estr[2] = {1, 1};
+          if (encode(&r.tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(g.src), dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            throw Error(CBG_ERR_CUDA, "cuTensorMapEncodeTiled failed");
+          r.tmap_src = g.src;
+        }
+        g.tmap = r.tmap;
+        g.use_tma = 1;
+      }
       g.relu = d.relu;
       g.slope = d.slope;
       g.S = S_;

@@ -103,6 +103,9 @@ struct NodeRT {
   // conv
   int npad = 0, n_tiles = 0, KB = 0;
   int prec = 1;                  // tcgen05 operand split: 0 = 3xTF32, 1 = 3xFP16 (scaled)
+  bool tma_a = false;            // 1x1 layer, staged A path fed by TMA gather4 (CBG_TMA_1X1=1, experiment)
+  CUtensorMap tmap{};
+  const float* tmap_src = nullptr;
   int w_exp = 0;                 // fp16: weights scaled by 2^-w_exp in the image
   bool exact = false;            // CUDA-core bit-exact path (conv_exact.cu) instead of tcgen05
   bool state_chw = false;        // first-layer exact conv: input state as CHW planes (= the frame layout)

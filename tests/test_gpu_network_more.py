@@ -320,6 +320,15 @@ def test_a_operand_paths(gpu, monkeypatch, direct):
     run_pair(spec, [0.05] * 5, frames_for(80, 112, noise=0.003))
 
 
+def test_tma_gather4_a_path_for_1x1_layers(gpu, monkeypatch):
+    """The experimental A producer of 1x1 layers (CBG_TMA_1X1=1): the tile's rows
+    arrive by TMA tile::gather4 into the staged path's swizzled stages (DESIGN.md
+    §8.25; slower than the direct path, kept off by default)."""
+    monkeypatch.setenv("CBG_TMA_1X1", "1")
+    spec = cbi.make_seg_spec(9, 80, 112)
+    run_pair(spec, [0.05] * 5, frames_for(80, 112, noise=0.003))
+
+
 def test_detached_output_copy_pipelines(gpu):
     """cbg_net_copy_output_detached: frame k's output lands in its own host
     buffer although frame k+1 (and k+2) were enqueued before anyone waited;
