@@ -96,11 +96,24 @@ __host__ __device__ constexpr bool is_direct(int p) { return p == kPrecF16Direct
 //             global memory into registers, split them and store them into
 //             TMEM with tcgen05.st.16x256b (4 threads per row, 2 rows per
 //             thread per store); A never touches shared memory
+// direct-path convert warps (groups of 4, one per TMEM lane quarter). Fewer
+// warps free registers for the other stream groups' kernels on the GEMM's SMs
+// (DESIGN.md §8.27): N = 256 runs MMA-bound with 2 groups as with 3
+#ifndef CBG_N256_CONV_WARPS
+#define CBG_N256_CONV_WARPS 8
+#endif
+#ifndef CBG_N256_EPI_WARPS  // epilogue warps of the N = 256 kernel (2 per TMEM lane quarter)
+#define CBG_N256_EPI_WARPS 8
+#endif
+#ifndef CBG_N128_CONV_WARPS  // N <= 128
+#define CBG_N128_CONV_WARPS 16
+#endif
 template <int NPAD, int PREC>
 struct Roles {
-  static constexpr int kEpiWarps = NPAD >= 256 ? 8 : 4;
+  static constexpr int kEpiWarps = NPAD >= 256 ? CBG_N256_EPI_WARPS : 4;
   static constexpr int kFetchWarps = is_direct(PREC) ? 0 : 8;
-  static constexpr int kConvWarps = is_direct(PREC) ? 20 - kEpiWarps : NPAD >= 256 ? 4 : 8;
+  static constexpr int kConvWarps = is_direct(PREC) ? (NPAD >= 256 ? CBG_N256_CONV_WARPS : CBG_N128_CONV_WARPS)
+                                                    : NPAD >= 256 ? 4 : 8;
   static constexpr int kFirstFetchWarp = kEpiWarps;
   static constexpr int kFirstConvWarp = kFirstFetchWarp + kFetchWarps;
   static constexpr int kMmaWarp = kFirstConvWarp + kConvWarps;
@@ -109,12 +122,11 @@ struct Roles {
   static constexpr int kFetchG = is_direct(PREC) ? 128 : kFetchWarps * 32 / kFetchGroups;
   static constexpr int kConvG = 128;
   static constexpr int kFetchChunks = 128 * 8 / kFetchG;   // 16-B A chunks per fetch thread per K-block
-  static_assert(kMmaWarp == 20, "21 warps");
+  static constexpr int kThreads = (kMmaWarp + 1) * 32;
 };
-constexpr int kThreads = 21 * 32;
 constexpr int kGroups = 2;  // stage counts are multiples of this (fetch and convert groups)
 // epilogue transpose buffers: one [32][CH + 4] per epilogue warp (CH = 32, or 16 for N = 16)
-__host__ __device__ constexpr int epi_buf_floats(int npad) { return (npad >= 256 ? 8 : 4) * 32 * 36; }
+__host__ __device__ constexpr int epi_buf_floats(int npad) { return (npad >= 256 ? CBG_N256_EPI_WARPS : 4) * 32 * 36; }
 constexpr int kBM = 128;                 // UMMA M
 constexpr int kBK = 32;                  // fp32 elements per K-block (= one 128-B swizzle row)
 constexpr int kABytes = kBM * kBK * 4;   // raw fp32 A rows of one K-block: 16 KB
@@ -142,7 +154,8 @@ struct Cfg {
   // (mbarrier parity aliases modulo 2) as complete.
   // (N = 256 has one convert group, so any count works there; 3 leaves room
   // for its 8 epilogue warps' transpose buffers)
-  static constexpr int kStages = is_direct(PREC) ? (NPAD >= 256 ? 3 : 8)
+  static constexpr int kStages = is_direct(PREC) ? (NPAD >= 256 ? (CBG_N256_CONV_WARPS == 12 ? 3 : 4)
+                                                                : (CBG_N128_CONV_WARPS == 12 ? 6 : 8))
                                  : is_f16(PREC)  ? (NPAD >= 256 ? 3 : NPAD >= 128 ? 6 : 8)
                                                  : (NPAD >= 256 ? 2 : NPAD >= 128 ? 4 : 6);
   static_assert(kStages % Roles<NPAD, PREC>::kConvGroups == 0, "stages must be a multiple of the convert groups");
@@ -162,9 +175,11 @@ __host__ __device__ constexpr int tail_bytes(int stages, int KB, int S, int nbia
 }
 
 template <int NPAD, int PREC>
-__global__ void __launch_bounds__(kThreads, 1) conv_gemm_kernel(const __grid_constant__ ConvGemmArgs a) {
+__global__ void __maxnreg__(80)  // 21 warps (17 for the 8-convert-warp N = 256 variant) x 80 registers
+    conv_gemm_kernel(const __grid_constant__ ConvGemmArgs a) {
   using C = Cfg<NPAD, PREC>;
   using R = Roles<NPAD, PREC>;
+  constexpr int kThreads = R::kThreads;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* tail = smem + C::kStages * C::kStageBytes;
@@ -727,7 +742,7 @@ void launch_impl(const ConvGemmArgs& a, cudaStream_t st) {
     cudaFuncSetAttribute(conv_gemm_kernel<NPAD, PREC>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     configured = true;
   }
-  launch_k(conv_gemm_kernel<NPAD, PREC>, dim3(a.grid), dim3(kThreads), smem, st, a);
+  launch_k(conv_gemm_kernel<NPAD, PREC>, dim3(a.grid), dim3(Roles<NPAD, PREC>::kThreads), smem, st, a);
 }
 
 template <int PREC>
