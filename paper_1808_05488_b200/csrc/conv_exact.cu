@@ -21,6 +21,9 @@
 // thread owns one changed pixel and G output channels: per K-row it does one
 // (L1-cached) input load, G/4 shared-memory float4 weight broadcasts and G
 // multiply/add pairs, so the FP32 pipe does the work.
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.hpp"
 
@@ -286,8 +289,10 @@ void launch_k(const ConvExactArgs& a, cudaStream_t st) {
     per_sm_smem = smem;
   }
   // persistent: every CTA resident, striding over the blocks of all streams
+  static const int cap = std::getenv("CBG_EXACT_PER_SM") ? std::atoi(std::getenv("CBG_EXACT_PER_SM")) : 0;
+  const int psm = cap > 0 ? std::min(cap, per_sm) : per_sm;
   const long long HWo = static_cast<long long>(a.Hout) * a.Wout;
-  long long bx = static_cast<long long>(a.sm_count) * per_sm;
+  long long bx = static_cast<long long>(a.sm_count) * psm;
   const long long most = ((HWo + kThreads * kPix - 1) / (kThreads * kPix)) * a.S;
   if (bx > most) bx = most;
   if (bx < 1) bx = 1;
