@@ -716,14 +716,12 @@ CBG_DEV uint32_t row_mask(int W, int wo) {  // valid bits of word wo of a W-pixe
   return v >= 32 ? 0xffffffffu : (v <= 0 ? 0u : ((1u << v) - 1u));
 }
 
-// Store the words of one warp (word i of a band of nw-word rows starting at
-// row r0; the band's rows are contiguous in the map) and append their marked
-// pixels to the list: one atomicAdd on the stream's count per warp places the
+// Store the words of one warp (word i of the band's map, whose bit 0 is pixel
+// `pix` of the image) and append their marked pixels to the list: one atomicAdd on the stream's count per warp places the
 // warp's run (row-major); a nonzero word's pixels are written by the lanes of
 // its bits (coalesced). Every lane of the warp must call it (v = 0 for lanes
 // without a word).
-CBG_DEV void emit_words(uint32_t v, bool valid, int i, int r0, int nw, int W, uint32_t* gmap, int32_t* list,
-                        int32_t* ctr) {
+CBG_DEV void emit_words(uint32_t v, bool valid, int i, int pix, uint32_t* gmap, int32_t* list, int32_t* ctr) {
   const int lane = threadIdx.x & 31;
   if (valid) gmap[i] = v;
   const int cnt = __reduce_add_sync(0xffffffffu, __popc(v));
@@ -732,15 +730,18 @@ CBG_DEV void emit_words(uint32_t v, bool valid, int i, int r0, int nw, int W, ui
   if (lane == 0) base = atomicAdd(ctr, cnt);
   base = __shfl_sync(0xffffffffu, base, 0);
   const uint32_t below = (1u << lane) - 1u;
-  const int i0 = i - lane;
   uint32_t nz = __ballot_sync(0xffffffffu, v != 0u);
+  // per nonzero word: its bits and first pixel from its lane (the loop body
+  // is the kernel's longest serial chain: no index arithmetic in it)
+  int32_t* out = list + base;
   while (nz) {
     const int k = __ffs(nz) - 1;
     nz &= nz - 1;
     const uint32_t wk = __shfl_sync(0xffffffffu, v, k);
-    const int rr = (i0 + k) / nw, wo = (i0 + k) - rr * nw;
-    if ((wk >> lane) & 1u) list[base + __popc(wk & below)] = (r0 + rr) * W + wo * 32 + lane;
-    base += __popc(wk);
+    const int pk = __shfl_sync(0xffffffffu, pix, k);
+    const int at = __popc(wk & below);
+    if ((wk >> lane) & 1u) out[at] = pk + lane;
+    out += __popc(wk);
   }
 }
 
@@ -771,11 +772,13 @@ __global__ void __launch_bounds__(512) dilate_compact_kernel(DilateCompactArgs a
     const int i = i0 + threadIdx.x;
     const bool mine = i < nout;
     uint32_t v = 0;
+    int pix = 0;
     if (mine) {
       const int rr = i / nwo, wo = i - rr * nwo;
-      if (boot) {
-        v = row_mask(a.Wout, wo);
-      } else if (a.up > 1) {  // nearest upsampling: out (jo, io) <- in (jo / up, io / up)
+      pix = (r0 + rr) * a.Wout + wo * 32;
+      // the map loads do not wait for the boot flag's load (a boot frame
+      // overrides the word at the end)
+      if (a.up > 1) {  // nearest upsampling: out (jo, io) <- in (jo / up, io / up)
         const uint32_t* row = in_s + static_cast<long long>((r0 + rr) / a.up) * nwi;
         if (a.up == 2) {  // the 16 source bits of the word, each doubled
           uint32_t x = (__ldg(row + (wo >> 1)) >> (16 * (wo & 1))) & 0xFFFFu;
@@ -852,9 +855,10 @@ __global__ void __launch_bounds__(512) dilate_compact_kernel(DilateCompactArgs a
         }
         v &= row_mask(a.Wout, wo);
       }
+      if (boot) v = row_mask(a.Wout, wo);
       if (a.pool_map) s_out[i] = v;
     }
-    emit_words(v, mine, i, r0, nwo, a.Wout, gmap, a.idx + s * HWo, a.count + s * a.cnt_stride);
+    emit_words(v, mine, i, pix, gmap, a.idx + s * HWo, a.count + s * a.cnt_stride);
   }
   if (a.pool_map == nullptr) return;
   __syncthreads();
@@ -870,15 +874,17 @@ __global__ void __launch_bounds__(512) dilate_compact_kernel(DilateCompactArgs a
     const int i = i0 + threadIdx.x;
     const bool mine = i < np;
     uint32_t v = 0;
+    int pix = 0;
     if (mine) {
       const int pr = i / nwp, pw = i - pr * nwp;
+      pix = (pr0 + pr) * a.Wp + pw * 32;
       const int ra = 2 * (pr0 + pr) - r0, rb = ra + 1;
       auto word = [&](int r, int w) { return (r < nrows && w < nwo) ? s_out[r * nwo + w] : 0u; };
       const uint32_t lo = word(ra, 2 * pw) | word(rb, 2 * pw);
       const uint32_t hi = word(ra, 2 * pw + 1) | word(rb, 2 * pw + 1);
       v = even_bits(lo | (lo >> 1), hi | (hi >> 1)) & row_mask(a.Wp, pw);
     }
-    emit_words(v, mine, i, pr0, nwp, a.Wp, pmap, plist, a.pool_count + s * a.cnt_stride);
+    emit_words(v, mine, i, pix, pmap, plist, a.pool_count + s * a.cnt_stride);
   }
 }
 
