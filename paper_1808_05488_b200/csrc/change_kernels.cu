@@ -609,6 +609,21 @@ __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListAr
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
   int nch = 0;
+  // output list (identity-window layers): a warp buffers up to 32 entries in
+  // shared memory and places them with one atomicAdd (coalesced 128-B stores)
+  __shared__ int32_t s_emit[kFrameThreads];
+  int32_t* wbuf = s_emit + (threadIdx.x & ~31);
+  int nbuf = 0;  // warp-uniform
+  int32_t* out_idx = a.out_idx ? a.out_idx + static_cast<long long>(s) * HW : nullptr;
+  auto flush = [&]() {
+    __syncwarp();
+    int b = 0;
+    if (lane == 0) b = atomicAdd(a.out_count + s * a.cnt_stride, nbuf);
+    b = __shfl_sync(0xffffffffu, b, 0);
+    if (lane < nbuf) out_idx[b + lane] = wbuf[lane];
+    __syncwarp();
+    nbuf = 0;
+  };
 
   const long long step = static_cast<long long>(gridDim.x) * wpb * gpw;
   const long long base0 = (static_cast<long long>(blockIdx.x) * wpb + warp) * gpw;
@@ -682,7 +697,19 @@ __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListAr
       map_set(m, p, a.W);
       ++nch;
     }
+    if (out_idx) {
+      const bool e = active && (any || boot) && sub == 0;
+      const uint32_t em = __ballot_sync(0xffffffffu, e);
+      const int k = __popc(em);
+      if (nbuf + k > 32) flush();
+      if (e) {
+        wbuf[nbuf + __popc(em & ((1u << lane) - 1u))] = static_cast<int32_t>(p);
+        if (boot) map_set(m, p, a.W);
+      }
+      nbuf += k;
+    }
   }
+  if (out_idx && nbuf) flush();
   detect_count(a.det_count ? a.det_count + s * a.cnt_stride : nullptr, nch, boot, HW);
 }
 
