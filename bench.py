@@ -757,17 +757,33 @@ def main():
                 dma.clear()
             barrier()
 
+            # diagnosis only: BENCH_E2E_PROBE=noapply skips the host mirror
+            # update, =noout also the delta copy (the line is then not an e2e number)
+            probe = os.environ.get("BENCH_E2E_PROBE", "")
+            host_t = [0.0, 0.0, 0.0]
+
             def e2e_step(k):
+                t_a = time.perf_counter()
                 for g in range(G):
                     put(g, frame_at(base_k + k))
-                    out(g, k)
-                if delta and k >= LAG:
+                    if probe != "noout":
+                        out(g, k)
+                t_b = time.perf_counter()
+                if delta and k >= LAG and not probe:
                     apply(k - LAG)
+                t_c = time.perf_counter()
+                host_t[0] += t_b - t_a
+                host_t[1] += t_c - t_b
+                host_t[2] += 1
 
             def finish():
                 for k in range(max(0, a.steps - LAG), a.steps):
                     apply(k)
             ems = max_over_ranks(timed_region(e2e_step, a.steps, finish if delta else None))
+            if True:  # host-side cost of the loop, to stderr
+                print(f"e2e probe {probe or '-'} u8={u8} delta={delta}: {ems / a.steps:.3f} ms/step device, host enqueue "
+                      f"{1e3 * host_t[0] / host_t[2]:.3f} ms/step, apply {1e3 * host_t[1] / host_t[2]:.3f} ms/step",
+                      file=sys.stderr)
             del enets
             r = {"value": total_streams * a.steps / (ems / 1000.0), "unit": "frames/s",
                  "h2d_bytes_per_step": frame8_bytes if u8 else frame_bytes,
