@@ -762,21 +762,31 @@ def main():
             probe = os.environ.get("BENCH_E2E_PROBE", "")
             host_t = [0.0, 0.0, 0.0]
 
+            # the host mirrors are updated by a background thread (step k - LAG
+            # while the main thread enqueues step k); a host buffer is reused
+            # only after the update that read it has finished
+            applier = ThreadPoolExecutor(max_workers=1) if delta else None
+            pending = {}
+
             def e2e_step(k):
                 t_a = time.perf_counter()
+                if delta and (k - LAG - 1) in pending:
+                    pending.pop(k - LAG - 1).result()
                 for g in range(G):
                     put(g, frame_at(base_k + k))
                     if probe != "noout":
                         out(g, k)
                 t_b = time.perf_counter()
                 if delta and k >= LAG and not probe:
-                    apply(k - LAG)
+                    pending[k - LAG] = applier.submit(apply, k - LAG)
                 t_c = time.perf_counter()
                 host_t[0] += t_b - t_a
                 host_t[1] += t_c - t_b
                 host_t[2] += 1
 
             def finish():
+                for k in sorted(pending):
+                    pending.pop(k).result()
                 for k in range(max(0, a.steps - LAG), a.steps):
                     apply(k)
             ems = max_over_ranks(timed_region(e2e_step, a.steps, finish if delta else None))
@@ -791,6 +801,7 @@ def main():
                  "ms_per_step": ems / a.steps}
             if delta:
                 appl.shutdown()
+                applier.shutdown()
                 r["d2h_full_output_bytes"] = out_bytes * G
                 r["d2h_delta_bytes_in_use"] = sum(dbytes) / len(dbytes)
             return r

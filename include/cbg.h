@@ -343,7 +343,9 @@ void* cbg_ctx_copy_stream(cbg_ctx ctx);
  * waits for the copy into host_buf, then scatters streams [stream_begin,
  * stream_end) into a host mirror [S][H][W][Cs] of the raw output that the
  * caller keeps across frames (initialised from a full copy, or zeros before the
- * first frame: every pixel of a full update is in the delta). */
+ * first frame: every pixel of a full update is in the delta). The apply may run
+ * on another host thread while the net's frame and copy calls go on, as long
+ * as host_buf is not handed to a new copy before its apply returned. */
 int cbg_net_output_delta_bytes(cbg_net net, int node, int64_t* bytes);
 /* Pinned, mapped, portable host memory (what the copy functions above expect). */
 int cbg_host_alloc(int64_t bytes, void** ptr);

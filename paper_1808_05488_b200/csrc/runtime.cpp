@@ -1298,7 +1298,7 @@ void Net::copy_output_delta(int node, void* host_buf) {
   size_t est = cap;
   if (delta_seen_ > 0) {
     size_t m = 0;
-    for (size_t v : delta_recent_) m = std::max(m, v);
+    for (const auto& v : delta_recent_) m = std::max(m, v.load(std::memory_order_relaxed));
     est = std::min(cap, (m + m / 4 + 65536 + 15) / 16 * 16);
   }
   DeltaArgs a{};
@@ -1317,18 +1317,28 @@ void Net::copy_output_delta(int node, void* host_buf) {
   CK(cudaMemcpyAsync(host_buf, delta_stage_[b].p, est, cudaMemcpyDeviceToHost, ctx_->d2h));
   delta_dma_last_ = est;
   CK(cudaEventRecord(ev_dpushed_[b], ctx_->d2h));
-  DeltaCopy& dc = delta_host_[host_buf];
-  if (!dc.ev) CK(cudaEventCreateWithFlags(&dc.ev, cudaEventDisableTiming));
-  CK(cudaEventRecord(dc.ev, ctx_->d2h));
+  cudaEvent_t ev;
+  {
+    std::lock_guard<std::mutex> lk(delta_mu_);
+    DeltaCopy& dc = delta_host_[host_buf];
+    if (!dc.ev) CK(cudaEventCreateWithFlags(&dc.ev, cudaEventDisableTiming));
+    ev = dc.ev;
+  }
+  CK(cudaEventRecord(ev, ctx_->d2h));
 }
 
 void Net::apply_output_delta(int node, const void* host_buf, float* mirror, int s0, int s1) {
   if (node < 0) node = static_cast<int>(nodes_.size()) - 1;
   if (node >= static_cast<int>(nodes_.size())) throw_invalid("apply_output_delta: bad node");
   if (s0 < 0 || s1 > S_ || s0 > s1) throw_invalid("apply_output_delta: bad stream range");
-  auto it = delta_host_.find(host_buf);
-  if (it == delta_host_.end()) throw_invalid("apply_output_delta: no delta was copied into this buffer");
-  CK(cudaEventSynchronize(it->second.ev));
+  cudaEvent_t ev;
+  {
+    std::lock_guard<std::mutex> lk(delta_mu_);
+    auto it = delta_host_.find(host_buf);
+    if (it == delta_host_.end()) throw_invalid("apply_output_delta: no delta was copied into this buffer");
+    ev = it->second.ev;
+  }
+  CK(cudaEventSynchronize(ev));
   const NodeRT& r = nodes_[node];
   const int Cs = r.Cs;
   const uint8_t* buf = static_cast<const uint8_t*>(host_buf);
@@ -1348,7 +1358,7 @@ void Net::apply_output_delta(int node, const void* host_buf, float* mirror, int 
   }
   if (s1 == S_) {  // the whole buffer's size feeds the next DMA estimates
     for (int s = s1; s < S_; ++s) off += delta_stream_bytes(hdr[s], Cs);
-    delta_recent_[delta_seen_++ % 4] = off;
+    delta_recent_[delta_seen_.fetch_add(1) % 4].store(off, std::memory_order_relaxed);
   }
 }
 

@@ -13,8 +13,10 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <map>
+#include <mutex>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -225,9 +227,12 @@ class Net {
   struct DeltaCopy {
     cudaEvent_t ev = nullptr;  // the copy into this host buffer completed
   };
+  // apply_output_delta may run on another host thread than the frame / copy
+  // calls (a host buffer is handed over by the caller: copy k, then apply k)
+  std::mutex delta_mu_;                             // guards delta_host_
   std::map<const void*, DeltaCopy> delta_host_;     // host buffer -> its last copy
-  size_t delta_recent_[4] = {0, 0, 0, 0};           // bytes in use of the last applied deltas
-  int delta_seen_ = 0;
+  std::atomic<size_t> delta_recent_[4] = {0, 0, 0, 0};  // bytes in use of the last applied deltas
+  std::atomic<int> delta_seen_{0};
   size_t delta_dma_last_ = 0;
   DevBuf out_stage_[2];
   cudaEvent_t ev_staged_[2] = {nullptr, nullptr}, ev_drained_[2] = {nullptr, nullptr};
