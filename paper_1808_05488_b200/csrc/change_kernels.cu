@@ -609,23 +609,6 @@ __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListAr
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
   int nch = 0;
-  // output list (identity-window layers): a warp buffers its entries in shared
-  // memory; at the end one atomicAdd per CTA places them (a full buffer is
-  // placed early with one atomicAdd of its own)
-  constexpr int kEmitCap = 256;
-  __shared__ int32_t s_emit[kFrameThreads / 32][kEmitCap];
-  int32_t* wbuf = s_emit[warp];
-  int nbuf = 0;  // warp-uniform
-  int32_t* out_idx = a.out_idx ? a.out_idx + static_cast<long long>(s) * HW : nullptr;
-  auto flush = [&]() {
-    __syncwarp();
-    int b = 0;
-    if (lane == 0) b = atomicAdd(a.out_count + s * a.cnt_stride, nbuf);
-    b = __shfl_sync(0xffffffffu, b, 0);
-    for (int j = lane; j < nbuf; j += 32) out_idx[b + j] = wbuf[j];
-    __syncwarp();
-    nbuf = 0;
-  };
 
   const long long step = static_cast<long long>(gridDim.x) * wpb * gpw;
   const long long base0 = (static_cast<long long>(blockIdx.x) * wpb + warp) * gpw;
@@ -699,35 +682,6 @@ __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListAr
       map_set(m, p, a.W);
       ++nch;
     }
-    if (out_idx) {
-      const bool e = active && (any || boot) && sub == 0;
-      const uint32_t em = __ballot_sync(0xffffffffu, e);
-      const int k = __popc(em);
-      if (nbuf + k > kEmitCap) flush();
-      if (e) {
-        wbuf[nbuf + __popc(em & ((1u << lane) - 1u))] = static_cast<int32_t>(p);
-        if (boot) map_set(m, p, a.W);
-      }
-      nbuf += k;
-    }
-  }
-  if (out_idx) {  // block-uniform
-    __shared__ int s_wbase[kFrameThreads / 32];
-    if (lane == 0) s_wbase[warp] = nbuf;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      int tot = 0;
-      for (int w = 0; w < wpb; ++w) {
-        const int c = s_wbase[w];
-        s_wbase[w] = tot;
-        tot += c;
-      }
-      const int b = tot ? atomicAdd(a.out_count + s * a.cnt_stride, tot) : 0;
-      for (int w = 0; w < wpb; ++w) s_wbase[w] += b;
-    }
-    __syncthreads();
-    __syncwarp();
-    for (int j = lane; j < nbuf; j += 32) out_idx[s_wbase[warp] + j] = wbuf[j];
   }
   detect_count(a.det_count ? a.det_count + s * a.cnt_stride : nullptr, nch, boot, HW);
 }

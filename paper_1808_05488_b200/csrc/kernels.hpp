@@ -94,11 +94,6 @@ struct DetectListArgs {
   uint32_t* split;
   int32_t* split_e;          // [2][S] exponent of the whole copy, by frame parity
   const float* amax_in;      // [S] the GEMM's operand bound
-  // identity-window consumer (1x1 / stride 1 / pad 0): the detect also emits the
-  // output list (nullable; order: per warp in walk order) and, on boot frames,
-  // the full map, so no compaction runs for the layer
-  int32_t* out_idx;          // [S][H*W]
-  int32_t* out_count;        // [s * cnt_stride], atomic
 };
 void launch_detect_list(const DetectListArgs& a, cudaStream_t st);
 

@@ -631,16 +631,7 @@ void Net::build() {
         r.inmap_words = static_cast<size_t>(S_) * map_words_of(d.Hi, d.Wi);
         r.inmap_plain = d.inputs[0] < 0 && detect_frame_plain_map(d.Ci, r.Csi, d.Wi, r.state_chw ? 1 : 0);
         clear_off.push_back({i, clear_words});
-        clear_words += ((r.inmap_words + 3) & ~static_cast<size_t>(3)) + 4;  // 16-B aligned, 16 B of slack
-        // identity window (1x1, stride 1, no padding) after an in-network
-        // producer: the output map is the detected map, so the detect kernel
-        // can emit the list itself and no compaction runs (CBG_DETECT_LIST=1;
-        // measured: -17 us of compaction, +11 us in the two detects and the
-        // unordered list, bench 65.3k -> 64.1k)
-        const char* dl_env = std::getenv("CBG_DETECT_LIST");
-        r.list_in_detect = dl_env && std::atoi(dl_env) != 0 && !reuse && d.inputs[0] >= 0 &&
-                           nodes_[d.inputs[0]].d.kind != kExternal && c.kernel_h == 1 && c.kernel_w == 1 &&
-                           c.stride == 1 && c.padding == 0 && d.H == d.Hi && d.W == d.Wi;
+        clear_words += (r.inmap_words + 3) & ~static_cast<size_t>(3);  // 16-B aligned
         // the direct 3xFP16 GEMM of a k x k layer (k > 1) gathers every input value
         // k^2 times: its detect keeps the state pre-split, once per changed pixel
         const char* ps_env = std::getenv("CBG_PRESPLIT");  // read per build: A/B in one process
@@ -653,7 +644,7 @@ void Net::build() {
           CK(cudaStreamSynchronize(nullptr));
         }
       }
-      if (!reuse && !r.list_in_detect && (d.policy == CBG_POLICY_DETECT || d.policy == CBG_POLICY_PROPAGATE))
+      if (!reuse && (d.policy == CBG_POLICY_DETECT || d.policy == CBG_POLICY_PROPAGATE))
         r.dc = dc_geometry(d.Hi, d.Wi, d.H, d.W, c.kernel_h, c.kernel_w, c.stride, c.padding, S_);
       // worst-case map buffers (record_worst_case, layers.cpp:108-117)
       if (d.inputs[0] >= 0) {
@@ -688,15 +679,6 @@ void Net::build() {
   if (clear_words) {
     clear_.alloc(clear_words * 4);
     for (auto& [i, off] : clear_off) nodes_[i].inmap = clear_.as<uint32_t>() + off;
-  }
-  for (int i = 0; i < n; ++i) {  // detect-listed layers' maps, and the Reuse1x1 aliases of them
-    NodeRT& r = nodes_[i];
-    if (r.list_in_detect) {
-      r.outmap_own = DevBuf();
-      r.outmap = r.inmap;
-    } else if (r.d.kind == CBG_LAYER_CONV && r.d.policy == CBG_POLICY_REUSE1X1) {
-      r.outmap = nodes_[r.d.inputs[0]].outmap;
-    }
   }
   frame_.alloc(static_cast<size_t>(S_) * topo_.C * topo_.H * topo_.W * sizeof(float));
   frame_slot_.alloc(sizeof(void*));
@@ -748,7 +730,7 @@ int Net::launch_count(unsigned flags) const {
     const NodeDesc& d = r.d;
     if (d.kind == kExternal) continue;
     if (d.kind == CBG_LAYER_CONV) {
-      k += (d.policy == CBG_POLICY_DETECT) + (d.policy != CBG_POLICY_REUSE1X1 && !r.list_in_detect) + 1;
+      k += (d.policy == CBG_POLICY_DETECT) + (d.policy != CBG_POLICY_REUSE1X1) + 1;
       if ((flags & CBG_FWD_RECORD_WORST_CASE) && d.inputs[0] >= 0) k += 1;
     } else {
       k += r.fused_into >= 0 ? 1 : 2;
@@ -859,18 +841,14 @@ void Net::enqueue_frame(unsigned flags, bool u8, bool bcast, int slot8, bool s8)
                            taus_.as<float>() + static_cast<size_t>(i) * S_,
                            topo_.mode == CBG_MODE_CLOSEDLOOP, cnt_stride_,
                            r.split.bytes ? r.split.as<uint32_t>() : nullptr, r.split_e.as<int32_t>(),
-                           amax_entry(amax_origin(src)),
-                           r.list_in_detect ? r.idx : nullptr,
-                           r.list_in_detect ? counts + r.count_slot : nullptr};
+                           amax_entry(amax_origin(src))};
           timed(d.name + ".detect", [&] { launch_detect_list(a, st); });
         }
         // ClosedLoop reads the state; FeedForward's state equals x after detection.
         column_src = r.state.as<float>();
-        if (!r.list_in_detect) {
-          const uint32_t* in[1] = {r.inmap};
-          const DilateCompactArgs dc = compaction(i, in, 1);
-          timed(d.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
-        }
+        const uint32_t* in[1] = {r.inmap};
+        const DilateCompactArgs dc = compaction(i, in, 1);
+        timed(d.name + ".dilcomp", [&] { launch_dilate_compact(dc, st); });
         done_map(i, st);
       } else if (d.policy == CBG_POLICY_PROPAGATE) {
         const uint32_t* in[1] = {prod->outmap};

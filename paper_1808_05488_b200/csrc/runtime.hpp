@@ -126,7 +126,6 @@ struct NodeRT {
   int count_slot = 0;            // index into Net::counts ([slot][S]): output list length
   int det_slot = -1;             // Detect policy: detected (pre-dilation) input pixels
   DilateCompactArgs dc{};        // geometry of this node's compaction (rows, bands, warps, smem)
-  bool list_in_detect = false;   // identity-window detect layer: its detect emits the list, map = inmap
   int pool_child = -1;           // 2x2/2 pool whose map and list this node's compaction also derives
   int fused_into = -1;           // pool: the producer whose compaction derives its map and list
   // worst-case map (record_worst_case)

@@ -329,17 +329,6 @@ def test_tma_gather4_a_path_for_1x1_layers(gpu, monkeypatch):
     run_pair(spec, [0.05] * 5, frames_for(80, 112, noise=0.003))
 
 
-def test_detect_emitted_list_for_1x1_layers(gpu, monkeypatch):
-    """The experimental list path of identity-window layers (CBG_DETECT_LIST=1):
-    the 1x1 layers' detect kernels emit the output list (warp-buffered, in walk
-    order) and the full map on boot frames, with no compaction launch (DESIGN.md
-    §8.29; slower on the bench, kept off by default). Outputs and change maps
-    as the reference's, through the bootstrap frame and sparse frames."""
-    monkeypatch.setenv("CBG_DETECT_LIST", "1")
-    spec = cbi.make_seg_spec(9, 80, 112)
-    run_pair(spec, [0.05] * 5, frames_for(80, 112, noise=0.003))
-
-
 def test_detached_output_copy_pipelines(gpu):
     """cbg_net_copy_output_detached: frame k's output lands in its own host
     buffer although frame k+1 (and k+2) were enqueued before anyone waited;
