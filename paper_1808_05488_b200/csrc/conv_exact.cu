@@ -102,9 +102,24 @@ __global__ void __maxnreg__(88) conv_exact_kernel(ConvExactArgs a) {  // launche
   __shared__ int s_prefix[kMaxStreams + 1];
   const int og = blockIdx.y;  // output-channel group
   const int K = a.Cin * a.kh * KW;
-  for (int i = threadIdx.x; i < K * G; i += blockDim.x) {
-    const int r = i / G, o = og * G + (i - r * G);
-    sw[i] = o < a.Cout ? a.w[static_cast<long long>(o) * K + r] : 0.0f;  // weights [Cout][K] row-major
+  // weights [Cout][K] row-major -> [K][G]: all of a thread's loads first (one
+  // memory latency per CTA, not one per element)
+  {
+    constexpr int kU = 8;
+    for (int i0 = 0; i0 < K * G; i0 += kU * kThreads) {
+      float v[kU];
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kThreads + threadIdx.x;
+        const int r = i / G, o = og * G + (i - r * G);
+        v[u] = (i < K * G && o < a.Cout) ? __ldg(a.w + static_cast<long long>(o) * K + r) : 0.0f;
+      }
+#pragma unroll
+      for (int u = 0; u < kU; ++u) {
+        const int i = i0 + u * kThreads + threadIdx.x;
+        if (i < K * G) sw[i] = v[u];
+      }
+    }
   }
   if (threadIdx.x < 32) {  // block counts: ceil(count / (kThreads*kPix)) per stream, exclusive prefix
     const int lane = threadIdx.x;
