@@ -17,6 +17,8 @@
 #include <algorithm>
 #include <cstdio>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 
 #include "common.cuh"
 #include "kernels.hpp"
@@ -47,6 +49,36 @@ int sm_count() {
     return v;
   }();
   return n;
+}
+
+// CTAs per stream (grid.x) of a grid-stride kernel: enough for the work, and at
+// most two whole waves of the kernel's resident CTAs over all streams, so no
+// launch ends with a sliver of a wave on a few SMs (blocks_for's fixed 8 CTAs
+// per SM left 2.05 waves of the 8-bit detect at 64 streams: SMs idle 22% of
+// the launch). CBG_WAVE_GRID=0: blocks_for.
+template <class... Args>
+int wave_grid(void (*kernel)(Args...), int threads, long long work, int per_cta, int S, int legacy_mult) {
+  static const bool on = !(std::getenv("CBG_WAVE_GRID") && std::atoi(std::getenv("CBG_WAVE_GRID")) == 0);
+  if (!on) return legacy_mult * blocks_for(work, per_cta * legacy_mult, S, sm_count());
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int> occ_cache;
+  int occ = 0;
+  {
+    std::lock_guard<std::mutex> lk(mu);
+    const auto key = std::make_pair(reinterpret_cast<const void*>(kernel), threads);
+    auto it = occ_cache.find(key);
+    if (it == occ_cache.end()) {
+      if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kernel, threads, 0) != cudaSuccess || occ < 1) {
+        cudaGetLastError();
+        occ = 1;
+      }
+      it = occ_cache.emplace(key, occ).first;
+    }
+    occ = it->second;
+  }
+  const long long need = (work + per_cta - 1) / per_cta;
+  const long long cap = std::max(1LL, 2LL * occ * sm_count() / S);
+  return static_cast<int>(std::max(1LL, std::min(need, cap)));
 }
 
 // ---------------------------------------------------------------------------
@@ -1109,13 +1141,15 @@ void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
   const long long HW = static_cast<long long>(a.H) * a.W;
   if (a.x8_slot) {
     if (HW % 4 == 0 && (a.state_chw || a.Cs == 4)) {
-      dim3 grid(2 * blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
+      auto go = [&](auto kernel) {
+        dim3 grid(wave_grid(kernel, kFrameThreads, HW / 4, kFrameThreads, a.S, 2), a.S);
+        launch_k(kernel, grid, dim3(kFrameThreads), 0, st, a);
+      };
       if (a.state_chw && a.C == 3 && a.use_state8 && a.state8)
-        a.map_plain ? launch_k(detect_frame_s8_kernel<2, true>, grid, dim3(kFrameThreads), 0, st, a)
-                    : launch_k(detect_frame_s8_kernel<2, false>, grid, dim3(kFrameThreads), 0, st, a);
-      else if (a.state_chw && a.C == 3) launch_k(detect_frame_u8_kernel<true, 3>, grid, dim3(kFrameThreads), 0, st, a);
-      else if (a.state_chw) launch_k(detect_frame_u8_kernel<true, 0>, grid, dim3(kFrameThreads), 0, st, a);
-      else launch_k(detect_frame_u8_kernel<false, 0>, grid, dim3(kFrameThreads), 0, st, a);
+        a.map_plain ? go(detect_frame_s8_kernel<2, true>) : go(detect_frame_s8_kernel<2, false>);
+      else if (a.state_chw && a.C == 3) go(detect_frame_u8_kernel<true, 3>);
+      else if (a.state_chw) go(detect_frame_u8_kernel<true, 0>);
+      else go(detect_frame_u8_kernel<false, 0>);
     } else {
       dim3 grid(blocks_for(HW, kThreads, a.S, sm_count()), a.S);
       launch_k(detect_frame_u8_scalar_kernel, grid, dim3(kThreads), 0, st, a);
@@ -1124,7 +1158,7 @@ void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
   }
   if (a.state_chw) {
     if (a.C <= 4 && HW % 4 == 0) {
-      dim3 grid(2 * blocks_for(HW / 4, kThreads, a.S, sm_count()), a.S);
+      dim3 grid(wave_grid(detect_frame_chw_kernel, kFrameThreads, HW / 4, kFrameThreads, a.S, 2), a.S);
       launch_k(detect_frame_chw_kernel, grid, dim3(kFrameThreads), 0, st, a);
     } else {
       dim3 grid(blocks_for(HW, kThreads, a.S, sm_count()), a.S);
@@ -1143,11 +1177,14 @@ void launch_detect_list(const DetectListArgs& a, cudaStream_t st) {
   const int glog = group_log2(a.Cs);
   const long long HW = static_cast<long long>(a.H) * a.W;
   // 128-thread CTAs (<= 88 registers) co-reside with a persistent GEMM CTA
-  dim3 grid(2 * blocks_for(HW, kThreads >> glog, a.S, sm_count()), a.S);
   const int per_lane = (a.Cs / 4 + (1 << glog) - 1) >> glog;
-  if (per_lane <= 1) launch_k(detect_list_kernel<1>, grid, dim3(kFrameThreads), 0, st, a, glog);
-  else if (per_lane <= 2) launch_k(detect_list_kernel<2>, grid, dim3(kFrameThreads), 0, st, a, glog);
-  else launch_k(detect_list_kernel<4>, grid, dim3(kFrameThreads), 0, st, a, glog);
+  auto go = [&](auto kernel) {
+    dim3 grid(wave_grid(kernel, kFrameThreads, HW, kFrameThreads >> glog, a.S, 2), a.S);
+    launch_k(kernel, grid, dim3(kFrameThreads), 0, st, a, glog);
+  };
+  if (per_lane <= 1) go(detect_list_kernel<1>);
+  else if (per_lane <= 2) go(detect_list_kernel<2>);
+  else go(detect_list_kernel<4>);
 }
 
 bool dilate_compact_tiling(int Hin, int Win, int Hout, int Wout, int kh, int stride, int Wp, int* rows, int* bands,
@@ -1171,14 +1208,14 @@ void launch_dilate_compact(const DilateCompactArgs& a, cudaStream_t st) {
 void launch_pool(const PoolArgs& a, cudaStream_t st) {
   const int glog = group_log2(a.Cs);
   const long long HWo = static_cast<long long>(a.Hout) * a.Wout;
-  dim3 grid(2 * blocks_for(HWo, kThreads >> glog, a.S, sm_count()), a.S);
+  dim3 grid(wave_grid(pool_kernel, kFrameThreads, HWo, kFrameThreads >> glog, a.S, 2), a.S);
   launch_k(pool_kernel, grid, dim3(kFrameThreads), 0, st, a, glog);
 }
 
 void launch_upsample(const PoolArgs& a, cudaStream_t st) {
   const int glog = group_log2(a.Cs);
   const long long HWo = static_cast<long long>(a.Hout) * a.Wout;
-  dim3 grid(2 * blocks_for(HWo, kThreads >> glog, a.S, sm_count()), a.S);
+  dim3 grid(wave_grid(upsample_kernel, kFrameThreads, HWo, kFrameThreads >> glog, a.S, 2), a.S);
   launch_k(upsample_kernel, grid, dim3(kFrameThreads), 0, st, a, glog);
 }
 
