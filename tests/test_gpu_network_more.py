@@ -398,6 +398,41 @@ def test_output_delta_mirror_equals_full_output(gpu):
     np.testing.assert_array_equal(mirror, want)
 
 
+def test_output_delta_applied_on_another_thread(gpu):
+    """The e2e loop's pattern (bench.py run_e2e): frames and delta copies are
+    enqueued on one host thread while a background thread applies frame k - LAG
+    into the mirror; a host buffer is handed to a new copy only after its apply
+    returned (cbg.h). After the last apply the mirror equals the full output."""
+    from concurrent.futures import ThreadPoolExecutor
+    S, H, W, T, LAG = 4, 120, 160, 12, 2
+    spec = cbi.make_seg_spec(8, H, W)
+    frames = np.stack([cbi.gen_synthetic(cbi.SyntheticConfig(H, W, 3, T, 3, 12, 3, 4, 0.01, 90 + s))
+                       for s in range(S)], axis=1)
+    net = cbi.convert_to_cb(spec, [0.03] * 5, n_streams=S)
+    nbytes = net.output_bytes(-1)
+    bufs = [cbi.HostBuffer(net.output_delta_bytes(-1)) for _ in range(LAG + 1)]
+    mirror = np.zeros(nbytes // 4, np.float32)
+    pool = ThreadPoolExecutor(max_workers=1)
+    pending = {}
+    apply = lambda k: net.apply_output_delta(bufs[k % (LAG + 1)].ptr, mirror.ctypes.data)
+    for t in range(T):
+        if (t - LAG - 1) in pending:
+            pending.pop(t - LAG - 1).result()
+        net.enqueue(frames[t])
+        net.copy_output_delta(bufs[t % (LAG + 1)].ptr)
+        if t >= LAG:
+            pending[t - LAG] = pool.submit(apply, t - LAG)
+    for k in sorted(pending):
+        pending.pop(k).result()
+    for k in range(T - LAG, T):
+        apply(k)
+    pool.shutdown()
+    full = cbi.HostBuffer(nbytes, np.float32)
+    net.copy_output_async(full.ptr)
+    net.synchronize()
+    np.testing.assert_array_equal(mirror, full.array)
+
+
 @pytest.mark.parametrize("h,w,wd", [(1080, 1920, 8), (270, 480, 1)])
 def test_yolov3_leaky_upsample_against_port(gpu, h, w, wd):
     """BASELINE configs[3] with the features the reference lacks (network.hpp:10,
