@@ -460,6 +460,7 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_s8_kernel(Detec
   const long long n4 = HW >> 2;
   const long long stride = static_cast<long long>(gridDim.x) * blockDim.x;
   const int lane = threadIdx.x & 31;
+  const uint64_t pol = l2_stream_policy();
   float vmax = 0.0f;
   int nch = 0;
   for (long long q0 = static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x; q0 - lane < n4;
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(kFrameThreads, 8) detect_frame_s8_kernel(Detec
         const uint32_t* ssrc = reinterpret_cast<const uint32_t*>(s8 + 12 * q);
 #pragma unroll
         for (int i = 0; i < 3; ++i) {
-          wd[u][i] = __ldg(src + i);
+          wd[u][i] = ldg_stream_u32(src + i, pol);
           sw[u][i] = boot ? 0u : ssrc[i];
         }
       }
@@ -640,6 +641,7 @@ __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListAr
   const unsigned gmask = (g == 32 ? 0xffffffffu : ((1u << g) - 1u)) << ((lane >> glog) * g);
   const bool write_all = boot || !a.closed_loop;
   const float tau = a.tau[s];
+  const uint64_t pol = l2_stream_policy();
   int nch = 0;
 
   const long long step = static_cast<long long>(gridDim.x) * wpb * gpw;
@@ -669,7 +671,7 @@ __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListAr
       for (int j = 0; j < kCache; ++j) {
         const int v = sub + j * g;
         if (v < nv) {
-          xc[j] = ldg_nc_f4(xp + 4 * v);
+          xc[j] = ldg_stream_f4(xp + 4 * v, pol);
           if (!boot) sc[j] = *reinterpret_cast<const float4*>(sp + 4 * v);
         }
       }
@@ -684,7 +686,7 @@ __global__ void __launch_bounds__(kFrameThreads) detect_list_kernel(DetectListAr
           }
         }
         for (int v = sub + kCache * g; v < nv; v += g) {  // wide pixels beyond the cache
-          const float4 xv = ldg_nc_f4(xp + 4 * v);
+          const float4 xv = ldg_stream_f4(xp + 4 * v, pol);
           const float4 sv = *reinterpret_cast<const float4*>(sp + 4 * v);
           changed |= fabsf(xv.x - sv.x) > tau;
           changed |= fabsf(xv.y - sv.y) > tau;
@@ -938,6 +940,7 @@ __global__ void __launch_bounds__(kFrameThreads) pool_kernel(PoolArgs a, int glo
   const int sub = threadIdx.x & (g - 1);
   const long long gid = (static_cast<long long>(blockIdx.x) * blockDim.x + threadIdx.x) >> glog;
   const long long gstride = (static_cast<long long>(gridDim.x) * blockDim.x) >> glog;
+  const uint64_t pol = l2_stream_policy();
   const int nv = a.Cs >> 2;
   for (long long k = gid; k < n; k += gstride) {
     const int p = list[k];
@@ -948,8 +951,8 @@ __global__ void __launch_bounds__(kFrameThreads) pool_kernel(PoolArgs a, int glo
       const float* q0 = x + (static_cast<long long>(j0) * a.Win + i0) * a.Cs;
       const float* q1 = q0 + static_cast<long long>(a.Win) * a.Cs;
       for (int v = sub; v < nv; v += g) {
-        const float4 u00 = ldg_nc_f4(q0 + 4 * v), u01 = ldg_nc_f4(q0 + a.Cs + 4 * v);
-        const float4 u10 = ldg_nc_f4(q1 + 4 * v), u11 = ldg_nc_f4(q1 + a.Cs + 4 * v);
+        const float4 u00 = ldg_stream_f4(q0 + 4 * v, pol), u01 = ldg_stream_f4(q0 + a.Cs + 4 * v, pol);
+        const float4 u10 = ldg_stream_f4(q1 + 4 * v, pol), u11 = ldg_stream_f4(q1 + a.Cs + 4 * v, pol);
         float4 m = u00;  // the reference's order: start at (j0, i0), then the window row-major
         const float4* us[4] = {&u00, &u01, &u10, &u11};
 #pragma unroll

@@ -60,6 +60,41 @@ CBG_DEV void warp_amax(float* dst, float v) {
   if ((threadIdx.x & 31) == 0 && dst != nullptr && v > 0.0f) atomicMax(reinterpret_cast<int*>(dst), __float_as_int(v));
 }
 
+// Streaming reads (data read once per frame: frame bytes, a producer's output
+// in its consumer's detect or pool): L2 evict-first, so they do not push the
+// GEMMs' gathered rows and weight images out of L2 (CBG_EVICT_FIRST=0: plain)
+#ifndef CBG_EVICT_FIRST
+#define CBG_EVICT_FIRST 1
+#endif
+CBG_DEV uint64_t l2_stream_policy() {
+  uint64_t p = 0;
+#if CBG_EVICT_FIRST
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+#endif
+  return p;
+}
+CBG_DEV float4 ldg_stream_f4(const float* ptr, uint64_t pol) {
+  float4 r;
+#if CBG_EVICT_FIRST
+  asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(ptr), "l"(pol));
+#else
+  (void)pol;
+  asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(ptr));
+#endif
+  return r;
+}
+CBG_DEV uint32_t ldg_stream_u32(const uint32_t* ptr, uint64_t pol) {
+  uint32_t r;
+#if CBG_EVICT_FIRST
+  asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(ptr), "l"(pol));
+#else
+  (void)pol;
+  r = __ldg(ptr);
+#endif
+  return r;
+}
 CBG_DEV float4 ldg_nc_f4(const float* p) {
   float4 r;
   asm volatile("ld.global.nc.v4.f32 {%0, %1, %2, %3}, [%4];"
