@@ -52,13 +52,15 @@ int sm_count() {
 }
 
 // CTAs per stream (grid.x) of a grid-stride kernel: enough for the work, and at
-// most two whole waves of the kernel's resident CTAs over all streams, so no
-// launch ends with a sliver of a wave on a few SMs (blocks_for's fixed 8 CTAs
-// per SM left 2.05 waves of the 8-bit detect at 64 streams: SMs idle 22% of
-// the launch). CBG_WAVE_GRID=0: blocks_for.
+// most one whole wave of the kernel's resident CTAs over all streams (CBG_WAVES
+// = n: n waves), so no launch ends with a sliver of a wave on a few SMs
+// (blocks_for's fixed 8 CTAs per SM left 2.05 waves of the 8-bit detect at 64
+// streams: SMs idle 22% of the launch) and each thread's iterations even out.
+// CBG_WAVE_GRID=0: blocks_for.
 template <class... Args>
 int wave_grid(void (*kernel)(Args...), int threads, long long work, int per_cta, int S, int legacy_mult) {
   static const bool on = !(std::getenv("CBG_WAVE_GRID") && std::atoi(std::getenv("CBG_WAVE_GRID")) == 0);
+  static const int waves = std::getenv("CBG_WAVES") ? std::max(1, std::atoi(std::getenv("CBG_WAVES"))) : 1;
   if (!on) return legacy_mult * blocks_for(work, per_cta * legacy_mult, S, sm_count());
   static std::mutex mu;
   static std::map<std::pair<const void*, int>, int> occ_cache;
@@ -77,7 +79,7 @@ int wave_grid(void (*kernel)(Args...), int threads, long long work, int per_cta,
     occ = it->second;
   }
   const long long need = (work + per_cta - 1) / per_cta;
-  const long long cap = std::max(1LL, 2LL * occ * sm_count() / S);
+  const long long cap = std::max(1LL, static_cast<long long>(waves) * occ * sm_count() / S);
   return static_cast<int>(std::max(1LL, std::min(need, cap)));
 }
 
