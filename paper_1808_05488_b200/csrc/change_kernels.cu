@@ -1179,7 +1179,11 @@ void launch_detect_frame(const DetectFrameArgs& a, cudaStream_t st) {
 }
 
 void launch_detect_list(const DetectListArgs& a, cudaStream_t st) {
-  const int glog = group_log2(a.Cs);
+  // lanes per pixel: two float4 of x per lane (more pixels per warp, loads in
+  // flight per lane doubled) where the pixel has >= 8 of them (CBG_DETECT_PER_LANE=1: one)
+  static const int per = std::getenv("CBG_DETECT_PER_LANE") ? std::max(1, std::atoi(std::getenv("CBG_DETECT_PER_LANE"))) : 2;
+  int glog = group_log2(a.Cs);
+  while (glog > 0 && (a.Cs / 4) / (1 << glog) < per) --glog;
   const long long HW = static_cast<long long>(a.H) * a.W;
   // 128-thread CTAs (<= 88 registers) co-reside with a persistent GEMM CTA
   const int per_lane = (a.Cs / 4 + (1 << glog) - 1) >> glog;
