@@ -1200,8 +1200,10 @@ bool dilate_compact_tiling(int Hin, int Win, int Hout, int Wout, int kh, int str
                            int* threads, int* smem_bytes) {
   (void)Hin, (void)Win, (void)kh, (void)stride;
   const int nwo = (Wout + 31) / 32;
-  // ~256 output words (threads) per band, an even number of rows (a fused pool's rows stay inside a band)
-  int r = std::max(2, std::min(64, 256 / std::max(1, nwo))) & ~1;
+  // ~128 output words (threads) per band (CBG_DC_THREADS; 256: 1.5 us more per
+  // 64-stream frame, 512: +2.5), an even number of rows (a fused pool's rows stay inside a band)
+  static const int target = std::getenv("CBG_DC_THREADS") ? std::max(32, std::atoi(std::getenv("CBG_DC_THREADS"))) : 128;
+  int r = std::max(2, std::min(64, target / std::max(1, nwo))) & ~1;
   r = std::min(r, Hout + (Hout & 1));
   *rows = r;
   *bands = (Hout + r - 1) / r;
